@@ -1,0 +1,163 @@
+/*
+ * cycheck_b200.h — C ABI of the B200-native MAP accepting-cycle engine.
+ *
+ * Drop-in boundary for the reference's MAP hot path
+ * (/root/reference/proj/include/cycheck/{graph,map_engine}.hpp). The
+ * reference exposes a C++ value API with exceptions; this ABI uses opaque
+ * handles, plain pointers, sizes and status codes. Every pointer argument
+ * may be host memory (pageable or pinned) or device memory of the context's
+ * GPU; the library detects which and copies host data inside the call.
+ *
+ * Status codes map onto the reference's exceptions (errors.hpp:10-22):
+ *   CYC_E_CONTRACT  -> cycheck::ContractError      (precondition broken)
+ *   CYC_E_RESOURCE  -> cycheck::ResourceLimitError (capacity / device OOM)
+ *   CYC_E_CUDA      -> runtime failure (CUDA / NCCL error)
+ * cyc_last_error() returns the calling thread's last message.
+ *
+ * Conventions (reference types.hpp:9, map_engine.hpp:16-29, bitset.hpp:12-72):
+ *   vertex ids are uint32_t; map values are codes id+1 with 0 = NIL;
+ *   vertex sets are uint64_t words, bit v in word v>>6, tail bits zero.
+ *   Limits of this engine: n < 2^31, snapshot edges m < 2^32.
+ */
+#ifndef CYCHECK_B200_H
+#define CYCHECK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum cyc_status {
+  CYC_OK = 0,
+  CYC_E_CONTRACT = 1,
+  CYC_E_RESOURCE = 2,
+  CYC_E_CUDA = 3,
+  CYC_E_INVALID = 4
+} cyc_status;
+
+/* reference types.hpp:12 `enum class Orientation { forward, transposed }` */
+enum { CYC_FORWARD = 0, CYC_TRANSPOSED = 1 };
+
+/* Propagation step selection inside the device loop. */
+enum { CYC_MODE_AUTO = 0, CYC_MODE_PULL = 1, CYC_MODE_PUSH = 2 };
+
+typedef struct cyc_ctx cyc_ctx;
+typedef struct cyc_graph cyc_graph;
+
+/* reference map_engine.hpp:33-36 MapOptions {workers, early_exit}; `workers`
+ * has no meaning on the GPU (results are worker-count invariant). */
+typedef struct cyc_map_options {
+  int32_t early_exit;      /* default 1 */
+  int32_t mode;            /* CYC_MODE_* (default AUTO) */
+  uint64_t max_iterations; /* 0 = run to verdict (run_map); 1 = one fixpoint */
+  uint64_t max_steps;      /* 0 = unbounded; else stop the first fixpoint after k steps */
+  uint32_t push_alpha;     /* push when frontier edges * alpha < m (0 = default 16) */
+  uint32_t reserved;
+} cyc_map_options;
+
+/* reference map_engine.hpp:101-106 MapStats + types.hpp:18-27 Verdict, plus
+ * device-side evidence for the roofline. */
+typedef struct cyc_map_stats {
+  int32_t cycle_found;
+  uint32_t witness;            /* valid iff cycle_found (original ids if restricted) */
+  uint64_t iterations;
+  uint64_t kernel_calls;
+  uint64_t demoted_total;
+  uint64_t steps_last;         /* steps of the last fixpoint */
+  uint64_t pull_steps, push_steps;
+  uint64_t edges_touched;      /* sum over steps of edges read */
+  uint64_t rows_touched;       /* sum over steps of rows processed */
+  uint64_t algorithmic_bytes;  /* sum over steps of 8*E_s + 12*V_s */
+  double loop_ms;              /* device time of the loop kernel(s), CUDA events */
+  uint32_t grid_blocks, block_threads;
+} cyc_map_stats;
+
+/* ---- context ------------------------------------------------------------ */
+cyc_status cyc_ctx_create(int device, cyc_ctx** out);
+void cyc_ctx_destroy(cyc_ctx* ctx);
+const char* cyc_last_error(void);
+/* Number of kernels this process has launched through the library. */
+uint64_t cyc_launch_count(void);
+cyc_status cyc_ctx_synchronize(cyc_ctx* ctx);
+/* The CUDA stream (cudaStream_t) every call of this context is ordered on. */
+void* cyc_ctx_stream(cyc_ctx* ctx);
+
+/* ---- graph (reference graph.hpp:27-42 CsrSnapshot) ---------------------- */
+/* build_snapshot (graph.hpp:97-98, graph.cpp:63-105): edges = 2*m_log u32
+ * (src,dst) pairs of the logged prefix; acc_words = accepting flags of the n
+ * vertices (EdgeLog::accepting_prefix, graph.cpp:206-213), may be NULL.
+ * Duplicates are removed and rows sorted. Builds both the snapshot relation
+ * and its reverse (the MaxPropagation gather index, map_engine.cpp:9-19). */
+cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
+                           const uint64_t* acc_words, int orientation, cyc_graph** out);
+/* restrict_to_accepting_sccs (graph.hpp:103-114, graph.cpp:190-221). */
+cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out);
+void cyc_graph_destroy(cyc_graph* g);
+cyc_status cyc_graph_info(const cyc_graph* g, uint32_t* n, uint64_t* m, int* orientation,
+                          int* restricted);
+/* Copies out the snapshot CSR: row_offsets (n+1 u64), col_indices (m u32),
+ * accepting (ceil(n/64) u64), kept (n u32, restricted graphs only). Any
+ * pointer may be NULL. */
+cyc_status cyc_graph_export(const cyc_graph* g, uint64_t* row_offsets, uint32_t* col_indices,
+                            uint64_t* acc_words, uint32_t* kept);
+/* Copies out the gather index (reverse relation) in the same layout. */
+cyc_status cyc_graph_export_gather(const cyc_graph* g, uint64_t* row_offsets,
+                                   uint32_t* col_indices);
+
+/* ---- map engine (reference map_engine.hpp:50-112) ----------------------- */
+/* MaxPropagation::step (map_engine.cpp:21-79): out = step(x); witness =
+ * UINT32_MAX when none. acc_words NULL = the snapshot's accepting set. */
+cyc_status cyc_map_step(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
+                        const uint32_t* x, uint32_t* out, int32_t* changed, uint32_t* witness);
+/* fixpoint (map_engine.cpp:94-121). values: n codes (nullable). */
+cyc_status cyc_fixpoint(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
+                        const cyc_map_options* opt, uint32_t* values, uint64_t* steps,
+                        uint32_t* witness);
+/* demote (map_engine.cpp:123-137): remaining = F \ D (words), demoted = D
+ * ascending (capacity n, nullable); returns |D| in n_demoted. */
+cyc_status cyc_demote(cyc_ctx* ctx, const uint32_t* values, uint32_t n,
+                      const uint64_t* acc_words, uint64_t* remaining, uint32_t* demoted,
+                      uint64_t* n_demoted);
+/* run_map (map_engine.cpp:139-162). final_values (n codes, nullable) = the
+ * last fixpoint vector; iter_hash / iter_steps (nullable, capacity cap) =
+ * per-iteration vector hash (sum of splitmix64((v<<32)|x[v])) and steps. */
+cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
+                       const cyc_map_options* opt, cyc_map_stats* stats, uint32_t* final_values,
+                       uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap);
+
+/* ---- one-call pipeline: edge log -> verdict ----------------------------- */
+/* cycheck graph / explore final round (cycheck_main.cpp:88-97,
+ * explore.cpp:71-124): build_snapshot [+ restrict] + run_map. Timings in
+ * ms_out[4] = {h2d+build, restrict, loop, total} (nullable). */
+cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
+                     const uint64_t* acc_words, int orientation, int scc_restrict,
+                     const cyc_map_options* opt, cyc_map_stats* stats, double* ms_out);
+
+/* ---- synthetic inputs and buffers (bench / tests) ----------------------- */
+/* Generates a cyc_gen.h configuration's edge log and accepting words into
+ * device or host buffers (edges: 2*m u32, acc: ceil(n/64) u64). */
+cyc_status cyc_gen_fill(cyc_ctx* ctx, const void* gen_params, uint32_t* edges,
+                        uint64_t* acc_words);
+cyc_status cyc_gen_preset(int index, void* gen_params);
+cyc_status cyc_gen_prepare(void* gen_params);
+cyc_status cyc_host_alloc(size_t bytes, void** out);      /* pinned */
+void cyc_host_free(void* p);
+cyc_status cyc_device_alloc(cyc_ctx* ctx, size_t bytes, void** out);
+void cyc_device_free(cyc_ctx* ctx, void* p);
+cyc_status cyc_memcpy(cyc_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* Writes `bytes` of a scratch buffer to evict L2 (timing hygiene). */
+cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes);
+
+/* ---- multi-GPU row sharding (one process per GPU) ------------------------ */
+/* Edge-balanced contiguous row ranges, the reference's worker partition rule
+ * (map_engine.cpp:35-43): bounds[r] for r in [0, parts], computed on the
+ * host from gather row offsets (n+1 u64). */
+cyc_status cyc_shard_bounds(const uint64_t* row_offsets, uint32_t n, int parts, uint32_t* bounds);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CYCHECK_B200_H */

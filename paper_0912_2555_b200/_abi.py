@@ -1,0 +1,183 @@
+"""ctypes binding of the C ABI in include/cycheck_b200.h.
+
+The shared library is built in-tree (paper_0912_2555_b200/_lib/) by
+``__graft_entry__.build()``. There is no fallback: if the library is missing,
+importing this module raises, so nothing can silently run on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libcycheck_b200.so")
+
+
+class CycheckError(RuntimeError):
+    """Base of the errors raised across the C ABI."""
+
+
+class ContractError(CycheckError, ValueError):
+    """cycheck::ContractError (reference errors.hpp:10-14)."""
+
+
+class ResourceLimitError(CycheckError):
+    """cycheck::ResourceLimitError (reference errors.hpp:16-20), incl. device OOM."""
+
+
+class CudaError(CycheckError):
+    """CUDA runtime failure inside the engine."""
+
+
+_ERRORS = {1: ContractError, 2: ResourceLimitError, 3: CudaError, 4: CycheckError}
+
+CYC_FORWARD, CYC_TRANSPOSED = 0, 1
+CYC_MODE_AUTO, CYC_MODE_PULL, CYC_MODE_PUSH = 0, 1, 2
+
+
+class MapOptionsC(C.Structure):
+    _fields_ = [
+        ("early_exit", C.c_int32),
+        ("mode", C.c_int32),
+        ("max_iterations", C.c_uint64),
+        ("max_steps", C.c_uint64),
+        ("push_alpha", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
+class MapStatsC(C.Structure):
+    _fields_ = [
+        ("cycle_found", C.c_int32),
+        ("witness", C.c_uint32),
+        ("iterations", C.c_uint64),
+        ("kernel_calls", C.c_uint64),
+        ("demoted_total", C.c_uint64),
+        ("steps_last", C.c_uint64),
+        ("pull_steps", C.c_uint64),
+        ("push_steps", C.c_uint64),
+        ("edges_touched", C.c_uint64),
+        ("rows_touched", C.c_uint64),
+        ("algorithmic_bytes", C.c_uint64),
+        ("loop_ms", C.c_double),
+        ("grid_blocks", C.c_uint32),
+        ("block_threads", C.c_uint32),
+    ]
+
+
+class GenParams(C.Structure):
+    """Mirror of cyc_gen_params (include/cyc_gen.h)."""
+
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("n", C.c_uint32),
+        ("m", C.c_uint64),
+        ("seed", C.c_uint64),
+        ("deg", C.c_uint32),
+        ("acc_thr", C.c_uint64),
+        ("L", C.c_uint32),
+        ("W", C.c_uint32),
+        ("S", C.c_uint32),
+        ("exit_all", C.c_uint32),
+        ("acc_all", C.c_uint32),
+        ("scale", C.c_uint32),
+        ("edgefactor", C.c_uint32),
+        ("thr_a", C.c_uint64),
+        ("thr_ab", C.c_uint64),
+        ("thr_abc", C.c_uint64),
+        ("perm_mul1", C.c_uint64),
+        ("perm_mul2", C.c_uint64),
+    ]
+
+
+_P = C.c_void_p
+_U32P = C.POINTER(C.c_uint32)
+_U64P = C.POINTER(C.c_uint64)
+
+_SIGS = {
+    "cyc_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "cyc_ctx_destroy": (None, [_P]),
+    "cyc_last_error": (C.c_char_p, []),
+    "cyc_launch_count": (C.c_uint64, []),
+    "cyc_ctx_synchronize": (C.c_int, [_P]),
+    "cyc_ctx_stream": (_P, [_P]),
+    "cyc_graph_build": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.POINTER(_P)]),
+    "cyc_graph_restrict": (C.c_int, [_P, _P, C.POINTER(_P)]),
+    "cyc_graph_destroy": (None, [_P]),
+    "cyc_graph_info": (C.c_int, [_P, _U32P, _U64P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "cyc_graph_export": (C.c_int, [_P, _P, _P, _P, _P]),
+    "cyc_graph_export_gather": (C.c_int, [_P, _P, _P]),
+    "cyc_map_step": (C.c_int, [_P, _P, _P, _P, _P, C.POINTER(C.c_int32), _U32P]),
+    "cyc_fixpoint": (C.c_int, [_P, _P, _P, C.POINTER(MapOptionsC), _P, _U64P, _U32P]),
+    "cyc_demote": (C.c_int, [_P, _P, C.c_uint32, _P, _P, _P, _U64P]),
+    "cyc_map_run": (C.c_int, [_P, _P, _P, C.POINTER(MapOptionsC), C.POINTER(MapStatsC), _P, _P, _P,
+                              C.c_uint64]),
+    "cyc_check": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.c_int,
+                            C.POINTER(MapOptionsC), C.POINTER(MapStatsC), C.POINTER(C.c_double)]),
+    "cyc_gen_fill": (C.c_int, [_P, C.POINTER(GenParams), _P, _P]),
+    "cyc_gen_preset": (C.c_int, [C.c_int, C.POINTER(GenParams)]),
+    "cyc_gen_prepare": (C.c_int, [C.POINTER(GenParams)]),
+    "cyc_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_P)]),
+    "cyc_host_free": (None, [_P]),
+    "cyc_device_alloc": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    "cyc_device_free": (None, [_P, _P]),
+    "cyc_memcpy": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "cyc_flush_l2": (C.c_int, [_P, C.c_size_t]),
+    "cyc_shard_bounds": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads the in-tree engine library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"B200 engine library missing at {LIB_PATH}; run __graft_entry__.build() "
+                "(there is no CPU fallback)"
+            )
+        lib_ = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib_, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib_
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().cyc_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, CycheckError)(msg)
+
+
+def ptr(a) -> C.c_void_p | None:
+    """Address of a numpy array, a torch tensor, or an int; None passes NULL."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return C.c_void_p(a)
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ContractError("array must be C-contiguous")
+        return C.c_void_p(a.ctypes.data)
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    raise TypeError(f"cannot pass {type(a)!r} across the C ABI")
+
+
+def preset(index: int) -> GenParams:
+    p = GenParams()
+    check(lib().cyc_gen_preset(index, C.byref(p)))
+    return p
+
+
+def prepare(p: GenParams) -> GenParams:
+    check(lib().cyc_gen_prepare(C.byref(p)))
+    return p

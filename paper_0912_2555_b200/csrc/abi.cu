@@ -1,0 +1,633 @@
+// abi.cu — the extern "C" boundary (include/cycheck_b200.h).
+//
+// Each entry point mirrors one reference operation (cited per function),
+// stages host inputs onto the context's stream, runs the device kernels and
+// copies results back. C++ exceptions never cross the ABI: they become
+// status codes plus a thread-local message (errors.hpp:10-22 mapping).
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cyc_gen.h"
+#include "map_run.cuh"
+#include "scc.cuh"
+
+std::atomic<uint64_t> cyc::g_launches{0};
+
+namespace {
+thread_local std::string g_err;
+}
+
+[[noreturn]] void cyc::throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  cyc_status code = e == cudaErrorMemoryAllocation ? CYC_E_RESOURCE : CYC_E_CUDA;
+  throw Error(code, std::string(cudaGetErrorName(e)) + " (" + cudaGetErrorString(e) + ") at " +
+                        what + " [" + file + ":" + std::to_string(line) + "]");
+}
+
+struct cyc_ctx {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  cyc::DevBuf flush;
+};
+
+struct cyc_graph {
+  cyc_ctx* ctx = nullptr;
+  int orientation = CYC_TRANSPOSED;
+  int restricted = 0;
+  cyc::DevCsr snap;  // the snapshot relation (rows as CsrSnapshot), push side
+  cyc::DevCsr gath;  // its reverse: the MaxPropagation gather index, pull side
+  cyc::DevBuf acc;   // u64 words
+  cyc::DevBuf kept;  // u32[n] original ids (restricted graphs)
+  cyc::RunWs ws;
+  uint32_t n() const { return gath.n; }
+};
+
+namespace {
+
+using cyc::DevBuf;
+using cyc::Error;
+
+template <class F>
+cyc_status guard(F&& f) {
+  try {
+    f();
+    return CYC_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return CYC_E_RESOURCE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CYC_E_CUDA;
+  }
+}
+
+void require(bool ok, cyc_status code, const char* msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Returns a device view of `p` (copying host data into tmp on stream s).
+template <class T>
+const T* stage_in(const T* p, size_t count, DevBuf& tmp, cudaStream_t s) {
+  if (!p || count == 0) return p;
+  if (is_device_ptr(p)) return p;
+  tmp.alloc(count * sizeof(T), s);
+  CYC_CUDA(cudaMemcpyAsync(tmp.p, p, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  return tmp.as<T>();
+}
+
+// Copies `count` items from device src to dst (host or device).
+template <class T>
+void copy_out(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (!dst || count == 0) return;
+  CYC_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDefault, s));
+}
+
+size_t acc_words64(uint32_t n) { return ((size_t)n + 63) / 64; }
+
+__global__ void k_trim_tail(uint64_t* w, uint32_t n) {
+  if (n & 63u) w[n >> 6] &= (1ull << (n & 63u)) - 1ull;
+}
+
+// Device copy of an accepting set (trimmed), from host/device words or zero.
+void load_acc(const uint64_t* words, uint32_t n, DevBuf& dst, cudaStream_t s) {
+  size_t nw = acc_words64(n);
+  dst.alloc((nw + 1) * 8, s);
+  CYC_CUDA(cudaMemsetAsync(dst.p, 0, (nw + 1) * 8, s));
+  if (words && nw) {
+    CYC_CUDA(cudaMemcpyAsync(dst.p, words, nw * 8, cudaMemcpyDefault, s));
+    k_trim_tail<<<1, 1, 0, s>>>(dst.as<uint64_t>(), n);
+    CYC_LAUNCHED();
+  }
+}
+
+__global__ void k_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+void export_offsets(const cyc::DevCsr& g, uint64_t* dst, cudaStream_t s) {
+  if (!dst) return;
+  DevBuf wide(((size_t)g.n + 1) * 8, s);
+  k_u32_to_u64<<<cyc::grid_for(g.n + 1ull, 256, 4), 256, 0, s>>>(g.o(), wide.as<uint64_t>(), g.n + 1ull);
+  CYC_LAUNCHED();
+  copy_out(dst, wide.as<uint64_t>(), (size_t)g.n + 1, s);
+  CYC_CUDA(cudaStreamSynchronize(s));
+}
+
+__global__ void k_gen(cyc_gen_params p, uint32_t* edges, uint64_t* acc, uint64_t nwords) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.m; i += stride) {
+    uint32_t a, b;
+    cyc_gen_edge(&p, i, &a, &b);
+    reinterpret_cast<uint2*>(edges)[i] = make_uint2(a, b);
+  }
+  if (acc) {
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+      uint64_t bits = 0;
+      for (uint32_t k = 0; k < 64; ++k) {
+        uint64_t v = w * 64 + k;
+        if (v < p.n && cyc_gen_accepting(&p, (uint32_t)v)) bits |= 1ull << k;
+      }
+      acc[w] = bits;
+    }
+  }
+}
+
+void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
+                 const uint64_t* acc_words, int orientation, cyc_graph* g) {
+  require(orientation == CYC_FORWARD || orientation == CYC_TRANSPOSED, CYC_E_CONTRACT,
+          "build_snapshot: bad orientation");
+  require(n < 0x80000000u, CYC_E_RESOURCE, "vertex count must be < 2^31");
+  require(m_log < 0xFFFFFFFFull, CYC_E_RESOURCE, "edge log prefix must be < 2^32");
+  require(m_log == 0 || edges, CYC_E_CONTRACT, "build_snapshot: null edge array");
+  cudaStream_t s = ctx->s;
+  DevBuf tmp_edges, err(16, s);
+  CYC_CUDA(cudaMemsetAsync(err.p, 0, 16, s));
+  const uint32_t* de = stage_in(edges, (size_t)m_log * 2, tmp_edges, s);
+  g->ctx = ctx;
+  g->orientation = orientation;
+  const int snap_key_dst = orientation == CYC_TRANSPOSED;
+  cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>());
+  cyc::build_csr(de, m_log, n, !snap_key_dst, s, g->gath, err.as<uint32_t>());
+  uint32_t herr = 0;
+  CYC_CUDA(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  require(herr == 0, CYC_E_CONTRACT, "build_snapshot: edge endpoint >= n (not interned)");
+  require(g->snap.m == g->gath.m, CYC_E_CUDA, "internal: snapshot/gather edge counts differ");
+  cyc::build_heavy(g->gath, 256, 1024, s);
+  load_acc(acc_words, n, g->acc, s);
+}
+
+void fill_stats(const cyc::RunOut& o, cyc_map_stats* st) {
+  if (!st) return;
+  std::memset(st, 0, sizeof *st);
+  st->cycle_found = (int32_t)o.res[cyc::kResCycle];
+  st->witness = (uint32_t)o.res[cyc::kResWitness];
+  st->iterations = o.res[cyc::kResIterations];
+  st->kernel_calls = o.res[cyc::kResKernelCalls];
+  st->demoted_total = o.res[cyc::kResDemoted];
+  st->steps_last = o.res[cyc::kResStepsLast];
+  st->pull_steps = o.res[cyc::kResPullSteps];
+  st->push_steps = o.res[cyc::kResPushSteps];
+  st->edges_touched = o.res[cyc::kResEdges];
+  st->rows_touched = o.res[cyc::kResRows];
+  st->algorithmic_bytes = o.res[cyc::kResBytes];
+  st->loop_ms = o.ms;
+  st->grid_blocks = o.grid;
+  st->block_threads = o.block;
+}
+
+cyc_map_options default_opts() {
+  cyc_map_options o;
+  std::memset(&o, 0, sizeof o);
+  o.early_exit = 1;
+  return o;
+}
+
+// Common body of fixpoint/run_map: loads F, launches the device loop.
+cyc::RunOut run_loop(cyc_ctx* ctx, cyc_graph* g, const uint64_t* acc_words,
+                     const cyc_map_options& o, uint64_t cap) {
+  cudaStream_t s = ctx->s;
+  const uint32_t n = g->n();
+  require(o.mode >= CYC_MODE_AUTO && o.mode <= CYC_MODE_PUSH, CYC_E_CONTRACT, "bad mode");
+  g->ws.ensure(n, s);
+  const size_t nw = acc_words64(n);
+  if (acc_words) {
+    CYC_CUDA(cudaMemcpyAsync(g->ws.F.p, acc_words, nw * 8, cudaMemcpyDefault, s));
+  } else {
+    CYC_CUDA(cudaMemcpyAsync(g->ws.F.p, g->acc.p, nw * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  if (nw) {
+    k_trim_tail<<<1, 1, 0, s>>>(g->ws.F.as<uint64_t>(), n);
+    CYC_LAUNCHED();
+  }
+  cyc::RunOut out;
+  cyc::launch_map_run(g->snap, g->gath, g->ws, o.early_exit != 0, o.mode, o.max_iterations,
+                      o.max_steps, o.push_alpha, cap, s, ctx->e0, ctx->e1, out);
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cyc_last_error(void) { return g_err.c_str(); }
+uint64_t cyc_launch_count(void) { return cyc::g_launches.load(); }
+
+cyc_status cyc_ctx_create(int device, cyc_ctx** out) {
+  return guard([&] {
+    require(out != nullptr, CYC_E_CONTRACT, "null out");
+    int count = 0;
+    CYC_CUDA(cudaGetDeviceCount(&count));
+    require(device >= 0 && device < count, CYC_E_CONTRACT, "no such CUDA device");
+    CYC_CUDA(cudaSetDevice(device));
+    int major = 0, minor = 0;
+    CYC_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CYC_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    require(major == 10 && minor == 0, CYC_E_INVALID,
+            "this library is built for sm_100a (B200) only");
+    auto* c = new cyc_ctx;
+    c->device = device;
+    CYC_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    CYC_CUDA(cudaEventCreate(&c->e0));
+    CYC_CUDA(cudaEventCreate(&c->e1));
+    CYC_CUDA(cudaEventCreate(&c->e2));
+    CYC_CUDA(cudaEventCreate(&c->e3));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+  });
+}
+
+void cyc_ctx_destroy(cyc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  ctx->flush.release();
+  cudaStreamSynchronize(ctx->s);
+  cudaEventDestroy(ctx->e0);
+  cudaEventDestroy(ctx->e1);
+  cudaEventDestroy(ctx->e2);
+  cudaEventDestroy(ctx->e3);
+  cudaStreamDestroy(ctx->s);
+  delete ctx;
+}
+
+cyc_status cyc_ctx_synchronize(cyc_ctx* ctx) {
+  return guard([&] { CYC_CUDA(cudaStreamSynchronize(ctx->s)); });
+}
+
+void* cyc_ctx_stream(cyc_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
+
+cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
+                           const uint64_t* acc_words, int orientation, cyc_graph** out) {
+  return guard([&] {
+    require(ctx && out, CYC_E_CONTRACT, "null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    auto* g = new cyc_graph;
+    try {
+      build_graph(ctx, edges, m_log, n, acc_words, orientation, g);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out) {
+  return guard([&] {
+    require(ctx && in && out, CYC_E_CONTRACT, "null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    auto* g = new cyc_graph;
+    try {
+      g->ctx = ctx;
+      g->orientation = in->orientation;
+      g->restricted = 1;
+      cyc::restrict_graph(in->snap, in->gath, in->acc.as<uint64_t>(), ctx->s, g->snap, g->gath,
+                          g->acc, g->kept);
+      cyc::build_heavy(g->gath, 256, 1024, ctx->s);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+void cyc_graph_destroy(cyc_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->ctx->device);
+  delete g;
+}
+
+cyc_status cyc_graph_info(const cyc_graph* g, uint32_t* n, uint64_t* m, int* orientation,
+                          int* restricted) {
+  return guard([&] {
+    require(g, CYC_E_CONTRACT, "null graph");
+    if (n) *n = g->n();
+    if (m) *m = g->snap.m;
+    if (orientation) *orientation = g->orientation;
+    if (restricted) *restricted = g->restricted;
+  });
+}
+
+cyc_status cyc_graph_export(const cyc_graph* g, uint64_t* row_offsets, uint32_t* col_indices,
+                            uint64_t* acc_words, uint32_t* kept) {
+  return guard([&] {
+    require(g, CYC_E_CONTRACT, "null graph");
+    cudaStream_t s = g->ctx->s;
+    export_offsets(g->snap, row_offsets, s);
+    copy_out(col_indices, g->snap.c(), g->snap.m, s);
+    copy_out(acc_words, g->acc.as<uint64_t>(), acc_words64(g->n()), s);
+    if (g->restricted) copy_out(kept, g->kept.as<uint32_t>(), g->n(), s);
+    CYC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+cyc_status cyc_graph_export_gather(const cyc_graph* g, uint64_t* row_offsets,
+                                   uint32_t* col_indices) {
+  return guard([&] {
+    require(g, CYC_E_CONTRACT, "null graph");
+    cudaStream_t s = g->ctx->s;
+    export_offsets(g->gath, row_offsets, s);
+    copy_out(col_indices, g->gath.c(), g->gath.m, s);
+    CYC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+cyc_status cyc_map_step(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
+                        const uint32_t* x, uint32_t* out, int32_t* changed, uint32_t* witness) {
+  return guard([&] {
+    require(ctx && g && x && out, CYC_E_CONTRACT, "propagate_step: null argument");
+    cudaStream_t s = ctx->s;
+    const uint32_t n = g->n();
+    DevBuf tx, tacc, accb, dout, flags(16, s);
+    const uint32_t* dx = stage_in(x, n, tx, s);
+    const uint64_t* dacc = g->acc.as<uint64_t>();
+    if (acc_words) {
+      load_acc(acc_words, n, accb, s);
+      dacc = accb.as<uint64_t>();
+    }
+    uint32_t* dst = out;
+    const bool dev_out = is_device_ptr(out);
+    if (!dev_out) {
+      dout.alloc(((size_t)n + 1) * 4, s);
+      dst = dout.as<uint32_t>();
+    }
+    cyc::launch_step_pull(g->gath, dx, reinterpret_cast<const uint32_t*>(dacc), dst,
+                          flags.as<uint32_t>(), s);
+    if (!dev_out) copy_out(out, dst, n, s);
+    uint32_t hf[2];
+    CYC_CUDA(cudaMemcpyAsync(hf, flags.p, 8, cudaMemcpyDeviceToHost, s));
+    CYC_CUDA(cudaStreamSynchronize(s));
+    if (changed) *changed = (int32_t)hf[0];
+    if (witness) *witness = hf[1];
+  });
+}
+
+cyc_status cyc_fixpoint(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
+                        const cyc_map_options* opt, uint32_t* values, uint64_t* steps,
+                        uint32_t* witness) {
+  return guard([&] {
+    require(ctx && g, CYC_E_CONTRACT, "fixpoint: null argument");
+    cyc_map_options o = opt ? *opt : default_opts();
+    o.max_iterations = 1;
+    auto* gg = const_cast<cyc_graph*>(g);
+    cyc::RunOut r = run_loop(ctx, gg, acc_words, o, 0);
+    const uint32_t n = g->n();
+    // fixpoint from an empty accepting set still performs one step
+    // (map_engine.cpp:98-112); the device loop skips it (run_map semantics),
+    // so account for it here: x stays all-NIL and nothing changes.
+    uint64_t st = r.res[cyc::kResIterations] ? r.res[cyc::kResStepsLast] : 1;
+    if (steps) *steps = st;
+    if (witness) *witness = r.res[cyc::kResCycle] ? (uint32_t)r.res[cyc::kResWitness] : cyc::kNone;
+    if (values && n) {
+      if (r.res[cyc::kResIterations] == 0) {
+        CYC_CUDA(cudaMemsetAsync(gg->ws.P[0].p, 0, (size_t)n * 4, ctx->s));
+        r.res[cyc::kResCur] = 0;
+      }
+      if (is_device_ptr(values)) {
+        cyc::strip_codes(gg->ws, (int)r.res[cyc::kResCur], n, values, ctx->s);
+      } else {
+        DevBuf tmp((size_t)n * 4, ctx->s);
+        cyc::strip_codes(gg->ws, (int)r.res[cyc::kResCur], n, tmp.as<uint32_t>(), ctx->s);
+        copy_out(values, tmp.as<uint32_t>(), n, ctx->s);
+      }
+      CYC_CUDA(cudaStreamSynchronize(ctx->s));
+    }
+  });
+}
+
+cyc_status cyc_demote(cyc_ctx* ctx, const uint32_t* values, uint32_t n,
+                      const uint64_t* acc_words, uint64_t* remaining, uint32_t* demoted,
+                      uint64_t* n_demoted) {
+  return guard([&] {
+    require(ctx && (values || n == 0) && acc_words, CYC_E_CONTRACT, "demote: null argument");
+    cudaStream_t s = ctx->s;
+    DevBuf tx, accb, rem((acc_words64(n) + 1) * 8, s), dem(((size_t)n + 1) * 4, s);
+    const uint32_t* dx = stage_in(values, n, tx, s);
+    load_acc(acc_words, n, accb, s);
+    uint64_t nd = cyc::run_demote(dx, n, reinterpret_cast<const uint32_t*>(accb.p),
+                                  rem.as<uint32_t>(), demoted ? dem.as<uint32_t>() : nullptr, s);
+    copy_out(remaining, rem.as<uint64_t>(), acc_words64(n), s);
+    if (demoted) copy_out(demoted, dem.as<uint32_t>(), nd, s);
+    CYC_CUDA(cudaStreamSynchronize(s));
+    if (n_demoted) *n_demoted = nd;
+  });
+}
+
+cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
+                       const cyc_map_options* opt, cyc_map_stats* stats, uint32_t* final_values,
+                       uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap) {
+  return guard([&] {
+    require(ctx && g, CYC_E_CONTRACT, "run_map: null argument");
+    cyc_map_options o = opt ? *opt : default_opts();
+    auto* gg = const_cast<cyc_graph*>(g);
+    const uint64_t hcap = (iter_hash || iter_steps) ? cap : 0;
+    cyc::RunOut r = run_loop(ctx, gg, acc_words, o, hcap);
+    fill_stats(r, stats);
+    const uint32_t n = g->n();
+    if (stats && g->restricted && stats->cycle_found) {
+      uint32_t orig = 0;
+      CYC_CUDA(cudaMemcpyAsync(&orig, g->kept.as<uint32_t>() + stats->witness, 4,
+                               cudaMemcpyDeviceToHost, ctx->s));
+      CYC_CUDA(cudaStreamSynchronize(ctx->s));
+      stats->witness = orig;
+    }
+    if (final_values && n) {
+      if (r.res[cyc::kResIterations] == 0) {
+        CYC_CUDA(cudaMemsetAsync(gg->ws.P[0].p, 0, (size_t)n * 4, ctx->s));
+        r.res[cyc::kResCur] = 0;
+      }
+      if (is_device_ptr(final_values)) {
+        cyc::strip_codes(gg->ws, (int)r.res[cyc::kResCur], n, final_values, ctx->s);
+      } else {
+        DevBuf tmp((size_t)n * 4, ctx->s);
+        cyc::strip_codes(gg->ws, (int)r.res[cyc::kResCur], n, tmp.as<uint32_t>(), ctx->s);
+        copy_out(final_values, tmp.as<uint32_t>(), n, ctx->s);
+      }
+    }
+    const uint64_t rec = hcap < r.res[cyc::kResIterations] ? hcap : r.res[cyc::kResIterations];
+    if (iter_hash && rec) copy_out(iter_hash, (uint64_t*)gg->ws.hist.p, rec, ctx->s);
+    if (iter_steps && rec) copy_out(iter_steps, (uint64_t*)gg->ws.hist.p + hcap, rec, ctx->s);
+    CYC_CUDA(cudaStreamSynchronize(ctx->s));
+  });
+}
+
+cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
+                     const uint64_t* acc_words, int orientation, int scc_restrict,
+                     const cyc_map_options* opt, cyc_map_stats* stats, double* ms_out) {
+  return guard([&] {
+    require(ctx, CYC_E_CONTRACT, "null ctx");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    using clk = std::chrono::steady_clock;
+    auto t0 = clk::now();
+    cyc_graph base;
+    build_graph(ctx, edges, m_log, n, acc_words, orientation, &base);
+    auto t1 = clk::now();
+    cyc_graph restricted;
+    cyc_graph* run_on = &base;
+    if (scc_restrict) {
+      restricted.ctx = ctx;
+      restricted.orientation = orientation;
+      restricted.restricted = 1;
+      cyc::restrict_graph(base.snap, base.gath, base.acc.as<uint64_t>(), ctx->s, restricted.snap,
+                          restricted.gath, restricted.acc, restricted.kept);
+      cyc::build_heavy(restricted.gath, 256, 1024, ctx->s);
+      run_on = &restricted;
+    }
+    auto t2 = clk::now();
+    cyc_map_options o = opt ? *opt : default_opts();
+    cyc::RunOut r = run_loop(ctx, run_on, nullptr, o, 0);
+    fill_stats(r, stats);
+    if (stats && run_on->restricted && stats->cycle_found) {
+      uint32_t orig = 0;
+      CYC_CUDA(cudaMemcpyAsync(&orig, run_on->kept.as<uint32_t>() + stats->witness, 4,
+                               cudaMemcpyDeviceToHost, ctx->s));
+      CYC_CUDA(cudaStreamSynchronize(ctx->s));
+      stats->witness = orig;
+    }
+    auto t3 = clk::now();
+    if (ms_out) {
+      auto ms = [](clk::time_point a, clk::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+      };
+      ms_out[0] = ms(t0, t1);
+      ms_out[1] = ms(t1, t2);
+      ms_out[2] = ms(t2, t3);
+      ms_out[3] = ms(t0, t3);
+    }
+  });
+}
+
+cyc_status cyc_gen_preset(int index, void* gen_params) {
+  return guard([&] {
+    require(gen_params, CYC_E_CONTRACT, "null params");
+    require(cyc_gen_config(static_cast<cyc_gen_params*>(gen_params), index) == 0, CYC_E_CONTRACT,
+            "unknown generator config");
+  });
+}
+
+cyc_status cyc_gen_prepare(void* gen_params) {
+  return guard([&] {
+    require(gen_params, CYC_E_CONTRACT, "null params");
+    require(cyc_gen_init(static_cast<cyc_gen_params*>(gen_params)) == 0, CYC_E_CONTRACT,
+            "bad generator parameters");
+  });
+}
+
+cyc_status cyc_gen_fill(cyc_ctx* ctx, const void* gen_params, uint32_t* edges,
+                        uint64_t* acc_words) {
+  return guard([&] {
+    require(ctx && gen_params, CYC_E_CONTRACT, "null argument");
+    const cyc_gen_params p = *static_cast<const cyc_gen_params*>(gen_params);
+    cudaStream_t s = ctx->s;
+    const uint64_t nw = acc_words64(p.n);
+    DevBuf te, ta;
+    uint32_t* de = edges;
+    uint64_t* da = acc_words;
+    const bool dev_e = is_device_ptr(edges), dev_a = is_device_ptr(acc_words);
+    if (edges && !dev_e) {
+      te.alloc(p.m * 8 + 8, s);
+      de = te.as<uint32_t>();
+    }
+    if (acc_words && !dev_a) {
+      ta.alloc(nw * 8 + 8, s);
+      da = ta.as<uint64_t>();
+    }
+    cyc_gen_params q = p;
+    if (!edges) q.m = 0;
+    k_gen<<<cyc::grid_for(p.m > nw ? p.m : nw, 256, 16), 256, 0, s>>>(q, de, da, nw);
+    CYC_LAUNCHED();
+    if (edges && !dev_e) copy_out(edges, de, p.m * 2, s);
+    if (acc_words && !dev_a) copy_out(acc_words, da, nw, s);
+    CYC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+cyc_status cyc_host_alloc(size_t bytes, void** out) {
+  return guard([&] {
+    require(out, CYC_E_CONTRACT, "null out");
+    CYC_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+  });
+}
+
+void cyc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+cyc_status cyc_device_alloc(cyc_ctx* ctx, size_t bytes, void** out) {
+  return guard([&] {
+    require(ctx && out, CYC_E_CONTRACT, "null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      throw Error(CYC_E_RESOURCE, "device memory exhausted");
+    }
+    CYC_CUDA(e);
+  });
+}
+
+void cyc_device_free(cyc_ctx* ctx, void* p) {
+  if (!p) return;
+  if (ctx) cudaSetDevice(ctx->device);
+  cudaFree(p);
+}
+
+cyc_status cyc_memcpy(cyc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    require(ctx, CYC_E_CONTRACT, "null ctx");
+    CYC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->s));
+    CYC_CUDA(cudaStreamSynchronize(ctx->s));
+  });
+}
+
+cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes) {
+  return guard([&] {
+    require(ctx, CYC_E_CONTRACT, "null ctx");
+    if (ctx->flush.bytes < bytes) ctx->flush.alloc(bytes, ctx->s);
+    CYC_CUDA(cudaMemsetAsync(ctx->flush.p, (int)(cyc::g_launches.load() & 0xFF), bytes, ctx->s));
+  });
+}
+
+// map_engine.cpp:35-43: bounds[w] = lower_bound(offsets, total*w/parts).
+cyc_status cyc_shard_bounds(const uint64_t* row_offsets, uint32_t n, int parts, uint32_t* bounds) {
+  return guard([&] {
+    require(row_offsets && bounds && parts >= 1, CYC_E_CONTRACT, "shard_bounds: bad argument");
+    const uint64_t total = row_offsets[n];
+    bounds[0] = 0;
+    for (int w = 1; w < parts; ++w) {
+      uint64_t target = total * (uint64_t)w / (uint64_t)parts;
+      uint32_t lo = 0, hi = n + 1;  // first index with offsets[idx] >= target
+      while (lo < hi) {
+        uint32_t mid = lo + (hi - lo) / 2;
+        if (row_offsets[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      bounds[w] = lo < n ? lo : n;
+    }
+    bounds[parts] = n;
+  });
+}
+
+}  // extern "C"

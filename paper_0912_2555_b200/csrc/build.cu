@@ -1,0 +1,529 @@
+// build.cu — K1: device CSR construction from an edge log.
+//
+// Replaces build_snapshot (reference graph.cpp:63-105) and the gather-index
+// construction of MaxPropagation (map_engine.cpp:9-19). Both are
+// single-threaded counting sorts on the CPU; here the same three phases run
+// as HBM-bound kernels over the whole log:
+//   1. row histogram     (atomics, warp-aggregated with match_any for hubs)
+//   2. exclusive scan    (reduce-then-scan, 3 launches)
+//   3. bucket scatter    (atomic cursors counting down from row ends)
+//   4. per-row sort+dedup, by row-length class: registers (<=16), one CTA in
+//      shared memory (<=4096), one CTA with a shared-memory-tiled bitonic
+//      network over global memory (larger hub rows)
+//   5. scan of unique counts, compaction into the final CSR.
+// Row offsets are u32 (snapshot edges < 2^32; checked by the caller).
+#include "build.cuh"
+
+namespace cyc {
+
+namespace {
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr uint32_t kScanTile = kScanThreads * kScanItems;
+constexpr uint32_t kSmallRow = 16;
+constexpr uint32_t kMedRow = 4096;
+constexpr int kMedThreads = 256;
+constexpr uint32_t kBigTile = 4096;
+constexpr int kBigThreads = 1024;
+
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* total) {
+  __shared__ uint32_t warp_sums[THREADS / 32];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint32_t incl = warp_incl_scan(x);
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < THREADS / 32 ? warp_sums[lane] : 0u;
+    s = warp_incl_scan(s);
+    if (lane < THREADS / 32) warp_sums[lane] = s;
+  }
+  __syncthreads();
+  uint32_t base = wid ? warp_sums[wid - 1] : 0u;
+  *total = warp_sums[THREADS / 32 - 1];
+  __syncthreads();
+  return base + incl - x;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __restrict__ in,
+                                                               uint32_t n, uint32_t per_block,
+                                                               uint32_t* __restrict__ bsum) {
+  uint64_t lo = (uint64_t)blockIdx.x * per_block;
+  uint64_t hi = lo + per_block < n ? lo + per_block : n;
+  uint32_t s = 0;
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += kScanThreads) s += in[i];
+  s = __reduce_add_sync(kFull, s);
+  __shared__ uint32_t ws[kScanThreads / 32];
+  if ((threadIdx.x & 31u) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t t = threadIdx.x < kScanThreads / 32 ? ws[threadIdx.x] : 0u;
+    t = __reduce_add_sync(kFull, t);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* bsum, uint32_t nb, uint32_t* total) {
+  uint32_t x = threadIdx.x < nb ? bsum[threadIdx.x] : 0u;
+  uint32_t tot;
+  uint32_t ex = block_excl_scan<1024>(x, &tot);
+  if (threadIdx.x < nb) bsum[threadIdx.x] = ex;
+  if (threadIdx.x == 0 && total) *total = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* in, uint32_t* out,
+                                                             uint32_t n, uint32_t per_block,
+                                                             const uint32_t* __restrict__ bsum) {
+  uint64_t lo = (uint64_t)blockIdx.x * per_block;
+  uint64_t hi = lo + per_block < n ? lo + per_block : n;
+  uint32_t run = bsum[blockIdx.x];
+  for (uint64_t t0 = lo; t0 < hi; t0 += kScanTile) {
+    uint32_t v[kScanItems];
+    uint64_t base = t0 + (uint64_t)threadIdx.x * kScanItems;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      v[k] = base + k < hi ? in[base + k] : 0u;
+      s += v[k];
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan<kScanThreads>(s, &tot) + run;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      if (base + k < hi) out[base + k] = ex;
+      ex += v[k];
+    }
+    run += tot;
+  }
+}
+
+// ---------------------------------------------------------------- histogram
+__global__ void k_hist(const uint2* __restrict__ edges, uint64_t m, uint32_t n, int key_dst,
+                       uint32_t* __restrict__ cnt, uint32_t* __restrict__ err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < m; i0 += stride) {
+    uint64_t i = i0 + threadIdx.x;
+    uint32_t row = kNone;
+    if (i < m) {
+      uint2 e = edges[i];
+      if (e.x >= n || e.y >= n) {
+        *err = 1u;
+      } else {
+        row = key_dst ? e.y : e.x;
+      }
+    }
+    uint32_t peers = __match_any_sync(kFull, row);
+    if (row != kNone && (__ffs(peers) - 1) == (int)lane_id()) atomicAdd(cnt + row, __popc(peers));
+  }
+}
+
+// Counting-down cursors: cnt[row] starts at the row length.
+__global__ void k_scatter(const uint2* __restrict__ edges, uint64_t m, uint32_t n, int key_dst,
+                          const uint32_t* __restrict__ roff, uint32_t* __restrict__ cnt,
+                          uint32_t* __restrict__ raw) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < m; i0 += stride) {
+    uint64_t i = i0 + threadIdx.x;
+    uint32_t row = kNone, other = 0;
+    if (i < m) {
+      uint2 e = edges[i];
+      if (e.x < n && e.y < n) {
+        row = key_dst ? e.y : e.x;
+        other = key_dst ? e.x : e.y;
+      }
+    }
+    uint32_t peers = __match_any_sync(kFull, row);
+    if (row != kNone) {
+      int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (leader == (int)lane_id()) base = atomicSub(cnt + row, (uint32_t)__popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      uint32_t rank = __popc(peers & lanemask_lt());
+      raw[roff[row] + base - 1u - rank] = other;
+    }
+  }
+}
+
+// ------------------------------------------------------------ small rows
+template <int N>
+__device__ __forceinline__ void sort_net(uint32_t (&a)[N]) {
+  // bitonic network, ascending (N power of two)
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        int p = i ^ j;
+        if (p > i) {
+          bool up = (i & k) == 0;
+          uint32_t x = a[i], y = a[p];
+          if ((x > y) == up) {
+            a[i] = y;
+            a[p] = x;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t sort_small_row(uint32_t* __restrict__ seg, uint32_t d) {
+  uint32_t a[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = (uint32_t)i < d ? seg[i] : kNone;
+  sort_net<N>(a);
+  uint32_t k = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    if ((uint32_t)i < d && (i == 0 || a[i] != a[i - 1])) seg[k++] = a[i];
+  }
+  return k;
+}
+
+__global__ void k_sort_small(uint32_t n, const uint32_t* __restrict__ roff,
+                             uint32_t* __restrict__ raw, uint32_t* __restrict__ ucnt,
+                             uint32_t* __restrict__ med, uint32_t* __restrict__ big,
+                             uint32_t* __restrict__ counts /* [0]=med [1]=big */) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    uint32_t b = roff[v], d = roff[v + 1] - b;
+    uint32_t* seg = raw + b;
+    if (d <= 1) {
+      ucnt[v] = d;
+    } else if (d == 2) {
+      uint32_t x = seg[0], y = seg[1];
+      if (x == y) {
+        ucnt[v] = 1;
+      } else {
+        seg[0] = min(x, y);
+        seg[1] = max(x, y);
+        ucnt[v] = 2;
+      }
+    } else if (d <= 4) {
+      ucnt[v] = sort_small_row<4>(seg, d);
+    } else if (d <= 8) {
+      ucnt[v] = sort_small_row<8>(seg, d);
+    } else if (d <= kSmallRow) {
+      ucnt[v] = sort_small_row<16>(seg, d);
+    } else if (d <= kMedRow) {
+      med[atomicAdd(counts + 0, 1u)] = v;
+    } else {
+      big[atomicAdd(counts + 1, 1u)] = v;
+    }
+  }
+}
+
+// Block-wide dedup of a sorted shared-memory array s[0..d) into seg, returns
+// unique count (all threads).
+template <int THREADS>
+__device__ uint32_t block_unique_store(const uint32_t* s, uint32_t d, uint32_t prev_last,
+                                       bool has_prev, uint32_t* seg_out) {
+  // each thread handles a contiguous run of items
+  const uint32_t per = (d + THREADS - 1) / THREADS;
+  const uint32_t lo = threadIdx.x * per;
+  const uint32_t hi = min(d, lo + per);
+  uint32_t c = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    bool first = i == 0 ? !has_prev || s[0] != prev_last : s[i] != s[i - 1];
+    c += first;
+  }
+  uint32_t tot;
+  uint32_t pos = block_excl_scan<THREADS>(c, &tot);
+  for (uint32_t i = lo; i < hi; ++i) {
+    bool first = i == 0 ? !has_prev || s[0] != prev_last : s[i] != s[i - 1];
+    if (first) seg_out[pos++] = s[i];
+  }
+  return tot;
+}
+
+__device__ __forceinline__ void smem_bitonic(uint32_t* s, uint32_t P, int nthreads) {
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += nthreads) {
+        uint32_t p = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);
+        if (p > i) {
+          uint32_t x = s[i], y = s[p];
+          if (x > y) {
+            s[i] = y;
+            s[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kMedThreads) k_sort_med(const uint32_t* __restrict__ rows,
+                                                         const uint32_t* __restrict__ counts,
+                                                         const uint32_t* __restrict__ roff,
+                                                         uint32_t* __restrict__ raw,
+                                                         uint32_t* __restrict__ ucnt) {
+  __shared__ uint32_t s[kMedRow];
+  const uint32_t nrows = counts[0];
+  for (uint32_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const uint32_t v = rows[r];
+    const uint32_t b = roff[v], d = roff[v + 1] - b;
+    uint32_t P = 1;
+    while (P < d) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += kMedThreads) s[i] = i < d ? raw[b + i] : kNone;
+    __syncthreads();
+    smem_bitonic(s, P, kMedThreads);
+    uint32_t u = block_unique_store<kMedThreads>(s, d, 0, false, raw + b);
+    if (threadIdx.x == 0) ucnt[v] = u;
+    __syncthreads();
+  }
+}
+
+// Hub rows: bitonic network (all-ascending "flip" formulation, so virtual
+// +inf padding beyond d never moves) with every stage whose partner distance
+// is below kBigTile run inside a shared-memory tile.
+__device__ void big_tile_stages(uint32_t* s, uint32_t* g, uint32_t d, uint32_t t0, uint32_t kmax,
+                                bool from_start) {
+  // load tile
+  for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads)
+    s[i] = t0 + i < d ? g[t0 + i] : kNone;
+  __syncthreads();
+  if (from_start) {
+    smem_bitonic(s, kBigTile, kBigThreads);
+  } else {
+    // only the half-cleaner tail j = kBigTile/2 .. 1 of merge size kmax
+    (void)kmax;
+    for (uint32_t j = kBigTile >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads) {
+        uint32_t p = i ^ j;
+        if (p > i) {
+          uint32_t x = s[i], y = s[p];
+          if (x > y) {
+            s[i] = y;
+            s[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < kBigTile; i += kBigThreads)
+    if (t0 + i < d) g[t0 + i] = s[i];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_sort_big(const uint32_t* __restrict__ rows,
+                                                         const uint32_t* __restrict__ counts,
+                                                         const uint32_t* __restrict__ roff,
+                                                         uint32_t* __restrict__ raw,
+                                                         uint32_t* __restrict__ ucnt) {
+  __shared__ uint32_t s[kBigTile];
+  __shared__ uint32_t carry;
+  const uint32_t nrows = counts[1];
+  for (uint32_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const uint32_t v = rows[r];
+    const uint32_t b = roff[v], d = roff[v + 1] - b;
+    uint32_t* g = raw + b;
+    uint32_t P = kBigTile;
+    while (P < d) P <<= 1;
+    for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) big_tile_stages(s, g, d, t0, kBigTile, true);
+    for (uint32_t k = kBigTile << 1; k <= P; k <<= 1) {
+      for (uint32_t j = k >> 1; j >= kBigTile; j >>= 1) {
+        const bool flip = j == (k >> 1);
+        for (uint32_t i = threadIdx.x; i < d; i += kBigThreads) {
+          uint32_t p = flip ? (i ^ (k - 1)) : (i ^ j);
+          if (p > i && p < d) {
+            uint32_t x = g[i], y = g[p];
+            if (x > y) {
+              g[i] = y;
+              g[p] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) big_tile_stages(s, g, d, t0, k, false);
+    }
+    // dedup tile by tile (writes never overtake reads: output index <= input index)
+    uint32_t written = 0;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) {
+      uint32_t len = min(kBigTile, d - t0);
+      for (uint32_t i = threadIdx.x; i < len; i += kBigThreads) s[i] = g[t0 + i];
+      __syncthreads();
+      uint32_t prev = carry;
+      __syncthreads();
+      uint32_t u = block_unique_store<kBigThreads>(s, len, prev, t0 > 0, g + written);
+      if (threadIdx.x == 0) carry = s[len - 1];
+      written += u;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) ucnt[v] = written;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ compact
+__global__ void k_compact_small(uint32_t n, const uint32_t* __restrict__ roff,
+                                const uint32_t* __restrict__ off,
+                                const uint32_t* __restrict__ raw, uint32_t* __restrict__ col) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    uint32_t b = roff[v], d = roff[v + 1] - b;
+    if (d > kSmallRow) continue;
+    uint32_t o = off[v], u = off[v + 1] - o;
+    for (uint32_t i = 0; i < u; ++i) col[o + i] = raw[b + i];
+  }
+}
+
+__global__ void k_compact_list(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cnt,
+                               const uint32_t* __restrict__ roff, const uint32_t* __restrict__ off,
+                               const uint32_t* __restrict__ raw, uint32_t* __restrict__ col) {
+  const uint32_t nrows = *cnt;
+  for (uint32_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    uint32_t v = rows[r];
+    uint32_t b = roff[v], o = off[v], u = off[v + 1] - o;
+    for (uint32_t i = threadIdx.x; i < u; i += blockDim.x) col[o + i] = raw[b + i];
+  }
+}
+
+__global__ void k_heavy_chunks(uint32_t n, const uint32_t* __restrict__ off, uint32_t heavy,
+                               uint32_t chunk, uint4* __restrict__ out, uint32_t* __restrict__ cnt) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    uint32_t b = off[v], e = off[v + 1];
+    if (e - b <= heavy) continue;
+    uint32_t nc = (e - b + chunk - 1) / chunk;
+    uint32_t base = atomicAdd(cnt, nc);
+    for (uint32_t c = 0; c < nc; ++c) {
+      uint32_t cb = b + c * chunk;
+      out[base + c] = make_uint4(v, cb, min(e, cb + chunk), 0u);
+    }
+  }
+}
+
+__global__ void k_max_degree(uint32_t n, const uint32_t* __restrict__ off, uint32_t* out) {
+  uint32_t mx = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
+    mx = max(mx, off[v + 1] - off[v]);
+  mx = __reduce_max_sync(kFull, mx);
+  if ((threadIdx.x & 31u) == 0) atomicMax(out, mx);
+}
+
+}  // namespace
+
+int sm_count() {
+  static int c = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return c;
+}
+
+uint32_t grid_for(uint64_t items, int threads, int per_sm) {
+  uint64_t want = (items + threads - 1) / threads;
+  uint64_t cap = (uint64_t)sm_count() * per_sm;
+  if (want > cap) want = cap;
+  return want ? (uint32_t)want : 1u;
+}
+
+void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* total,
+                    cudaStream_t s, DevBuf& scratch) {
+  // out has n+1 entries; out[n] = total (also written to *total if non-null, device ptr)
+  uint32_t nb = div_up(n ? n : 1, kScanTile);
+  if (nb > 1024) nb = 1024;
+  uint32_t per_block = div_up(div_up(n ? n : 1, nb), kScanTile) * kScanTile;
+  nb = div_up(n ? n : 1, per_block);
+  if (scratch.bytes < (nb + 1) * sizeof(uint32_t)) scratch.alloc((nb + 1) * sizeof(uint32_t), s);
+  uint32_t* bsum = scratch.as<uint32_t>();
+  k_scan_reduce<<<nb, kScanThreads, 0, s>>>(in, n, per_block, bsum);
+  CYC_LAUNCHED();
+  k_scan_blocks<<<1, 1024, 0, s>>>(bsum, nb, out + n);
+  CYC_LAUNCHED();
+  k_scan_down<<<nb, kScanThreads, 0, s>>>(in, out, n, per_block, bsum);
+  CYC_LAUNCHED();
+  if (total) CYC_CUDA(cudaMemcpyAsync(total, out + n, 4, cudaMemcpyDeviceToDevice, s));
+}
+
+// Builds a deduplicated, row-sorted CSR keyed by one half of each logged pair.
+void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
+               DevCsr& out, uint32_t* d_err) {
+  out.n = n;
+  out.off.alloc(((size_t)n + 1) * 4, s);
+  DevBuf cnt(((size_t)n + 1) * 4, s), roff(((size_t)n + 1) * 4, s);
+  DevBuf raw((m_log ? m_log : 1) * 4, s), ucnt(((size_t)n + 1) * 4, s);
+  DevBuf lists(((size_t)n + 1) * 4 * 2, s), counts(16, s), scratch;
+  uint32_t* c = cnt.as<uint32_t>();
+  CYC_CUDA(cudaMemsetAsync(c, 0, ((size_t)n + 1) * 4, s));
+  CYC_CUDA(cudaMemsetAsync(counts.p, 0, 16, s));
+  const uint2* e2 = reinterpret_cast<const uint2*>(d_edges);
+  if (m_log) {
+    k_hist<<<grid_for(m_log, 256, 16), 256, 0, s>>>(e2, m_log, n, key_dst, c, d_err);
+    CYC_LAUNCHED();
+  }
+  exclusive_scan(c, roff.as<uint32_t>(), n, nullptr, s, scratch);
+  if (m_log) {
+    k_scatter<<<grid_for(m_log, 256, 16), 256, 0, s>>>(e2, m_log, n, key_dst, roff.as<uint32_t>(), c,
+                                                        raw.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
+  uint32_t* med = lists.as<uint32_t>();
+  uint32_t* big = med + n + 1;
+  uint32_t* cts = counts.as<uint32_t>();
+  if (n) {
+    k_sort_small<<<grid_for(n, 256, 16), 256, 0, s>>>(n, roff.as<uint32_t>(), raw.as<uint32_t>(),
+                                                       ucnt.as<uint32_t>(), med, big, cts);
+    CYC_LAUNCHED();
+    k_sort_med<<<sm_count() * 8, kMedThreads, 0, s>>>(med, cts, roff.as<uint32_t>(),
+                                                       raw.as<uint32_t>(), ucnt.as<uint32_t>());
+    CYC_LAUNCHED();
+    k_sort_big<<<sm_count(), kBigThreads, 0, s>>>(big, cts, roff.as<uint32_t>(), raw.as<uint32_t>(),
+                                                  ucnt.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
+  exclusive_scan(ucnt.as<uint32_t>(), out.off.as<uint32_t>(), n, nullptr, s, scratch);
+  uint32_t m = 0;
+  CYC_CUDA(cudaMemcpyAsync(&m, out.off.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  out.m = m;
+  out.col.alloc((m ? m : 1) * 4ull, s);
+  if (n) {
+    k_compact_small<<<grid_for(n, 256, 16), 256, 0, s>>>(n, roff.as<uint32_t>(), out.off.as<uint32_t>(),
+                                                         raw.as<uint32_t>(), out.col.as<uint32_t>());
+    CYC_LAUNCHED();
+    k_compact_list<<<sm_count() * 4, 256, 0, s>>>(med, cts + 0, roff.as<uint32_t>(),
+                                                  out.off.as<uint32_t>(), raw.as<uint32_t>(),
+                                                  out.col.as<uint32_t>());
+    CYC_LAUNCHED();
+    k_compact_list<<<sm_count() * 4, 256, 0, s>>>(big, cts + 1, roff.as<uint32_t>(),
+                                                  out.off.as<uint32_t>(), raw.as<uint32_t>(),
+                                                  out.col.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
+}
+
+void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s) {
+  uint64_t cap = g.m / chunk + g.m / (heavy ? heavy : 1) + 2;
+  g.heavy.alloc(cap * sizeof(uint4), s);
+  DevBuf cnt(8, s);
+  CYC_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
+  if (g.n) {
+    k_heavy_chunks<<<grid_for(g.n, 256, 16), 256, 0, s>>>(g.n, g.off.as<uint32_t>(), heavy, chunk,
+                                                          g.heavy.as<uint4>(), cnt.as<uint32_t>());
+    CYC_LAUNCHED();
+    k_max_degree<<<grid_for(g.n, 256, 8), 256, 0, s>>>(g.n, g.off.as<uint32_t>(),
+                                                       cnt.as<uint32_t>() + 1);
+    CYC_LAUNCHED();
+  }
+  uint32_t h[2] = {0, 0};
+  CYC_CUDA(cudaMemcpyAsync(h, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  g.n_heavy_chunks = h[0];
+  g.max_degree = h[1];
+  g.heavy_deg = heavy;
+}
+
+}  // namespace cyc

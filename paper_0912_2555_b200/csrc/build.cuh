@@ -1,0 +1,29 @@
+// build.cuh — device CSR layout and the K1 build entry points.
+#pragma once
+
+#include "common.cuh"
+
+namespace cyc {
+
+// One CSR on the device. Row offsets are u32 (n+1), columns u32 (m).
+struct DevCsr {
+  uint32_t n = 0;
+  uint32_t m = 0;
+  DevBuf off, col;
+  DevBuf heavy;                 // uint4 {row, beg, end, 0} chunks of rows with deg > heavy_deg
+  uint32_t n_heavy_chunks = 0;
+  uint32_t heavy_deg = 0;
+  uint32_t max_degree = 0;
+  const uint32_t* o() const { return off.as<uint32_t>(); }
+  const uint32_t* c() const { return col.as<uint32_t>(); }
+};
+
+int sm_count();
+uint32_t grid_for(uint64_t items, int threads, int per_sm);
+void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* total,
+                    cudaStream_t s, DevBuf& scratch);
+void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
+               DevCsr& out, uint32_t* d_err);
+void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s);
+
+}  // namespace cyc

@@ -1,0 +1,86 @@
+// map_run.cuh — workspace and launch interface of the persistent MAP loop.
+#pragma once
+
+#include "build.cuh"
+
+namespace cyc {
+
+// Control block of one k_map_run launch. Per-step counters rotate over three
+// slots (step g writes slot g%3, reads slot (g-1)%3, and clears slot (g+1)%3),
+// per-iteration counters over two. The grid barrier sits on its own lines.
+struct RunCtl {
+  GridBar bar;
+  unsigned long long list_ctr[3];  // (entries << 32) | edge total of the frontier list
+  unsigned int cand_cnt[3];        // self-witness candidates appended
+  unsigned int wit[3];             // exact min self-witness (pull rows)
+  unsigned int changed[3];
+  unsigned int nraised[3];
+  unsigned long long it_hash[2];
+  unsigned int it_finwit[2];
+  unsigned int it_dcount[2];
+  unsigned long long it_fsize[2];
+  unsigned long long res[16];
+};
+
+enum RunRes {
+  kResCycle = 0, kResWitness, kResIterations, kResKernelCalls, kResDemoted, kResStepsLast,
+  kResPullSteps, kResPushSteps, kResEdges, kResRows, kResBytes, kResCur, kResTag
+};
+
+struct RunArgs {
+  uint32_t n, m;
+  const uint32_t* goff;  // gather index (pull): row v = sources flowing into v
+  const uint32_t* gcol;
+  const uint32_t* poff;  // snapshot relation (push): row u = targets u flows into
+  const uint32_t* pcol;
+  const uint4* heavy;    // gather rows longer than heavy_deg, split into chunks
+  uint32_t n_heavy, heavy_deg;
+  uint32_t* P[2];                  // packed map words: accepting<<31 | code
+  unsigned long long* T[2];        // (step tag << 32) | value raised in that step
+  uint32_t* Lv[2];                 // frontier vertices
+  uint32_t* Le[2];                 // frontier edge starts (prefix of push degrees)
+  uint32_t* C[2];                  // self-witness candidates
+  uint32_t* F;                     // accepting set, u32 words (demoted in place)
+  uint32_t* used;                  // scratch bitmap, zero between iterations
+  uint32_t nwords;
+  RunCtl* ctl;
+  unsigned long long* iter_hash;
+  unsigned long long* iter_steps;
+  unsigned long long cap;
+  unsigned long long max_iterations, max_steps;
+  uint32_t tag0;                   // first step tag of this launch (tags only grow)
+  uint32_t alpha;
+  int early_exit, mode;
+};
+
+struct RunWs {
+  uint32_t n = 0;
+  DevBuf P[2], T[2], Lv[2], Le[2], C[2], F, used, ctl, hist;
+  uint32_t tag = 1;
+  void ensure(uint32_t n, cudaStream_t s);
+};
+
+struct RunOut {
+  unsigned long long res[16];
+  float ms;
+  uint32_t grid, block;
+};
+
+// Runs the device-resident MAP loop. F must already hold the accepting words.
+void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early_exit, int mode,
+                    unsigned long long max_iterations, unsigned long long max_steps,
+                    uint32_t alpha, unsigned long long cap, cudaStream_t s, cudaEvent_t e0,
+                    cudaEvent_t e1, RunOut& out);
+
+// Writes the codes (flag bit stripped) of workspace buffer `cur` into dst.
+void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream_t s);
+
+// Dense single Jacobi step (MaxPropagation::step) on plain codes.
+void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* accw, uint32_t* out,
+                      uint32_t* flags, cudaStream_t s);
+
+// demote(): remaining = F & ~used(x); demoted ascending; returns |D| on host.
+uint64_t run_demote(const uint32_t* x, uint32_t n, const uint32_t* accw, uint32_t* remaining,
+                    uint32_t* demoted, cudaStream_t s);
+
+}  // namespace cyc

@@ -1,0 +1,328 @@
+"""GPU parity: every engine entry point, called through the C ABI, against the
+oracle restatement (pinned to the reference in test_oracle.py) and the golden
+fixtures made by the reference itself. Integer work: bit-exact everywhere."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.json")
+MODES = ("auto", "pull", "push")
+G1 = [(0, 1), (1, 2), (2, 1)]
+
+
+def digest(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+def snap_of(eng, n, edges, acc, transposed=True):
+    o = eng.Orientation.transposed if transposed else eng.Orientation.forward
+    return eng.build_snapshot((n, np.asarray(edges, np.uint32).reshape(-1, 2), acc), o)
+
+
+def oracle_run(R, n, edges, acc, transposed, early):
+    gat = R.transpose(R.build_snapshot(n, edges, transposed))
+    return R.run_map(gat, acc, early)
+
+
+def assert_same_run(run, ref):
+    got = (run.verdict.cycle_found(), run.verdict.witness, run.stats.iterations,
+           run.stats.kernel_calls, run.stats.demoted_total)
+    want = (ref.cycle, ref.witness, ref.iterations, ref.kernel_calls, ref.demoted_total)
+    assert got == want
+    assert np.array_equal(run.final_values, ref.final_x)
+    assert np.array_equal(run.iter_hash, ref.iter_hash[: len(run.iter_hash)])
+    assert np.array_equal(run.iter_steps, ref.iter_steps[: len(run.iter_steps)])
+
+
+# ------------------------------------------------------------------ KATs
+def test_kat_snapshot(eng):
+    s = snap_of(eng, 3, G1, [False, True, False], True)
+    assert s.row_offsets.tolist() == [0, 0, 2, 3] and s.col_indices.tolist() == [0, 2, 1]
+    off, col = s.gather_index()
+    assert off.tolist() == [0, 1, 2, 3] and col.tolist() == [1, 2, 1]
+    f = snap_of(eng, 3, G1, [False, True, False], False)
+    assert f.row_offsets.tolist() == [0, 1, 2, 3] and f.col_indices.tolist() == [1, 2, 1]
+    e = snap_of(eng, 0, np.zeros((0, 2)), np.zeros(0, bool))
+    assert e.row_offsets.tolist() == [0] and e.m == 0
+
+
+def test_kat_steps_and_fixpoint(eng):
+    s = snap_of(eng, 3, G1, [False, True, False])
+    x1, ch = eng.propagate_step(s, eng.init_vector(s), s.accepting)
+    assert x1.tolist() == [2, 0, 2] and ch
+    r = eng.MaxPropagation(s).step(x1, s.accepting)
+    assert r.changed and r.self_witness == 1
+    for mode in MODES:
+        fr = eng.fixpoint(s, s.accepting, eng.MapOptions(mode=mode))
+        assert fr.witness == 1 and fr.steps == 2 and fr.values.tolist() == [2, 2, 2]
+    chain = snap_of(eng, 3, [(0, 1), (1, 2)], [False, False, True])
+    for mode in MODES:
+        fr = eng.fixpoint(chain, chain.accepting, eng.MapOptions(mode=mode))
+        assert fr.values.tolist() == [3, 3, 0] and fr.steps == 3 and fr.witness is None
+    empty = snap_of(eng, 0, np.zeros((0, 2)), np.zeros(0, bool))
+    fr = eng.fixpoint(empty, empty.accepting)
+    assert fr.steps == 1 and fr.witness is None
+    nof = snap_of(eng, 4, [(0, 1), (1, 2)], [False] * 4)
+    fr = eng.fixpoint(nof, nof.accepting)
+    assert fr.steps == 1 and fr.values.tolist() == [0, 0, 0, 0]
+
+
+def test_kat_demote(eng):
+    d = eng.demote([3, 3, 0], [False, False, True])
+    assert d.demoted.tolist() == [2] and d.remaining.count() == 0
+    d = eng.demote([0, 0, 0, 0], [True, False, True, True])
+    assert d.demoted.tolist() == [] and d.remaining.indices().tolist() == [0, 2, 3]
+    d = eng.demote([4, 0, 4, 0], [False, True, False, True])
+    assert d.demoted.tolist() == [3] and d.remaining.indices().tolist() == [1]
+
+
+def test_kat_run_map(eng):
+    s = snap_of(eng, 1, [(0, 0)], [True])
+    v, st = eng.run_map(s, s.accepting)
+    assert v.cycle_found() and v.witness == 0 and st.iterations == 1
+    dag = snap_of(eng, 3, [(0, 1), (1, 2)], [True, True, True])
+    v, st = eng.run_map(dag, dag.accepting)
+    assert not v.cycle_found()
+    none = snap_of(eng, 2, [(0, 1)], [False, False])
+    v, st = eng.run_map(none, none.accepting)
+    assert not v.cycle_found() and st.iterations == 0 and st.kernel_calls == 0
+
+
+def test_kat_restrict(eng):
+    s = snap_of(eng, 3, G1, [False, True, False])
+    r = eng.restrict_to_accepting_sccs(s)
+    assert r.kept.tolist() == [1, 2] and r.snapshot.n == 2
+    assert r.snapshot.row_offsets.tolist() == [0, 1, 2] and r.snapshot.col_indices.tolist() == [1, 0]
+    assert r.snapshot.accepting.indices().tolist() == [0]
+    c = snap_of(eng, 3, [(0, 1), (1, 2)], [False, False, True])
+    assert eng.restrict_to_accepting_sccs(c).kept.tolist() == []
+
+
+def test_contract_errors(eng):
+    with pytest.raises(eng.ContractError):
+        snap_of(eng, 2, [(0, 5)], [False, False])
+    s = snap_of(eng, 3, G1, [False, True, False])
+    with pytest.raises(eng.ContractError):
+        eng.propagate_step(s, np.zeros(4, np.uint32), s.accepting)
+    with pytest.raises(eng.ContractError):
+        eng.run_map(s, np.zeros(5, bool))
+
+
+# -------------------------------------------------------------- golden
+def test_golden_random(eng, golden):
+    for case in golden["random"]:
+        n = case["n"]
+        acc = np.zeros(n, bool)
+        acc[case["accepting"]] = True
+        s = snap_of(eng, n, case["edges"], acc)
+        assert s.row_offsets.tolist() == case["row_offsets"]
+        assert s.col_indices.tolist() == case["col_indices"]
+        x1, ch = eng.propagate_step(s, eng.init_vector(s), acc)
+        assert x1.tolist() == case["step1"] and ch == case["step1_changed"]
+        for mode in MODES:
+            for key, early in (("early", True), ("full", False)):
+                run = eng.run_map_detailed(s, acc, eng.MapOptions(early_exit=early, mode=mode))
+                want = case[key]
+                assert (run.verdict.cycle_found(), run.verdict.witness, run.stats.iterations,
+                        run.stats.kernel_calls, run.stats.demoted_total) == (
+                    want["cycle"], want["witness"], want["iterations"], want["kernel_calls"],
+                    want["demoted_total"]), (mode, key)
+                assert run.final_values.tolist() == case["final_x_" + key]
+                assert [int(h) for h in run.iter_hash] == want["iter_hash"]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_L16", "c5_L16", "c3_s12"])
+def test_golden_configs(eng, R, golden, name):
+    cfg = golden["configs"][name]
+    p = R.preset(cfg["config"])
+    for k, v in cfg["overrides"].items():
+        setattr(p, k, v)
+    R.prepare(p)
+    n, e, accw = R.generate(p)
+    # the device generator reproduces the same log
+    de = np.zeros_like(e)
+    da = np.zeros_like(accw)
+    from paper_0912_2555_b200 import _abi
+    ctx = eng.default_context()
+    _abi.check(_abi.lib().cyc_gen_fill(ctx.handle, _abi.C.byref(p), _abi.ptr(de), _abi.ptr(da)))
+    assert np.array_equal(de, e) and np.array_equal(da, accw)
+    acc = eng.Bitset.from_words(accw, n)
+    for orient, tr in (("transposed", True), ("forward", False)):
+        s = snap_of(eng, n, e, acc, tr)
+        want = cfg[orient]
+        assert s.m == want["m"]
+        assert digest(s.row_offsets) == want["off_digest"] and digest(s.col_indices) == want["col_digest"]
+        for mode in MODES:
+            for key, early in (("early", True), ("full", False)):
+                run = eng.run_map_detailed(s, acc, eng.MapOptions(early_exit=early, mode=mode))
+                w = want[key]
+                assert (run.verdict.cycle_found(), run.verdict.witness, run.stats.iterations,
+                        run.stats.kernel_calls, run.stats.demoted_total) == (
+                    w["cycle"], w["witness"], w["iterations"], w["kernel_calls"], w["demoted_total"]), (
+                    orient, mode, key)
+                assert digest(run.final_values) == w["final_x_digest"]
+                assert [int(h) for h in run.iter_hash[:256]] == w["iter_hash"]
+        r = eng.restrict_to_accepting_sccs(s)
+        wr = want["restricted"]
+        assert (r.snapshot.n, r.snapshot.m) == (wr["n"], wr["m"])
+        assert digest(r.kept) == wr["kept_digest"]
+        assert digest(r.snapshot.row_offsets) == wr["off_digest"]
+        assert digest(r.snapshot.col_indices) == wr["col_digest"]
+        if wr["n"]:
+            v, st = eng.run_map(r.snapshot, r.snapshot.accepting)
+            w = wr["early"]
+            assert (v.cycle_found(), st.iterations, st.kernel_calls) == (w["cycle"], w["iterations"],
+                                                                         w["kernel_calls"])
+            if w["cycle"]:
+                assert int(r.kept[v.witness]) == w["witness_original"]
+
+
+# ------------------------------------------------------- differential
+def random_graph(rng, n, m, hubs=0):
+    e = rng.integers(0, n, size=(m, 2)).astype(np.uint32)
+    if hubs:
+        # a few hub rows/columns beyond the small/medium/heavy thresholds
+        for h in range(hubs):
+            d = int(rng.integers(300, 9000))
+            hub = int(rng.integers(0, n))
+            other = rng.integers(0, n, size=d).astype(np.uint32)
+            pair = np.stack([np.full(d, hub, np.uint32), other], 1) if h % 2 else \
+                np.stack([other, np.full(d, hub, np.uint32)], 1)
+            e = np.concatenate([e, pair])
+    return e
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_differential_random(eng, R, seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(200, 20000))
+    m = int(n * rng.choice([1, 2, 4, 8]))
+    e = random_graph(rng, n, m, hubs=seed % 3)
+    acc = rng.random(n) < rng.choice([0.001, 0.01, 0.05, 0.3])
+    for tr in (True, False):
+        s = snap_of(eng, n, e, acc, tr)
+        g = R.build_snapshot(n, e, tr)
+        assert np.array_equal(s.row_offsets, g.off) and np.array_equal(s.col_indices, g.col)
+        gat = R.transpose(g)
+        off, col = s.gather_index()
+        assert np.array_equal(off, gat.off) and np.array_equal(col, gat.col)
+        for early in (True, False):
+            ref = R.run_map(gat, acc, early)
+            for mode in MODES:
+                run = eng.run_map_detailed(s, acc, eng.MapOptions(early_exit=early, mode=mode))
+                assert_same_run(run, ref)
+
+
+def test_per_step_vectors(eng, R):
+    # Jacobi step-for-step: x after k steps, all step kinds
+    rng = np.random.default_rng(77)
+    n, m = 3000, 6000
+    e = random_graph(rng, n, m, hubs=2)
+    acc = rng.random(n) < 0.02
+    s = snap_of(eng, n, e, acc)
+    gat = R.transpose(R.build_snapshot(n, e, True))
+    x = np.zeros(n, np.uint32)
+    for k in range(1, 12):
+        x, ch, w = R.step(gat, x, acc)
+        for mode in MODES:
+            fr = eng.fixpoint(s, acc, eng.MapOptions(early_exit=False, mode=mode), max_steps=k)
+            assert fr.steps <= k
+            assert np.array_equal(fr.values, x), (k, mode)
+        if not ch:
+            break
+
+
+def test_dense_step_matches_oracle_on_arbitrary_vectors(eng, R):
+    rng = np.random.default_rng(9)
+    n = 5000
+    e = random_graph(rng, n, 20000, hubs=2)
+    acc = rng.random(n) < 0.1
+    s = snap_of(eng, n, e, acc)
+    gat = R.transpose(R.build_snapshot(n, e, True))
+    for _ in range(5):
+        x = rng.integers(0, n + 1, size=n).astype(np.uint32)
+        want = R.step(gat, x, acc)
+        r = eng.MaxPropagation(s)
+        res = r.step(x, acc)
+        assert np.array_equal(r.last_out, want[0])
+        assert res.changed == want[1] and res.self_witness == want[2]
+
+
+def test_restrict_differential(eng, R):
+    rng = np.random.default_rng(31)
+    for t in range(8):
+        n = int(rng.integers(50, 5000))
+        e = random_graph(rng, n, int(n * rng.choice([1, 2, 3])), hubs=t % 2)
+        acc = rng.random(n) < rng.choice([0.01, 0.1, 0.5])
+        for tr in (True, False):
+            s = snap_of(eng, n, e, acc, tr)
+            g = R.build_snapshot(n, e, tr)
+            rg, racc, kept = R.restrict(g, acc)
+            r = eng.restrict_to_accepting_sccs(s)
+            assert np.array_equal(r.kept, kept)
+            assert np.array_equal(r.snapshot.row_offsets, rg.off)
+            assert np.array_equal(r.snapshot.col_indices, rg.col)
+            assert np.array_equal(r.snapshot.accepting.words()[: len(racc)], racc[: len(r.snapshot.accepting.words())])
+            # verdict preserved under restriction (graph.hpp:110-113)
+            v1, _ = eng.run_map(s, acc)
+            v2, _ = eng.run_map(r.snapshot, r.snapshot.accepting)
+            assert v1.cycle_found() == v2.cycle_found()
+
+
+def test_check_pipeline(eng, R):
+    rng = np.random.default_rng(4)
+    n = 4000
+    e = random_graph(rng, n, 12000)
+    acc = rng.random(n) < 0.05
+    for restrict in (False, True):
+        v, st = eng.check_graph(n, e, acc, eng.Orientation.transposed, restrict)
+        g = R.build_snapshot(n, e, True)
+        if restrict:
+            rg, racc, kept = R.restrict(g, acc)
+            ref = R.run_map(R.transpose(rg), racc, True)
+            wit = int(kept[ref.witness]) if ref.cycle else None
+        else:
+            ref = R.run_map(R.transpose(g), acc, True)
+            wit = ref.witness
+        assert (v.cycle_found(), v.witness, st.iterations, st.kernel_calls) == (
+            ref.cycle, wit, ref.iterations, ref.kernel_calls)
+
+
+# ------------------------------------------------------- full-size properties
+def test_c2_full_size_closed_form(eng):
+    """Config 2 at 2^22: iterations = L+1 = 65, kernel_calls = (L+1)^2 = 4225,
+    no cycle, one connector demoted per round."""
+    p = eng.preset(2)
+    from paper_0912_2555_b200 import _abi
+    ctx = eng.default_context()
+    e = np.zeros((p.m, 2), np.uint32)
+    a = np.zeros((p.n + 63) // 64, np.uint64)
+    _abi.check(_abi.lib().cyc_gen_fill(ctx.handle, _abi.C.byref(p), _abi.ptr(e), _abi.ptr(a)))
+    s = snap_of(eng, p.n, e, eng.Bitset.from_words(a, p.n))
+    for mode in MODES:
+        v, st = eng.run_map(s, s.accepting, eng.MapOptions(mode=mode))
+        assert not v.cycle_found()
+        assert (st.iterations, st.kernel_calls, st.demoted_total) == (65, 65 ** 2, 64), mode
+
+
+def test_monotone_and_idempotent(eng, R):
+    rng = np.random.default_rng(12)
+    n = 20000
+    e = random_graph(rng, n, 60000)
+    acc = rng.random(n) < 0.01
+    s = snap_of(eng, n, e, acc)
+    fr = eng.fixpoint(s, acc, eng.MapOptions(early_exit=False))
+    # idempotence at the fixpoint
+    x2, ch = eng.propagate_step(s, fr.values, acc)
+    assert not ch and np.array_equal(x2, fr.values)

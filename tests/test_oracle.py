@@ -1,0 +1,239 @@
+"""CPU tests: the oracle restatement is pinned against the SPEC.md [OP]
+known-answer examples, the committed golden fixtures (generated from the
+reference itself, tests/golden/make_golden.py), and — where the reference
+build is present — the reference on fresh random inputs."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.json")
+NIL = 0
+
+
+def code(v):  # map value of vertex v (map_engine.hpp:23)
+    return v + 1
+
+
+def digest(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+G1 = [(0, 1), (1, 2), (2, 1)]
+
+
+# ---------------------------------------------------------------- SPEC KATs
+def test_spec_snapshot_transposed(R):
+    g = R.build_snapshot(3, G1, True)
+    assert g.off.tolist() == [0, 0, 2, 3] and g.col.tolist() == [0, 2, 1]
+
+
+def test_spec_snapshot_forward(R):
+    g = R.build_snapshot(3, G1, False)
+    assert g.off.tolist() == [0, 1, 2, 3] and g.col.tolist() == [1, 2, 1]
+
+
+def test_spec_empty_snapshot(R):
+    g = R.build_snapshot(0, [], True)
+    assert g.off.tolist() == [0] and g.m == 0
+
+
+def test_spec_dedup(R):  # SPEC.md:74-75, graph.cpp:89-101
+    g = R.build_snapshot(2, [(0, 1), (0, 1), (1, 0)], True)
+    assert g.m == 2
+
+
+def test_spec_restrict_kept(R):
+    g = R.build_snapshot(3, G1, True)
+    r, acc, kept = R.restrict(g, np.array([False, True, False]))
+    assert kept.tolist() == [1, 2]
+
+
+def test_spec_restrict_chain_empty(R):
+    g = R.build_snapshot(3, [(0, 1), (1, 2)], True)
+    _, _, kept = R.restrict(g, np.array([False, False, True]))
+    assert kept.tolist() == []
+
+
+def test_spec_steps_g1(R):
+    gat = R.transpose(R.build_snapshot(3, G1, True))
+    acc = np.array([False, True, False])
+    x1, ch1, _ = R.step(gat, np.zeros(3, np.uint32), acc)
+    assert x1.tolist() == [code(1), NIL, code(1)] and ch1
+    x2, ch2, w2 = R.step(gat, x1, acc)
+    assert x2.tolist() == [code(1)] * 3 and ch2 and w2 == 1
+
+
+def test_spec_fixpoint_g1_witness(R):
+    gat = R.transpose(R.build_snapshot(3, G1, True))
+    x, steps, w = R.fixpoint(gat, np.array([False, True, False]), True)
+    assert w == 1 and steps == 2
+
+
+def test_spec_chain_fixpoint(R):
+    gat = R.transpose(R.build_snapshot(3, [(0, 1), (1, 2)], True))
+    x, steps, w = R.fixpoint(gat, np.array([False, False, True]), True)
+    assert x.tolist() == [code(2), code(2), NIL] and steps == 3 and w is None
+
+
+def test_spec_empty_fixpoint(R):
+    gat = R.transpose(R.build_snapshot(0, [], True))
+    _, steps, w = R.fixpoint(gat, np.zeros(0, bool), True)
+    assert steps == 1 and w is None
+
+
+def test_spec_demote_chain(R):
+    rem, d = R.demote([code(2), code(2), NIL], np.array([False, False, True]))
+    assert d.tolist() == [2] and int(rem[0]) == 0
+
+
+def test_spec_demote_nil(R):
+    acc = np.array([True, False, True, True])
+    rem, d = R.demote([NIL] * 4, acc)
+    assert d.tolist() == [] and int(rem[0]) == 0b1101
+
+
+def test_spec_demote_partial(R):  # only 3 appears as a value
+    acc = np.array([False, True, False, True])
+    rem, d = R.demote([code(3), NIL, code(3), NIL], acc)
+    assert d.tolist() == [3] and int(rem[0]) == 0b0010
+
+
+def test_spec_self_loop_cycle(R):
+    gat = R.transpose(R.build_snapshot(1, [(0, 0)], True))
+    r = R.run_map(gat, np.array([True]), True)
+    assert r.cycle and r.witness == 0 and r.iterations == 1
+
+
+def test_spec_dag_no_cycle(R):
+    rng = np.random.default_rng(3)
+    n = 30
+    e = [(a, b) for a, b in rng.integers(0, n, (80, 2)).tolist() if a < b]
+    gat = R.transpose(R.build_snapshot(n, e, True))
+    for early in (True, False):
+        assert not R.run_map(gat, rng.random(n) < 0.4, early).cycle
+
+
+# -------------------------------------------------------------- golden
+def test_golden_random_graphs(R, golden):
+    for case in golden["random"]:
+        n = case["n"]
+        e = np.array(case["edges"], np.uint32).reshape(-1, 2)
+        acc = np.zeros(n, bool)
+        acc[case["accepting"]] = True
+        g = R.build_snapshot(n, e, True)
+        assert g.off.tolist() == case["row_offsets"] and g.col.tolist() == case["col_indices"]
+        gat = R.transpose(g)
+        x1, ch1, _ = R.step(gat, np.zeros(n, np.uint32), acc)
+        assert x1.tolist() == case["step1"] and ch1 == case["step1_changed"]
+        for mode, early in (("early", True), ("full", False)):
+            r = R.run_map(gat, acc, early)
+            want = case[mode]
+            assert (r.cycle, r.witness, r.iterations, r.kernel_calls, r.demoted_total) == (
+                want["cycle"], want["witness"], want["iterations"], want["kernel_calls"],
+                want["demoted_total"])
+            assert r.final_x.tolist() == case["final_x_" + mode]
+            assert [int(h) for h in r.iter_hash] == want["iter_hash"]
+            assert [int(s) for s in r.iter_steps] == want["iter_steps"]
+        assert r.cycle == case["scc_cycle"]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_L16", "c5_L16", "c3_s12"])
+def test_golden_configs(R, golden, name):
+    cfg = golden["configs"][name]
+    p = R.preset(cfg["config"])
+    for k, v in cfg["overrides"].items():
+        setattr(p, k, v)
+    R.prepare(p)
+    n, e, accw = R.generate(p)
+    assert digest(e) == cfg["edges_digest"] and digest(accw) == cfg["acc_digest"]
+    vec = np.load(os.path.join(os.path.dirname(GOLDEN), "golden_vectors.npz"))
+    for orient, tr in (("transposed", True), ("forward", False)):
+        g = R.build_snapshot(n, e, tr)
+        want = cfg[orient]
+        assert g.m == want["m"] and digest(g.off) == want["off_digest"] and digest(g.col) == want["col_digest"]
+        gat = R.transpose(g)
+        for mode, early in (("early", True), ("full", False)):
+            r = R.run_map(gat, accw, early)
+            w = want[mode]
+            assert (r.cycle, r.witness, r.iterations, r.kernel_calls, r.demoted_total) == (
+                w["cycle"], w["witness"], w["iterations"], w["kernel_calls"], w["demoted_total"])
+            assert digest(r.final_x) == w["final_x_digest"]
+            assert [int(h) for h in r.iter_hash[:256]] == w["iter_hash"]
+            key = f"{name}_{orient}_{mode}_final_x"
+            if key in vec:
+                assert np.array_equal(vec[key], r.final_x)
+        rg, racc, kept = R.restrict(g, accw)
+        wr = want["restricted"]
+        assert rg.n == wr["n"] and rg.m == wr["m"] and digest(kept) == wr["kept_digest"]
+        assert digest(rg.off) == wr["off_digest"] and digest(rg.col) == wr["col_digest"]
+
+
+def test_closed_form_layered(R, golden):
+    # C2 family has iterations = L+1, kernel_calls = (L+1)^2
+    w = golden["configs"]["c2_L16"]["transposed"]["early"]
+    assert w["iterations"] == 17 and w["kernel_calls"] == 17 ** 2 and not w["cycle"]
+
+
+# ------------------------------------------- differential vs the reference
+def test_random_differential_reference(R, REF):
+    rng = np.random.default_rng(2555)
+    for t in range(300):
+        n = int(rng.integers(1, 50))
+        m = int(rng.integers(0, 4 * n))
+        e = rng.integers(0, n, size=(m, 2)).astype(np.uint32)
+        acc = rng.random(n) < [0.1, 0.3][t % 2]
+        for tr in (True, False):
+            rs = REF.snapshot(n, e, acc, tr)
+            c, racc, _ = rs.export()
+            g = R.build_snapshot(n, e, tr)
+            assert np.array_equal(g.off, c.off) and np.array_equal(g.col, c.col)
+            gat = R.transpose(g)
+            for early in (True, False):
+                a, b = R.run_map(gat, acc, early), rs.run_map(None, early)
+                assert (a.cycle, a.witness, a.iterations, a.kernel_calls, a.demoted_total) == (
+                    b.cycle, b.witness, b.iterations, b.kernel_calls, b.demoted_total)
+                assert np.array_equal(a.final_x, b.final_x)
+                assert np.array_equal(a.iter_hash, b.iter_hash)
+            rg, _, kept = R.restrict(g, acc)
+            rr = rs.restrict()
+            c2, _, k2 = rr.export()
+            assert np.array_equal(kept, k2) and np.array_equal(rg.off, c2.off) and np.array_equal(rg.col, c2.col)
+            # verdict equals the SCC oracle
+            assert R.run_map(gat, acc, True).cycle == rs.scc_verdict()
+
+
+def test_reference_step_worker_invariance(REF):
+    # map_engine.hpp:46-49: bitwise identical for every worker count
+    rng = np.random.default_rng(7)
+    n = 500
+    e = rng.integers(0, n, size=(2000, 2)).astype(np.uint32)
+    acc = rng.random(n) < 0.2
+    rs = REF.snapshot(n, e, acc, True)
+    x = rng.integers(0, n + 1, size=n).astype(np.uint32)
+    outs = [rs.step(x, None, w) for w in (1, 2, 4)]
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and o[1:] == outs[0][1:]
+
+
+def test_generators_deterministic(R):
+    for idx in (1, 2, 5):
+        p = R.preset(idx)
+        if idx == 2:
+            p.L, p.W, p.S = 4, 8, 4
+        if idx == 5:
+            p.L, p.W, p.S = 4, 2, 8
+        R.prepare(p)
+        a = R.generate(p)
+        b = R.generate(p)
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    p = R.preset(2)
+    assert (p.n, p.m) == (64 * (4096 * 16 + 1) + 1, 64 * 4096 * (1 + 16 + 16))
