@@ -53,15 +53,16 @@ typedef struct cyc_map_options {
   int32_t mode;            /* CYC_MODE_* (default AUTO) */
   uint64_t max_iterations; /* 0 = run to verdict (run_map); 1 = one fixpoint */
   uint64_t max_steps;      /* 0 = unbounded; else stop the first fixpoint after k steps */
-  uint32_t push_alpha;     /* push when frontier edges * alpha < m (0 = default 16) */
-  uint32_t reserved;
+  uint32_t push_alpha;     /* push when frontier edges * alpha < m (0 = default) */
+  uint32_t trace_cap;      /* > 0: record up to this many steps (cyc_map_trace) */
 } cyc_map_options;
 
 /* reference map_engine.hpp:101-106 MapStats + types.hpp:18-27 Verdict, plus
  * device-side evidence for the roofline. */
 typedef struct cyc_map_stats {
   int32_t cycle_found;
-  uint32_t witness;            /* valid iff cycle_found (original ids if restricted) */
+  uint32_t witness;            /* valid iff cycle_found; cyc_check maps it back to the
+                                  log's ids when it restricted (explore.cpp:117-118) */
   uint64_t iterations;
   uint64_t kernel_calls;
   uint64_t demoted_total;
@@ -126,6 +127,10 @@ cyc_status cyc_demote(cyc_ctx* ctx, const uint32_t* values, uint32_t n,
 cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
                        const cyc_map_options* opt, cyc_map_stats* stats, uint32_t* final_values,
                        uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap);
+
+/* Per-step record of the graph's last loop run with trace_cap > 0: 4 u64 per
+ * step = {mode << 32 | step-in-fixpoint, frontier edges, raised, SM clock}. */
+cyc_status cyc_map_trace(const cyc_graph* g, uint64_t* out, uint32_t cap, uint32_t* len);
 
 /* ---- one-call pipeline: edge log -> verdict ----------------------------- */
 /* cycheck graph / explore final round (cycheck_main.cpp:88-97,

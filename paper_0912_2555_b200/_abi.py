@@ -44,7 +44,7 @@ class MapOptionsC(C.Structure):
         ("max_iterations", C.c_uint64),
         ("max_steps", C.c_uint64),
         ("push_alpha", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("trace_cap", C.c_uint32),
     ]
 
 
@@ -126,6 +126,7 @@ _SIGS = {
     "cyc_memcpy": (C.c_int, [_P, _P, _P, C.c_size_t]),
     "cyc_flush_l2": (C.c_int, [_P, C.c_size_t]),
     "cyc_shard_bounds": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
+    "cyc_map_trace": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -428,13 +428,14 @@ class MapOptions:
     early_exit: bool = True
     mode: str = "auto"            # "auto" | "pull" | "push"
     push_alpha: int = 0
+    trace_cap: int = 0            # > 0: keep a per-step device trace (map_trace)
 
     def to_c(self, max_iterations: int = 0, max_steps: int = 0) -> _abi.MapOptionsC:
         modes = {"auto": _abi.CYC_MODE_AUTO, "pull": _abi.CYC_MODE_PULL, "push": _abi.CYC_MODE_PUSH}
         if self.mode not in modes:
             raise ContractError(f"unknown mode {self.mode!r}")
         return _abi.MapOptionsC(int(bool(self.early_exit)), modes[self.mode], max_iterations,
-                                max_steps, int(self.push_alpha), 0)
+                                max_steps, int(self.push_alpha), int(self.trace_cap))
 
 
 @dataclass
@@ -585,6 +586,20 @@ def run_map(snap: CsrSnapshot, accepting=None, options: Optional[MapOptions] = N
     return r.verdict, r.stats
 
 
+def map_trace(snap: CsrSnapshot, cap: int = 1 << 20) -> np.ndarray:
+    """Per-step device trace of the snapshot's last run with trace_cap > 0:
+    rows of {mode (1 pull, 2 push), step in fixpoint, frontier edges, raised, SM clock}."""
+    buf = np.zeros((cap, 4), dtype=np.uint64)
+    n = C.c_uint32()
+    check(_abi.lib().cyc_map_trace(snap.handle, ptr(buf), cap, C.byref(n)))
+    t = buf[: n.value]
+    out = np.zeros((len(t), 5), dtype=np.int64)
+    out[:, 0] = (t[:, 0] >> np.uint64(32)).astype(np.int64)
+    out[:, 1] = (t[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    out[:, 2:] = t[:, 1:].astype(np.int64)
+    return out
+
+
 def stats_dict(st: _abi.MapStatsC) -> dict:
     return {name: getattr(st, name) for name, _ in st._fields_}
 
@@ -626,5 +641,5 @@ __all__ = [
     "Orientation", "Outcome", "ResourceLimitError", "SccRestriction", "StepResult", "Verdict",
     "as_bitset", "build_snapshot", "check_graph", "default_context", "demote", "fixpoint",
     "init_vector", "launch_count", "propagate_step", "restrict_to_accepting_sccs", "run_map",
-    "run_map_detailed", "shard_bounds",
+    "run_map_detailed", "shard_bounds", "map_trace",
 ]

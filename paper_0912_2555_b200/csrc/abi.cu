@@ -171,7 +171,7 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   CYC_CUDA(cudaStreamSynchronize(s));
   require(herr == 0, CYC_E_CONTRACT, "build_snapshot: edge endpoint >= n (not interned)");
   require(g->snap.m == g->gath.m, CYC_E_CUDA, "internal: snapshot/gather edge counts differ");
-  cyc::build_heavy(g->gath, 256, 1024, s);
+  cyc::build_heavy(g->gath, 256, 256, s);
   load_acc(acc_words, n, g->acc, s);
 }
 
@@ -207,7 +207,7 @@ cyc::RunOut run_loop(cyc_ctx* ctx, cyc_graph* g, const uint64_t* acc_words,
   cudaStream_t s = ctx->s;
   const uint32_t n = g->n();
   require(o.mode >= CYC_MODE_AUTO && o.mode <= CYC_MODE_PUSH, CYC_E_CONTRACT, "bad mode");
-  g->ws.ensure(n, s);
+  g->ws.ensure(n, g->gath.m, s);
   const size_t nw = acc_words64(n);
   if (acc_words) {
     CYC_CUDA(cudaMemcpyAsync(g->ws.F.p, acc_words, nw * 8, cudaMemcpyDefault, s));
@@ -220,7 +220,7 @@ cyc::RunOut run_loop(cyc_ctx* ctx, cyc_graph* g, const uint64_t* acc_words,
   }
   cyc::RunOut out;
   cyc::launch_map_run(g->snap, g->gath, g->ws, o.early_exit != 0, o.mode, o.max_iterations,
-                      o.max_steps, o.push_alpha, cap, s, ctx->e0, ctx->e1, out);
+                      o.max_steps, o.push_alpha, cap, o.trace_cap, s, ctx->e0, ctx->e1, out);
   return out;
 }
 
@@ -305,7 +305,7 @@ cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out
       g->restricted = 1;
       cyc::restrict_graph(in->snap, in->gath, in->acc.as<uint64_t>(), ctx->s, g->snap, g->gath,
                           g->acc, g->kept);
-      cyc::build_heavy(g->gath, 256, 1024, ctx->s);
+      cyc::build_heavy(g->gath, 256, 256, ctx->s);
     } catch (...) {
       delete g;
       throw;
@@ -445,15 +445,8 @@ cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_wor
     auto* gg = const_cast<cyc_graph*>(g);
     const uint64_t hcap = (iter_hash || iter_steps) ? cap : 0;
     cyc::RunOut r = run_loop(ctx, gg, acc_words, o, hcap);
-    fill_stats(r, stats);
+    fill_stats(r, stats);  // witness in this snapshot's ids, as run_map returns it
     const uint32_t n = g->n();
-    if (stats && g->restricted && stats->cycle_found) {
-      uint32_t orig = 0;
-      CYC_CUDA(cudaMemcpyAsync(&orig, g->kept.as<uint32_t>() + stats->witness, 4,
-                               cudaMemcpyDeviceToHost, ctx->s));
-      CYC_CUDA(cudaStreamSynchronize(ctx->s));
-      stats->witness = orig;
-    }
     if (final_values && n) {
       if (r.res[cyc::kResIterations] == 0) {
         CYC_CUDA(cudaMemsetAsync(gg->ws.P[0].p, 0, (size_t)n * 4, ctx->s));
@@ -493,7 +486,7 @@ cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32
       restricted.restricted = 1;
       cyc::restrict_graph(base.snap, base.gath, base.acc.as<uint64_t>(), ctx->s, restricted.snap,
                           restricted.gath, restricted.acc, restricted.kept);
-      cyc::build_heavy(restricted.gath, 256, 1024, ctx->s);
+      cyc::build_heavy(restricted.gath, 256, 256, ctx->s);
       run_on = &restricted;
     }
     auto t2 = clk::now();
@@ -612,6 +605,18 @@ cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes) {
 }
 
 // map_engine.cpp:35-43: bounds[w] = lower_bound(offsets, total*w/parts).
+cyc_status cyc_map_trace(const cyc_graph* g, uint64_t* out, uint32_t cap, uint32_t* len) {
+  return guard([&] {
+    require(g && len, CYC_E_CONTRACT, "null argument");
+    const uint32_t k = g->ws.trace_len < cap ? g->ws.trace_len : cap;
+    *len = k;
+    if (k && out) {
+      copy_out(out, g->ws.trace.as<uint64_t>(), (size_t)k * 4, g->ctx->s);
+      CYC_CUDA(cudaStreamSynchronize(g->ctx->s));
+    }
+  });
+}
+
 cyc_status cyc_shard_bounds(const uint64_t* row_offsets, uint32_t n, int parts, uint32_t* bounds) {
   return guard([&] {
     require(row_offsets && bounds && parts >= 1, CYC_E_CONTRACT, "shard_bounds: bad argument");

@@ -5,14 +5,20 @@
 
 namespace cyc {
 
+// Frontier vertices whose push degree exceeds kBigDeg are expanded as chunks
+// of kChunk edges by whole warps; the rest lane by lane from the bitmap.
+constexpr uint32_t kBigDeg = 32;
+constexpr uint32_t kChunk = 128;
+
 // Control block of one k_map_run launch. Per-step counters rotate over three
 // slots (step g writes slot g%3, reads slot (g-1)%3, and clears slot (g+1)%3),
 // per-iteration counters over two. The grid barrier sits on its own lines.
 struct RunCtl {
   GridBar bar;
-  unsigned long long list_ctr[3];  // (entries << 32) | edge total of the frontier list
-  unsigned int cand_cnt[3];        // self-witness candidates appended
-  unsigned int wit[3];             // exact min self-witness (pull rows)
+  unsigned long long fedges[3];  // sum of push degrees of the step's frontier
+  unsigned int nchunk[3];        // big-vertex chunks of the step's frontier
+  unsigned int cand_cnt[3];      // self-witness candidates appended
+  unsigned int wit[3];           // exact min self-witness (pull rows)
   unsigned int changed[3];
   unsigned int nraised[3];
   unsigned long long it_hash[2];
@@ -37,27 +43,32 @@ struct RunArgs {
   uint32_t n_heavy, heavy_deg;
   uint32_t* P[2];                  // packed map words: accepting<<31 | code
   unsigned long long* T[2];        // (step tag << 32) | value raised in that step
-  uint32_t* Lv[2];                 // frontier vertices
-  uint32_t* Le[2];                 // frontier edge starts (prefix of push degrees)
+  uint32_t* FB[2];                 // frontier bitmaps (raised, 0 < push degree <= kBigDeg)
+  uint4* BC[2];                    // frontier chunks {v, beg, end} of big-degree vertices
   uint32_t* C[2];                  // self-witness candidates
   uint32_t* F;                     // accepting set, u32 words (demoted in place)
   uint32_t* used;                  // scratch bitmap, zero between iterations
   uint32_t nwords;
+  uint32_t chunk_cap;
   RunCtl* ctl;
   unsigned long long* iter_hash;
   unsigned long long* iter_steps;
   unsigned long long cap;
   unsigned long long max_iterations, max_steps;
   uint32_t tag0;                   // first step tag of this launch (tags only grow)
+  unsigned long long* trace;       // optional per-step record {mode|steps, edges, raised, clock}
+  uint32_t trace_cap;
   uint32_t alpha;
   int early_exit, mode;
 };
 
 struct RunWs {
-  uint32_t n = 0;
-  DevBuf P[2], T[2], Lv[2], Le[2], C[2], F, used, ctl, hist;
+  uint32_t n = 0, m = 0;
+  DevBuf P[2], T[2], FB[2], BC[2], C[2], F, used, ctl, hist, trace;
+  uint32_t trace_cap = 0, trace_len = 0;
+  uint32_t chunk_cap = 0;
   uint32_t tag = 1;
-  void ensure(uint32_t n, cudaStream_t s);
+  void ensure(uint32_t n, uint32_t m, cudaStream_t s);
 };
 
 struct RunOut {
@@ -69,8 +80,8 @@ struct RunOut {
 // Runs the device-resident MAP loop. F must already hold the accepting words.
 void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early_exit, int mode,
                     unsigned long long max_iterations, unsigned long long max_steps,
-                    uint32_t alpha, unsigned long long cap, cudaStream_t s, cudaEvent_t e0,
-                    cudaEvent_t e1, RunOut& out);
+                    uint32_t alpha, unsigned long long cap, uint32_t trace_cap, cudaStream_t s,
+                    cudaEvent_t e0, cudaEvent_t e1, RunOut& out);
 
 // Writes the codes (flag bit stripped) of workspace buffer `cur` into dst.
 void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream_t s);
