@@ -128,8 +128,11 @@ cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_wor
                        const cyc_map_options* opt, cyc_map_stats* stats, uint32_t* final_values,
                        uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap);
 
-/* Per-step record of the graph's last loop run with trace_cap > 0: 4 u64 per
- * step = {mode << 32 | step-in-fixpoint, frontier edges, raised, SM clock}. */
+/* Per-step record of the graph's last loop run with trace_cap > 0: 64 u64 per
+ * step (index = step tag - 2): [0] = mode << 60 | input chunks << 24 | step in
+ * fixpoint, [1] frontier edges, [2] raised, [3] t_start, [7] t_end, [16..64)
+ * = 16 spread slots each of t_phase0, t_phase1, t_flags (globaltimer ns, the
+ * latest any warp reached that point; take the max over the slots). */
 cyc_status cyc_map_trace(const cyc_graph* g, uint64_t* out, uint32_t cap, uint32_t* len);
 
 /* ---- one-call pipeline: edge log -> verdict ----------------------------- */

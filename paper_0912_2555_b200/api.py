@@ -586,17 +586,25 @@ def run_map(snap: CsrSnapshot, accepting=None, options: Optional[MapOptions] = N
     return r.verdict, r.stats
 
 
-def map_trace(snap: CsrSnapshot, cap: int = 1 << 20) -> np.ndarray:
-    """Per-step device trace of the snapshot's last run with trace_cap > 0:
-    rows of {mode (1 pull, 2 push), step in fixpoint, frontier edges, raised, SM clock}."""
-    buf = np.zeros((cap, 4), dtype=np.uint64)
+def map_trace(snap: CsrSnapshot, cap: int = 1 << 16) -> np.ndarray:
+    """Per-step device trace of the snapshot's last run with trace_cap > 0.
+    Columns: mode (1 pull, 2 push), step in fixpoint, frontier edges, raised,
+    t_start, t_phase0, t_phase1, t_flags, t_end (globaltimer ns), input chunks."""
+    buf = np.zeros((cap, 64), dtype=np.uint64)
     n = C.c_uint32()
     check(_abi.lib().cyc_map_trace(snap.handle, ptr(buf), cap, C.byref(n)))
     t = buf[: n.value]
-    out = np.zeros((len(t), 5), dtype=np.int64)
-    out[:, 0] = (t[:, 0] >> np.uint64(32)).astype(np.int64)
-    out[:, 1] = (t[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.int64)
-    out[:, 2:] = t[:, 1:].astype(np.int64)
+    t = t[(t[:, 0] >> np.uint64(60)) > 0]
+    out = np.zeros((len(t), 10), dtype=np.int64)
+    out[:, 0] = (t[:, 0] >> np.uint64(60)).astype(np.int64)
+    out[:, 1] = (t[:, 0] & np.uint64(0xFFFFFF)).astype(np.int64)
+    out[:, 2] = t[:, 1].astype(np.int64)
+    out[:, 3] = t[:, 2].astype(np.int64)
+    out[:, 4] = t[:, 3].astype(np.int64)
+    for ph in range(3):
+        out[:, 5 + ph] = t[:, 16 + 16 * ph: 32 + 16 * ph].max(axis=1).astype(np.int64)
+    out[:, 8] = t[:, 7].astype(np.int64)
+    out[:, 9] = ((t[:, 0] >> np.uint64(24)) & np.uint64((1 << 36) - 1)).astype(np.int64)
     return out
 
 

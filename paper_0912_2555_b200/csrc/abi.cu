@@ -26,12 +26,30 @@ thread_local std::string g_err;
                         what + " [" + file + ":" + std::to_string(line) + "]");
 }
 
+// A context lives until cyc_ctx_destroy was called AND its last graph is gone
+// (graphs keep a reference), so teardown order between them does not matter.
 struct cyc_ctx {
   int device = 0;
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   cyc::DevBuf flush;
+  std::atomic<int> refs{1};
 };
+
+namespace {
+void ctx_release(cyc_ctx* ctx) {
+  if (ctx->refs.fetch_sub(1) != 1) return;
+  cudaSetDevice(ctx->device);
+  ctx->flush.release();
+  cudaStreamSynchronize(ctx->s);
+  cudaEventDestroy(ctx->e0);
+  cudaEventDestroy(ctx->e1);
+  cudaEventDestroy(ctx->e2);
+  cudaEventDestroy(ctx->e3);
+  cudaStreamDestroy(ctx->s);
+  delete ctx;
+}
+}  // namespace
 
 struct cyc_graph {
   cyc_ctx* ctx = nullptr;
@@ -172,6 +190,7 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   require(herr == 0, CYC_E_CONTRACT, "build_snapshot: edge endpoint >= n (not interned)");
   require(g->snap.m == g->gath.m, CYC_E_CUDA, "internal: snapshot/gather edge counts differ");
   cyc::build_heavy(g->gath, 256, 256, s);
+  cyc::build_ell(g->gath, s);
   load_acc(acc_words, n, g->acc, s);
 }
 
@@ -207,7 +226,7 @@ cyc::RunOut run_loop(cyc_ctx* ctx, cyc_graph* g, const uint64_t* acc_words,
   cudaStream_t s = ctx->s;
   const uint32_t n = g->n();
   require(o.mode >= CYC_MODE_AUTO && o.mode <= CYC_MODE_PUSH, CYC_E_CONTRACT, "bad mode");
-  g->ws.ensure(n, g->gath.m, s);
+  g->ws.ensure(n, g->gath.m, g->snap.o(), s);
   const size_t nw = acc_words64(n);
   if (acc_words) {
     CYC_CUDA(cudaMemcpyAsync(g->ws.F.p, acc_words, nw * 8, cudaMemcpyDefault, s));
@@ -260,16 +279,7 @@ cyc_status cyc_ctx_create(int device, cyc_ctx** out) {
 }
 
 void cyc_ctx_destroy(cyc_ctx* ctx) {
-  if (!ctx) return;
-  cudaSetDevice(ctx->device);
-  ctx->flush.release();
-  cudaStreamSynchronize(ctx->s);
-  cudaEventDestroy(ctx->e0);
-  cudaEventDestroy(ctx->e1);
-  cudaEventDestroy(ctx->e2);
-  cudaEventDestroy(ctx->e3);
-  cudaStreamDestroy(ctx->s);
-  delete ctx;
+  if (ctx) ctx_release(ctx);
 }
 
 cyc_status cyc_ctx_synchronize(cyc_ctx* ctx) {
@@ -290,6 +300,7 @@ cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, 
       delete g;
       throw;
     }
+    ctx->refs.fetch_add(1);
     *out = g;
   });
 }
@@ -306,18 +317,22 @@ cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out
       cyc::restrict_graph(in->snap, in->gath, in->acc.as<uint64_t>(), ctx->s, g->snap, g->gath,
                           g->acc, g->kept);
       cyc::build_heavy(g->gath, 256, 256, ctx->s);
+      cyc::build_ell(g->gath, ctx->s);
     } catch (...) {
       delete g;
       throw;
     }
+    ctx->refs.fetch_add(1);
     *out = g;
   });
 }
 
 void cyc_graph_destroy(cyc_graph* g) {
   if (!g) return;
-  cudaSetDevice(g->ctx->device);
+  cyc_ctx* ctx = g->ctx;
+  cudaSetDevice(ctx->device);
   delete g;
+  ctx_release(ctx);
 }
 
 cyc_status cyc_graph_info(const cyc_graph* g, uint32_t* n, uint64_t* m, int* orientation,
@@ -487,6 +502,7 @@ cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32
       cyc::restrict_graph(base.snap, base.gath, base.acc.as<uint64_t>(), ctx->s, restricted.snap,
                           restricted.gath, restricted.acc, restricted.kept);
       cyc::build_heavy(restricted.gath, 256, 256, ctx->s);
+      cyc::build_ell(restricted.gath, ctx->s);
       run_on = &restricted;
     }
     auto t2 = clk::now();
@@ -611,7 +627,7 @@ cyc_status cyc_map_trace(const cyc_graph* g, uint64_t* out, uint32_t cap, uint32
     const uint32_t k = g->ws.trace_len < cap ? g->ws.trace_len : cap;
     *len = k;
     if (k && out) {
-      copy_out(out, g->ws.trace.as<uint64_t>(), (size_t)k * 4, g->ctx->s);
+      copy_out(out, g->ws.trace.as<uint64_t>(), (size_t)k * 64, g->ctx->s);
       CYC_CUDA(cudaStreamSynchronize(g->ctx->s));
     }
   });

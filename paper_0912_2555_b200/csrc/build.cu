@@ -411,7 +411,90 @@ __global__ void k_max_degree(uint32_t n, const uint32_t* __restrict__ off, uint3
   if ((threadIdx.x & 31u) == 0) atomicMax(out, mx);
 }
 
+// per K in {1,2,4,8}: rows longer than K and the edges beyond K
+__global__ void k_ell_hist(uint32_t n, const uint32_t* __restrict__ off,
+                           unsigned long long* __restrict__ out /* [8] */) {
+  unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const uint32_t d = off[v + 1] - off[v];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t k = 1u << i;
+      if (d > k) {
+        acc[2 * i] += 1;
+        acc[2 * i + 1] += d - k;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long x = acc[i];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    if ((threadIdx.x & 31u) == 0 && x) atomicAdd(out + i, x);
+  }
+}
+
+// Column-major slab of the first K columns of every row (rows padded to np,
+// sentinel np for absent entries); heavy rows get only sentinels (a separate
+// chunk pass owns them) and, like rows longer than K, their ovf bit.
+__global__ void k_ell_fill(uint32_t n, uint32_t np, const uint32_t* __restrict__ off,
+                           const uint32_t* __restrict__ col, uint32_t K, uint32_t heavy,
+                           uint32_t* __restrict__ ell, uint32_t* __restrict__ ovf) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < np; v0 += stride) {
+    const uint32_t v = v0 + lane;
+    bool over = false;
+    uint32_t b = 0, d = 0;
+    if (v < n) {
+      b = off[v];
+      d = off[v + 1] - b;
+      over = d > K;
+      if (d > heavy) d = 0;
+    }
+    for (uint32_t k = 0; k < K; ++k) ell[(size_t)k * np + v] = k < d ? col[b + k] : np;
+    const uint32_t w = __ballot_sync(kFull, over);
+    if (lane == 0) ovf[v0 >> 5] = w;
+  }
+}
+
 }  // namespace
+
+void build_ell(DevCsr& g, cudaStream_t s) {
+  g.ell_k = 0;
+  g.ell_n = 0;
+  if (!g.n) return;
+  DevBuf h(64, s);
+  CYC_CUDA(cudaMemsetAsync(h.p, 0, 64, s));
+  k_ell_hist<<<grid_for(g.n, 256, 8), 256, 0, s>>>(g.n, g.o(), h.as<unsigned long long>());
+  CYC_LAUNCHED();
+  unsigned long long hh[8];
+  CYC_CUDA(cudaMemcpyAsync(hh, h.p, 64, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  // bytes per dense step: slab reads 4Kn; overflow rows add offsets (8 B) and
+  // their remaining columns (4 B each)
+  uint32_t best_k = 1;
+  double best = 1e300;
+  for (int i = 0; i < 4; ++i) {
+    const double cost = 4.0 * (1u << i) * g.n + 8.0 * (double)hh[2 * i] + 4.0 * (double)hh[2 * i + 1];
+    if (cost < best * 0.97) {  // prefer narrower slabs on near-ties
+      best = cost;
+      best_k = 1u << i;
+    }
+  }
+  g.ell_k = best_k;
+  const uint32_t np = (uint32_t)(((uint64_t)g.n + kRowPad - 1) / kRowPad * kRowPad);
+  g.ell_n = np;
+  g.ell.alloc((size_t)best_k * np * 4, s);
+  const size_t words = (size_t)np / 32 + 1;
+  g.ovf.alloc(words * 4, s);
+  CYC_CUDA(cudaMemsetAsync(g.ovf.p, 0, words * 4, s));
+  k_ell_fill<<<grid_for(np, 256, 8), 256, 0, s>>>(g.n, np, g.o(), g.c(), best_k,
+                                                  g.heavy_deg ? g.heavy_deg : 0xFFFFFFFFu,
+                                                  g.ell.as<uint32_t>(), g.ovf.as<uint32_t>());
+  CYC_LAUNCHED();
+}
 
 int sm_count() {
   static int c = [] {

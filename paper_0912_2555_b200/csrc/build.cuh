@@ -5,6 +5,8 @@
 
 namespace cyc {
 
+constexpr uint32_t kRowPad = 256;  // row padding of map buffers and the HYB slab
+
 // One CSR on the device. Row offsets are u32 (n+1), columns u32 (m).
 struct DevCsr {
   uint32_t n = 0;
@@ -14,6 +16,12 @@ struct DevCsr {
   uint32_t n_heavy_chunks = 0;
   uint32_t heavy_deg = 0;
   uint32_t max_degree = 0;
+  // HYB slab (gather side): the first ell_k columns of every row, column-major
+  // (ell[k*n + v], kNone padded), and bit v of ovf = row v has more than ell_k.
+  // Rows are padded to ell_n (a multiple of kRowPad); padding columns and
+  // absent entries hold the sentinel ell_n, an always-NIL map slot.
+  DevBuf ell, ovf;
+  uint32_t ell_k = 0, ell_n = 0;
   const uint32_t* o() const { return off.as<uint32_t>(); }
   const uint32_t* c() const { return col.as<uint32_t>(); }
 };
@@ -25,5 +33,7 @@ void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* tot
 void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
                DevCsr& out, uint32_t* d_err);
 void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s);
+// Chooses ell_k in {1,2,4,8} minimising per-step pull bytes and builds the slab.
+void build_ell(DevCsr& g, cudaStream_t s);
 
 }  // namespace cyc

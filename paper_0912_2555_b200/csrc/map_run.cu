@@ -8,32 +8,36 @@
 // barriers. No per-step host synchronisation.
 //
 // Jacobi semantics are kept exactly (map_engine.cpp:56-66):
-// after k steps x[v] = max{u in F : path u -> v of length 1..k}. Two step
-// kinds compute the same Jacobi step:
-//   pull  dense over all rows of the gather index, reading P[cur] and
-//         writing P[cur^1] (double buffer); the north_star SpMV in the
-//         (max, vertex-id) semiring. Each lane walks kRows rows in lock-step
-//         so it keeps several independent gathers in flight.
-//   push  only vertices raised in the previous step scatter their frozen
-//         previous-step value with atomicMax into P[cur] in place. A vertex
-//         that did not change cannot change anyone's max, so this equals
-//         the dense step. The frozen value of a raised vertex is the maximum
-//         raise it received in that step, kept per step parity in T[] as
-//         (tag << 32 | value); tags grow monotonically, so T never needs
-//         clearing and "first raise in this step" is a 64-bit atomicMax whose
-//         previous tag is older. The frontier itself is a bitmap per step
-//         parity (no list, no contended counter); vertices of push degree
-//         > kBigDeg go to a short list of kChunk-edge chunks instead.
-// The step kind is chosen on the device from the previous frontier's edge
-// count (push when edges * alpha < m): direction-optimising traversal.
+// after k steps x[v] = max{u in F : path u -> v of length 1..k}. Every step
+// reads the frozen map buffer P[cur] (= x_{k-1}) and produces P[cur^1]
+// (= x_k), which then becomes current. P[cur^1] enters the step holding
+// x_{k-2}, which differs from x_{k-1} exactly at the vertices changed in
+// step k-1 — the frontier, kept as a bitmap. Two step kinds:
+//   pull  dense over all rows of the gather index (the north_star SpMV in
+//         the (max, vertex-id) semiring); each lane walks kRows rows in
+//         lock-step so it keeps several independent gathers in flight.
+//   push  only frontier vertices act: each max-copies its own x_{k-1} into
+//         P[cur^1] and scatters cand = max(x_{k-1}[u], u+1 if accepting) to
+//         its targets with atomicMax. A vertex that did not change cannot
+//         change anyone's max, so this equals the dense step.
+// Both kinds record the vertices they raise in the next frontier bitmap (with
+// a one-bit-per-word summary so a sparse frontier is found without scanning
+// all n/32 words); vertices of push degree > kBigDeg are also split into
+// kChunk-edge chunks expanded by whole warps. The step kind is chosen on the
+// device from the frontier's edge count (push when edges * alpha < m):
+// direction-optimising traversal.
 //
-// Self-witness (map_engine.cpp:66): exact per row in pull; in push the
-// raises to exactly v+1 of accepting v are candidates, confirmed after the
-// barrier when T shows v+1 is that step's maximum raise.
+// Self-witness (map_engine.cpp:66): exact per row in pull; push (and heavy
+// pull rows) record raises to exactly v+1 of accepting v as candidates,
+// confirmed after the barrier by reading the new buffer.
+#include <cooperative_groups.h>
+
 #include <cstring>
 
 #include "../../include/cyc_gen.h"
 #include "map_run.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace cyc {
 
@@ -41,13 +45,13 @@ namespace {
 
 constexpr int kRunThreads = 1024;
 constexpr int kModePull = 1, kModePush = 2;
-constexpr int kRows = 4;         // rows per lane in a pull step
-constexpr int kBatch = 4;        // frontier vertices per lane in a push step
-constexpr int kHeavyPerLane = 8;  // pull heavy chunk = 256 edges
-constexpr uint32_t kTileWords = 8;  // bitmap words per warp tile (256 vertices)
+constexpr int kRows = 4;            // rows per lane in a pull step (the ovf test below assumes 4)
+static_assert(kRows == 4, "pull overflow test unrolled for 4 rows");
+constexpr int kBatch = 4;           // frontier vertices per lane in a push step
+constexpr int kHeavyPerLane = 8;    // pull heavy chunk = 256 edges
 
-__device__ __forceinline__ bool f_bit(const uint32_t* F, uint32_t v) {
-  return (__ldcg(F + (v >> 5)) >> (v & 31u)) & 1u;
+__device__ __forceinline__ bool bit_of(const uint32_t* words, uint32_t v) {
+  return (__ldcg(words + (v >> 5)) >> (v & 31u)) & 1u;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
@@ -56,31 +60,44 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
   return x;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Trace hook: latest time any warp passed phase `ph` of the current step.
+__device__ __forceinline__ void phase_mark(const RunArgs& a, unsigned long long k, int ph) {
+  if (a.trace && k < a.trace_cap && lane_id() == 0) {
+    const uint32_t spread = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) & 15u;
+    atomicMax(a.trace + 64u * k + 16u + 16u * ph + spread, gtimer());
+  }
+}
+
+// candidate value a vertex u with map word w contributes to its successors
 __device__ __forceinline__ uint32_t cand_of(uint32_t w, uint32_t u) {
   return (w & kFlag) ? max(w & kCode, u + 1u) : w;
 }
 
 // ---------------------------------------------------------- block helpers
 struct BlockSh {
-  unsigned long long w[32];
-  unsigned long long bcast[2];
+  unsigned long long w[32][3];
+  unsigned long long bcast;
   uint32_t wmin[33];
-  uint32_t q[kRunThreads / 32][kTileWords * 32];  // per-warp push queues
 };
 
-// Sum over the CTA, result in every thread.
 __device__ unsigned long long block_sum(unsigned long long x, BlockSh* sh) {
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   x = warp_sum64(x);
-  if (lane == 0) sh->w[wid] = x;
+  if (lane == 0) sh->w[wid][0] = x;
   __syncthreads();
   if (wid == 0) {
-    unsigned long long y = lane < nw ? sh->w[lane] : 0ull;
+    unsigned long long y = lane < nw ? sh->w[lane][0] : 0ull;
     y = warp_sum64(y);
-    if (lane == 0) sh->bcast[0] = y;
+    if (lane == 0) sh->bcast = y;
   }
   __syncthreads();
-  const unsigned long long r = sh->bcast[0];
+  const unsigned long long r = sh->bcast;
   __syncthreads();
   return r;
 }
@@ -104,104 +121,220 @@ __device__ uint32_t block_min(uint32_t x, BlockSh* sh) {
 // Per-thread step counters, reduced once per CTA per step.
 struct StepAcc {
   unsigned long long raised = 0;  // successful raises (any > 0 => changed)
-  unsigned long long first = 0;   // distinct vertices raised
-  unsigned long long fedges = 0;  // push degrees of the next frontier
+  unsigned long long first = 0;   // vertices newly entered in the next frontier
+  unsigned long long fedges = 0;  // their push degrees (when known)
 };
 
-__device__ void step_flags(const StepAcc& acc, RunCtl* ctl, uint32_t slot, BlockSh* sh) {
-  const unsigned long long r = block_sum(acc.raised, sh);
-  const unsigned long long c = block_sum(acc.first, sh);
-  const unsigned long long e = block_sum(acc.fedges, sh);
-  if (threadIdx.x == 0) {
-    if (r) *(volatile unsigned int*)&ctl->changed[slot] = 1u;
-    if (c) atomicAdd(&ctl->nraised[slot], (unsigned)c);
-    if (e) atomicAdd(&ctl->fedges[slot], e);
+// One fused 3-value reduction, one flag store and two atomics per CTA.
+__device__ void step_flags(const StepAcc& acc, SlotCtl* sl, BlockSh* sh) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned long long r = warp_sum64(acc.raised), f = warp_sum64(acc.first),
+                           e = warp_sum64(acc.fedges);
+  if (lane == 0) {
+    sh->w[wid][0] = r;
+    sh->w[wid][1] = f;
+    sh->w[wid][2] = e;
   }
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long rr = lane < nw ? sh->w[lane][0] : 0ull;
+    unsigned long long ff = lane < nw ? sh->w[lane][1] : 0ull;
+    unsigned long long ee = lane < nw ? sh->w[lane][2] : 0ull;
+    rr = warp_sum64(rr);
+    ff = warp_sum64(ff);
+    ee = warp_sum64(ee);
+    if (lane == 0) {
+      if (rr) *(volatile unsigned int*)&sl->changed = 1u;
+      if (ff) atomicAdd(&sl->nraised, (unsigned)ff);
+      if (ee) atomicAdd(&sl->fedges, ee);
+    }
+  }
+  __syncthreads();
 }
 
-// Frontier bookkeeping of a vertex v first raised in step `slot`: a bit in
-// the step's bitmap, or kChunk-edge chunks for a big push degree.
-__device__ __forceinline__ void enlist(const RunArgs& a, uint32_t v, uint32_t b, uint32_t e,
-                                       uint32_t* fb, uint4* bc, unsigned int* nchunk) {
-  const uint32_t deg = e - b;
-  if (deg == 0) return;
-  if (deg <= kBigDeg) {
-    atomicOr(fb + (v >> 5), 1u << (v & 31u));
-  } else {
-    const uint32_t nc = (deg + kChunk - 1) / kChunk;
-    const uint32_t base = atomicAdd(nchunk, nc);
-    for (uint32_t c = 0; c < nc && base + c < a.chunk_cap; ++c)
-      bc[base + c] = make_uint4(v, b + c * kChunk, min(e, b + (c + 1) * kChunk), 0u);
-  }
+// Sets bit v of the frontier bitmap (and its summary bit); true iff new.
+__device__ __forceinline__ bool mark(uint32_t* fb, uint32_t* sb, uint32_t v) {
+  const uint32_t w = v >> 5, bit = 1u << (v & 31u);
+  const uint32_t old = atomicOr(fb + w, bit);
+  if (old == 0u) atomicOr(sb + (w >> 5), 1u << (w & 31u));
+  return !(old & bit);
 }
 
-// Batched atomicMax raise of P[tgt[r]] to val[r] (Jacobi push). Written as
-// predicated stages (load, raise, tag, degree, enlist) so the R independent
-// chains overlap instead of running one dependent chain after another. The
-// first raise of a target in step g enlists it in the next frontier.
+// Chunks of a big-degree vertex for the next push step; returns its degree.
+__device__ __forceinline__ uint32_t enlist(const RunArgs& a, uint32_t v, uint4* bc,
+                                           unsigned int* nchunk) {
+  const uint32_t b = __ldg(a.poff + v), e = __ldg(a.poff + v + 1);
+  const uint32_t nc = (e - b + kChunk - 1) / kChunk;
+  const uint32_t base = atomicAdd(nchunk, nc);
+  for (uint32_t c = 0; c < nc && base + c < a.chunk_cap; ++c)
+    bc[base + c] = make_uint4(v, b + c * kChunk, min(e, b + (c + 1) * kChunk), 0u);
+  return e - b;
+}
+
+struct PushCtx {
+  const uint32_t* Pc;  // frozen x_{k-1}
+  uint32_t* Pn;        // x_k under construction
+  uint32_t* fb;        // next frontier
+  uint32_t* sb;
+  uint4* bc;
+  unsigned int* nchunk;
+  uint32_t* Cn;
+  unsigned int* ccnt;
+};
+
+// Batched Jacobi push of val[r] into tgt[r], as predicated stages (read the
+// frozen value, fire-and-forget atomicMax, frontier mark, big-vertex chunks)
+// so the R chains of a lane overlap.
 template <int R>
-__device__ __forceinline__ void raise_batch(const RunArgs& a, uint32_t* P, unsigned long long* Tc,
-                                            uint32_t g, const uint32_t (&tgt)[R],
-                                            const uint32_t (&val)[R], uint32_t* fb, uint4* bc,
-                                            unsigned int* nchunk, uint32_t* Cn, unsigned int* ccnt,
+__device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
+                                            const uint32_t (&tgt)[R], const uint32_t (&val)[R],
                                             StepAcc& acc) {
-  uint32_t old[R], prev[R];
+  uint32_t old[R];
   bool go[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) old[r] = tgt[r] != kNone ? __ldcg(P + tgt[r]) : kCode;
+  for (int r = 0; r < R; ++r) old[r] = tgt[r] != kNone ? __ldca(c.Pc + tgt[r]) : kCode;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     go[r] = tgt[r] != kNone && val[r] > (old[r] & kCode);
-    prev[r] = go[r] ? atomicMax(P + tgt[r], (old[r] & kFlag) | val[r]) : kCode;
+    if (go[r]) atomicMax(c.Pn + tgt[r], (old[r] & kFlag) | val[r]);
   }
-  unsigned long long pt[R];
-  const unsigned long long tag = (unsigned long long)g << 32;
+  bool first[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    go[r] = go[r] && (prev[r] & kCode) < val[r];
-    pt[r] = go[r] ? atomicMax(Tc + tgt[r], tag | val[r]) : tag;
+  for (int r = 0; r < R; ++r) first[r] = go[r] && mark(c.fb, c.sb, tgt[r]);
+  uint32_t bw[R], b[R], e[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {  // one round trip for the big bit and the degree
+    bw[r] = first[r] ? __ldcg(a.bigm + (tgt[r] >> 5)) : 0u;
+    b[r] = first[r] ? __ldg(a.poff + tgt[r]) : 0u;
+    e[r] = first[r] ? __ldg(a.poff + tgt[r] + 1) : 0u;
   }
-  uint32_t b[R], e[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     acc.raised += go[r];
-    const bool first = go[r] && (uint32_t)(pt[r] >> 32) < g;
-    b[r] = first ? __ldg(a.poff + tgt[r]) : 0u;
-    e[r] = first ? __ldg(a.poff + tgt[r] + 1) : 0u;
-    acc.first += first;
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    if (e[r] > b[r]) {
-      acc.fedges += e[r] - b[r];
-      enlist(a, tgt[r], b[r], e[r], fb, bc, nchunk);
-    }
-    if (go[r] && (old[r] & kFlag) && val[r] == tgt[r] + 1u) Cn[atomicAdd(ccnt, 1u)] = tgt[r];
+    acc.first += first[r];
+    acc.fedges += e[r] - b[r];
+    if ((bw[r] >> (tgt[r] & 31u)) & 1u) enlist(a, tgt[r], c.bc, c.nchunk);
+    if (go[r] && (old[r] & kFlag) && val[r] == tgt[r] + 1u) c.Cn[atomicAdd(c.ccnt, 1u)] = tgt[r];
   }
 }
 
+// Summaries rotate over three buffers: step g reads SB[(g-1)%3], writes
+// SB[g%3] and clears SB[(g+1)%3] (last read in step g-1, next written in g+1).
+__device__ __forceinline__ void clear_summary(const RunArgs& a, uint32_t g) {
+  uint32_t* sz = a.SB[(g + 1u) % 3u];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.nsum; i += gridDim.x * blockDim.x)
+    sz[i] = 0u;
+}
+
 // ------------------------------------------------------------------ pull
-__device__ void pull_step(const RunArgs& a, uint32_t g, int cur, bool clear_prev, BlockSh* sh) {
-  const uint32_t slot = g % 3u;
+// Light rows of a pull step. Each lane owns R rows (32*R consecutive rows per
+// warp, rows padded to a multiple of kRowPad so no bound checks). Their first
+// K columns come from the column-major HYB slab; absent entries point at the
+// always-NIL padding slot, so every gather is unconditional and the inner loop
+// is straight-line: one round trip for own values + slab, one for gathers.
+// Rows flagged in `ovf` (longer than K, or heavy) take a slow path.
+template <int K, int R>
+__device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __restrict__ P,
+                                           uint32_t* __restrict__ Q, uint32_t* fb, uint32_t* sb,
+                                           uint32_t* fp, uint4* bc, SlotCtl* sl, StepAcc& acc) {
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t np = a.n_pad;
+  for (uint32_t base = gw * (32u * R); base < np; base += nw * (32u * R)) {
+    uint32_t own[R], best[R];
+    uint32_t anyov = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      own[k] = __ldca(P + base + 32u * k + lane);
+      anyov |= __ldg(a.ovf + (base >> 5) + k);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      uint32_t u[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) u[k] = __ldg(a.ell + (size_t)j * np + base + 32u * k + lane);
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const uint32_t w = __ldca(P + u[k]);
+        const uint32_t c = max(w & kCode, (w >> 31) * (u[k] + 1u));
+        best[k] = j == 0 ? max(own[k] & kCode, c) : max(best[k], c);
+      }
+    }
+    if (K == 0) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) best[k] = own[k] & kCode;
+    }
+    uint32_t skip = 0;  // bit k: heavy row (owned by the chunk pass)
+    if (anyov) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const uint32_t v = base + 32u * k + lane;
+        if ((__ldg(a.ovf + (base >> 5) + k) >> lane) & 1u) {
+          const uint32_t b = __ldg(a.goff + v), e = __ldg(a.goff + v + 1);
+          if (e - b > a.heavy_deg) {
+            skip |= 1u << k;
+          } else {
+            for (uint32_t i = b + K; i < e; ++i) {
+              const uint32_t u = __ldg(a.gcol + i);
+              best[k] = max(best[k], cand_of(__ldca(P + u), u));
+            }
+          }
+        }
+      }
+    }
+    uint32_t words[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const uint32_t v = base + 32u * k + lane;
+      const bool up = !((skip >> k) & 1u) && best[k] > (own[k] & kCode);
+      if (!((skip >> k) & 1u)) Q[v] = (own[k] & kFlag) | best[k];
+      if ((own[k] & kFlag) && best[k] == v + 1u && !((skip >> k) & 1u)) atomicMin(&sl->wit, v);
+      words[k] = __ballot_sync(kFull, up);
+      acc.raised += up;
+      acc.first += up;
+    }
+    // next frontier words (the bitmap is zero at step start; heavy rows are
+    // disjoint): fire-and-forget ORs, previous frontier words consumed
+    if (lane < (uint32_t)R) {
+      uint32_t wd = 0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) wd = lane == (uint32_t)k ? words[k] : wd;
+      const uint32_t wi = (base >> 5) + lane;
+      fp[wi] = 0u;
+      if (wd) {
+        atomicOr(fb + wi, wd);
+        atomicOr(sb + (wi >> 5), 1u << (wi & 31u));
+      }
+    }
+    // raised vertices of big push degree: chunks for the next push step
+    uint32_t big[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) big[k] = words[k] ? __ldcg(a.bigm + (base >> 5) + k) & words[k] : 0u;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if ((big[k] >> lane) & 1u) acc.fedges += enlist(a, base + 32u * k + lane, bc, &sl->nchunk);
+  }
+}
+
+__device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, unsigned long long tk) {
   const uint32_t* __restrict__ P = a.P[cur];
   uint32_t* __restrict__ Q = a.P[cur ^ 1];
-  unsigned long long* Tc = a.T[g & 1u];
+  SlotCtl* sl = &a.ctl->slot[g % 3u];
+  uint32_t* fb = a.FB[g & 1u];
+  uint32_t* sb = a.SB[g % 3u];
+  uint32_t* fp = a.FB[(g - 1u) & 1u];
+  uint4* bc = a.BC[g & 1u];
   uint32_t* Cn = a.C[g & 1u];
-  RunCtl* ctl = a.ctl;
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
-  if (clear_prev) {  // keep the bitmap invariant: FB[(g+1)&1] is zero when step g+1 starts
-    uint32_t* fb = a.FB[(g - 1u) & 1u];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.nwords; i += gridDim.x * blockDim.x)
-      fb[i] = 0u;
-  }
+  clear_summary(a, g);
   // heavy rows first (they are the long poles): one warp per chunk of at
   // most 32*kHeavyPerLane edges, every lane issuing all its loads at once;
-  // combined with atomicMax into Q (Q holds an earlier, never larger, value
-  // of the same fixpoint)
-  for (uint32_t c = gw; c < a.n_heavy; c += nw) {
+  // combined with atomicMax into Q (Q holds x_{k-2}, never larger)
+  for (uint32_t c = nw - 1u - gw; c < a.n_heavy; c += nw) {  // tail warps do fewer light rows
     const uint4 ch = a.heavy[c];
     const uint32_t v = ch.x;
     uint32_t u[kHeavyPerLane];
@@ -213,138 +346,61 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, bool clear_prev
     uint32_t best = 0;
 #pragma unroll
     for (int r = 0; r < kHeavyPerLane; ++r)
-      if (u[r] != kNone) best = max(best, cand_of(__ldcg(P + u[r]), u[r]));
+      if (u[r] != kNone) best = max(best, cand_of(__ldca(P + u[r]), u[r]));
     best = __reduce_max_sync(kFull, best);
     if (lane == 0) {
-      const uint32_t own = __ldcg(P + v);
+      const uint32_t own = __ldca(P + v);
       best = max(best, own & kCode);
       atomicMax(Q + v, (own & kFlag) | best);
       if (best > (own & kCode)) {
         ++acc.raised;
-        const unsigned long long pt = atomicMax(Tc + v, ((unsigned long long)g << 32) | best);
-        acc.first += (uint32_t)(pt >> 32) < g;
-        if ((own & kFlag) && best == v + 1u) Cn[atomicAdd(&ctl->cand_cnt[slot], 1u)] = v;
-      }
-    }
-  }
-  // light rows: each lane owns kRows rows (32*kRows consecutive rows per warp)
-  // and walks their edge lists in lock-step, so every lane keeps up to
-  // 2*kRows independent col/gather loads in flight (latency hiding by ILP).
-  for (uint32_t base = gw * (32u * kRows); base < a.n; base += nw * (32u * kRows)) {
-    uint32_t b[kRows], e[kRows], own[kRows], best[kRows];
-    uint32_t skip = 0;  // bit k: row k is past n or heavy (chunk pass below)
-#pragma unroll
-    for (int k = 0; k < kRows; ++k) {
-      const uint32_t v = base + 32u * k + lane;
-      b[k] = e[k] = 0;
-      if (v < a.n) {
-        b[k] = __ldg(a.goff + v);
-        e[k] = __ldg(a.goff + v + 1);
-        if (e[k] - b[k] > a.heavy_deg) {
-          e[k] = b[k];
-          skip |= 1u << k;
+        if (mark(fb, sb, v)) {
+          ++acc.first;
+          if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk);
         }
-      } else {
-        skip |= 1u << k;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kRows; ++k) {
-      const uint32_t v = base + 32u * k + lane;
-      own[k] = v < a.n ? __ldcg(P + v) : 0u;
-      best[k] = own[k] & kCode;
-    }
-    for (uint32_t j = 0;; j += 2) {
-      uint32_t u0[kRows], u1[kRows];
-      bool any = false;
-#pragma unroll
-      for (int k = 0; k < kRows; ++k) {
-        u0[k] = b[k] + j < e[k] ? __ldg(a.gcol + b[k] + j) : kNone;
-        u1[k] = b[k] + j + 1 < e[k] ? __ldg(a.gcol + b[k] + j + 1) : kNone;
-        any |= b[k] + j < e[k];
-      }
-      if (!any) break;
-#pragma unroll
-      for (int k = 0; k < kRows; ++k) {
-        if (u0[k] != kNone) best[k] = max(best[k], cand_of(__ldcg(P + u0[k]), u0[k]));
-        if (u1[k] != kNone) best[k] = max(best[k], cand_of(__ldcg(P + u1[k]), u1[k]));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kRows; ++k) {
-      const uint32_t v = base + 32u * k + lane;
-      if (!((skip >> k) & 1u)) {
-        Q[v] = (own[k] & kFlag) | best[k];
-        const bool up = best[k] > (own[k] & kCode);
-        acc.raised += up;
-        acc.first += up;
-        if ((own[k] & kFlag) && best[k] == v + 1u) atomicMin(&ctl->wit[slot], v);
+        if ((own & kFlag) && best == v + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
       }
     }
   }
-  step_flags(acc, ctl, slot, sh);
+  phase_mark(a, tk, 0);
+  switch (a.ell_k) {
+    case 1: pull_light<1, 8>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
+    case 2: pull_light<2, 8>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
+    case 4: pull_light<4, 4>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
+    default: pull_light<8, 4>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
+  }
+  phase_mark(a, tk, 1);
+  step_flags(acc, sl, sh);
+  phase_mark(a, tk, 2);
 }
 
-// After a pull step (tag gp), rebuild that step's frontier from the two
-// buffers so a push step can follow: T values, bitmap words, big chunks.
-__device__ void transition_pass(const RunArgs& a, uint32_t gp, int cur, BlockSh* sh) {
-  const uint32_t* P = a.P[cur];
-  const uint32_t* Q = a.P[cur ^ 1];
-  unsigned long long* Tp = a.T[gp & 1u];
-  uint32_t* fb = a.FB[gp & 1u];
-  uint4* bc = a.BC[gp & 1u];
-  unsigned int* nchunk = &a.ctl->nchunk[gp % 3u];
+// ------------------------------------------------------------------ push
+__device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, unsigned long long tk) {
+  SlotCtl* sl = &a.ctl->slot[g % 3u];
+  const SlotCtl* pl = &a.ctl->slot[(g - 1u) % 3u];
+  PushCtx c;
+  c.Pc = a.P[cur];
+  c.Pn = a.P[cur ^ 1];
+  c.fb = a.FB[g & 1u];
+  c.sb = a.SB[g % 3u];
+  c.bc = a.BC[g & 1u];
+  c.nchunk = &sl->nchunk;
+  c.Cn = a.C[g & 1u];
+  c.ccnt = &sl->cand_cnt;
+  uint32_t* fp = a.FB[(g - 1u) & 1u];
+  const uint32_t* sp = a.SB[(g - 1u) % 3u];
+  const uint4* bp = a.BC[(g - 1u) & 1u];
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
-  for (uint32_t wi = gw; wi < a.nwords; wi += nw) {
-    const uint32_t v = wi * 32u + lane;
-    bool small = false;
-    if (v < a.n) {
-      const uint32_t xb = __ldcg(P + v) & kCode, xa = __ldcg(Q + v) & kCode;
-      if (xb != xa) {
-        Tp[v] = ((unsigned long long)gp << 32) | xb;
-        const uint32_t b = __ldg(a.poff + v), e = __ldg(a.poff + v + 1);
-        acc.fedges += e - b;
-        small = e > b && e - b <= kBigDeg;
-        if (e - b > kBigDeg) enlist(a, v, b, e, fb, bc, nchunk);
-      }
-    }
-    const uint32_t word = __ballot_sync(kFull, small);
-    if (lane == 0) fb[wi] = word;
-  }
-  const unsigned long long fe = block_sum(acc.fedges, sh);
-  if (threadIdx.x == 0 && fe) atomicAdd(&a.ctl->fedges[gp % 3u], fe);
-}
-
-// ------------------------------------------------------------------ push
-__device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh) {
-  const uint32_t slot = g % 3u, pslot = (g - 1u) % 3u;
-  RunCtl* ctl = a.ctl;
-  uint32_t* fp = a.FB[(g - 1u) & 1u];
-  const uint4* bp = a.BC[(g - 1u) & 1u];
-  const unsigned long long* Tp = a.T[(g - 1u) & 1u];
-  unsigned long long* Tc = a.T[g & 1u];
-  uint32_t* fb = a.FB[g & 1u];
-  uint4* bc = a.BC[g & 1u];
-  unsigned int* nchunk = &ctl->nchunk[slot];
-  unsigned int* ccnt = &ctl->cand_cnt[slot];
-  uint32_t* Cn = a.C[g & 1u];
-  uint32_t* P = a.P[cur];
-  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  uint32_t* q = sh->q[wid];
-  StepAcc acc;
+  clear_summary(a, g);
   // big frontier vertices first: one warp per kChunk-edge chunk, each lane
   // raising kChunk/32 targets as one batch
-  const uint32_t nch = min(__ldcg(&ctl->nchunk[pslot]), a.chunk_cap);
-  for (uint32_t c = gw; c < nch; c += nw) {
-    const uint4 ch = bp[c];
-    const uint32_t v = ch.x;
-    uint32_t vv = (uint32_t)__ldcg(Tp + v);
-    if (f_bit(a.F, v)) vv = max(vv, v + 1u);
+  const uint32_t nch = min(__ldcg(&pl->nchunk), a.chunk_cap);
+  for (uint32_t k = gw; k < nch; k += nw) {
+    const uint4 ch = bp[k];
+    const uint32_t vv = cand_of(__ldca(c.Pc + ch.x), ch.x);
     uint32_t t[kChunk / 32], val[kChunk / 32];
 #pragma unroll
     for (int r = 0; r < (int)(kChunk / 32); ++r) {
@@ -352,55 +408,55 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh) {
       t[r] = i < ch.z ? __ldg(a.pcol + i) : kNone;
       val[r] = vv;
     }
-    raise_batch(a, P, Tc, g, t, val, fb, bc, nchunk, Cn, ccnt, acc);
+    raise_batch(a, c, t, val, acc);
   }
-  // small frontier vertices, from the bitmap (each word read once and cleared)
-  for (uint32_t wb = gw * kTileWords; wb < a.nwords; wb += nw * kTileWords) {
-    uint32_t word = 0;
-    const uint32_t wi = wb + lane;
-    if (lane < kTileWords && wi < a.nwords) {
-      word = __ldcg(fp + wi);
-      if (word) fp[wi] = 0u;
-    }
-    const uint32_t c = __popc(word);
-    const uint32_t incl = warp_incl_scan(c);
-    const uint32_t total = __shfl_sync(kFull, incl, 31);
-    if (total == 0) continue;
-    uint32_t pos = incl - c;
-    while (word) {
-      q[pos++] = wi * 32u + (uint32_t)(__ffs(word) - 1);
-      word &= word - 1u;
+  phase_mark(a, tk, 0);
+  // every frontier vertex: max-copy itself into the new buffer, and push its
+  // edges unless it is big (chunks above). Warps take 4 consecutive bitmap
+  // words per iteration, interleaved over the grid (a contiguous wave of
+  // raised ids spreads over many warps); lane i owns bit i of each word.
+  // Words are cleared by their owner; the summary is cleared a step later.
+  for (uint32_t it = gw; it * 4u < a.nwords; it += nw) {
+    const uint32_t w0 = it * 4u;
+    const uint32_t m4 = (__ldca(sp + (w0 >> 5)) >> (w0 & 31u)) & 0xFu;
+    if (!m4) continue;
+    uint32_t v[kBatch], b[kBatch], e[kBatch], val[kBatch];
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const uint32_t wd = ((m4 >> r) & 1u) ? __ldcg(fp + w0 + r) : 0u;
+      v[r] = (wd >> lane) & 1u ? (w0 + r) * 32u + lane : kNone;
     }
     __syncwarp();
-    for (uint32_t k0 = 0; k0 < total; k0 += 32u * kBatch) {
-      uint32_t v[kBatch], b[kBatch], e[kBatch], val[kBatch];
+    if (lane < 4u && ((m4 >> lane) & 1u)) fp[w0 + lane] = 0u;
 #pragma unroll
-      for (int r = 0; r < kBatch; ++r) {
-        const uint32_t k = k0 + 32u * r + lane;
-        v[r] = k < total ? q[k] : kNone;
-        b[r] = v[r] != kNone ? __ldg(a.poff + v[r]) : 0u;
-        e[r] = v[r] != kNone ? __ldg(a.poff + v[r] + 1) : 0u;
-      }
-#pragma unroll
-      for (int r = 0; r < kBatch; ++r) {
-        val[r] = v[r] != kNone ? (uint32_t)__ldcg(Tp + v[r]) : 0u;
-        if (v[r] != kNone && f_bit(a.F, v[r])) val[r] = max(val[r], v[r] + 1u);
-      }
-      for (uint32_t j = 0;; ++j) {
-        uint32_t t[kBatch];
-        bool any = false;
-#pragma unroll
-        for (int r = 0; r < kBatch; ++r) {
-          t[r] = b[r] + j < e[r] ? __ldg(a.pcol + b[r] + j) : kNone;
-          any |= t[r] != kNone;
-        }
-        if (!any) break;
-        raise_batch(a, P, Tc, g, t, val, fb, bc, nchunk, Cn, ccnt, acc);
+    for (int r = 0; r < kBatch; ++r) {
+      b[r] = e[r] = 0u;
+      val[r] = 0u;
+      if (v[r] != kNone) {  // all four loads in one round trip
+        const uint32_t xu = __ldca(c.Pc + v[r]);
+        const uint32_t bwv = __ldcg(a.bigm + (v[r] >> 5));
+        b[r] = __ldg(a.poff + v[r]);
+        e[r] = __ldg(a.poff + v[r] + 1);
+        atomicMax(c.Pn + v[r], xu);  // bring x_{k-2} up to x_{k-1}
+        val[r] = cand_of(xu, v[r]);
+        if ((bwv >> (v[r] & 31u)) & 1u) e[r] = b[r];  // big: chunks push its edges
       }
     }
-    __syncwarp();
+    for (uint32_t j = 0;; ++j) {
+      uint32_t t[kBatch];
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < kBatch; ++r) {
+        t[r] = b[r] + j < e[r] ? __ldg(a.pcol + b[r] + j) : kNone;
+        any |= t[r] != kNone;
+      }
+      if (!any) break;
+      raise_batch(a, c, t, val, acc);
+    }
   }
-  step_flags(acc, ctl, slot, sh);
+  phase_mark(a, tk, 1);
+  step_flags(acc, sl, sh);
+  phase_mark(a, tk, 2);
 }
 
 // ------------------------------------------------------- iteration passes
@@ -473,60 +529,71 @@ __device__ void demote_pass(const RunArgs& a, unsigned int* dcount, unsigned lon
 }
 
 // Start of a fixpoint (setup tag g): both map buffers all-NIL with the
-// accepting bit; the initial frontier = every accepting vertex, value id+1
-// (bitmap FB[g&1] written in full, FB[(g+1)&1] cleared).
+// accepting bit; the initial frontier is the accepting set itself (every
+// accepting u offers cand = u+1), FB[(g+1)&1] / SB[(g+1)&1] cleared.
 __device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
-  unsigned long long* Tg = a.T[g & 1u];
   uint32_t* fb = a.FB[g & 1u];
+  uint32_t* sb = a.SB[g % 3u];
   uint32_t* fz = a.FB[(g + 1u) & 1u];
+  uint32_t* sz = a.SB[(g + 1u) % 3u];
+  SlotCtl* sl = &a.ctl->slot[g % 3u];
   uint4* bc = a.BC[g & 1u];
-  unsigned int* nchunk = &a.ctl->nchunk[g % 3u];
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  StepAcc acc;
-  for (uint32_t wi = gw; wi < a.nwords; wi += nw) {
-    const uint32_t v = wi * 32u + lane;
-    bool small = false;
-    if (v < a.n) {
-      const bool accv = f_bit(a.F, v);
-      const uint32_t val = accv ? kFlag : 0u;
-      a.P[0][v] = val;
-      a.P[1][v] = val;
-      if (accv) {
-        const uint32_t b = __ldg(a.poff + v), e = __ldg(a.poff + v + 1);
-        if (e > b) Tg[v] = ((unsigned long long)g << 32) | (v + 1u);
-        acc.fedges += e - b;
-        small = e > b && e - b <= kBigDeg;
-        if (e - b > kBigDeg) enlist(a, v, b, e, fb, bc, nchunk);
-      }
-    }
-    const uint32_t word = __ballot_sync(kFull, small);
-    if (lane == 0) {
-      fb[wi] = word;
+  unsigned long long fe = 0;
+  // 32 words (1024 vertices) per warp iteration: one summary word each
+  for (uint32_t s = gw; s < a.nsum; s += nw) {
+    const uint32_t wi = s * 32u + lane;
+    const uint32_t f = wi < a.nwords ? __ldcg(a.F + wi) : 0u;
+    if (wi < a.nwords) {
+      fb[wi] = f;
       fz[wi] = 0u;
     }
+    const uint32_t sw = __ballot_sync(kFull, f != 0u);
+    if (lane == 0) {
+      sb[s] = sw;
+      sz[s] = 0u;
+    }
+    for (uint32_t j = 0; j < 32u; ++j) {
+      const uint32_t fj = __shfl_sync(kFull, f, j);
+      const uint32_t v = (s * 32u + j) * 32u + lane;
+      if (v < a.n) {
+        const bool accv = (fj >> lane) & 1u;
+        const uint32_t val = accv ? kFlag : 0u;
+        a.P[0][v] = val;
+        a.P[1][v] = val;
+        if (accv) {
+          if (bit_of(a.bigm, v)) {
+            fe += enlist(a, v, bc, &sl->nchunk);
+          } else {
+            fe += __ldg(a.poff + v + 1) - __ldg(a.poff + v);
+          }
+        }
+      }
+    }
   }
-  const unsigned long long fe = block_sum(acc.fedges, sh);
-  if (threadIdx.x == 0 && fe) atomicAdd(&a.ctl->fedges[g % 3u], fe);
+  fe = block_sum(fe, sh);
+  if (threadIdx.x == 0 && fe) atomicAdd(&sl->fedges, fe);
 }
 
 __device__ __forceinline__ void reset_slot(RunCtl* c, uint32_t s) {
-  c->fedges[s] = 0;
-  c->nchunk[s] = 0;
-  c->cand_cnt[s] = 0;
-  c->wit[s] = kNone;
-  c->changed[s] = 0;
-  c->nraised[s] = 0;
+  SlotCtl& sl = c->slot[s];
+  sl.fedges = 0;
+  sl.nraised = 0;
+  sl.changed = 0;
+  sl.nchunk = 0;
+  sl.cand_cnt = 0;
+  sl.wit = kNone;
 }
 
 __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
   __shared__ BlockSh sh;
   // run statistics live in shared memory of block 0 (kept out of registers)
   __shared__ unsigned long long stat[kResTag + 1];
+  cg::grid_group grid = cg::this_grid();
   RunCtl* ctl = a.ctl;
-  unsigned long long epoch = 0;
-  uint32_t g = a.tag0;
+  uint32_t g = 1;
   int cur = 0;
   int cycle = 0;
   uint32_t witness = kNone;
@@ -542,13 +609,13 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
   demote_pass(a, nullptr, &ctl->it_fsize[0], &sh);
   if (lead) reset_slot(ctl, (g + 1u) % 3u);
   reset_pass(a, g, &sh);
-  grid_sync(&ctl->bar, epoch);
+  grid.sync();
   uint64_t t = 0;
   bool truncated = false;
   if (__ldcg(&ctl->it_fsize[0]) != 0) {
     for (;;) {
       unsigned long long steps = 0;
-      bool prev_push = true;  // a frontier (bitmap + chunks) of the previous tag exists
+      bool prev_push = true;  // the previous tag's fedges is exact (push or setup)
       for (;;) {
         ++g;
         ++steps;
@@ -558,56 +625,55 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
         if (mode != kModePull && mode != kModePush) {
           unsigned long long est;
           if (prev_push) {
-            est = __ldcg(&ctl->fedges[pslot]);
-          } else {
-            const unsigned long long nr = __ldcg(&ctl->nraised[pslot]);
-            est = a.n ? nr * a.m / a.n : 0;
+            est = __ldcg(&ctl->slot[pslot].fedges);
+          } else {  // pull steps count big-vertex degrees exactly, the rest by average
+            const unsigned long long nr = __ldcg(&ctl->slot[pslot].nraised);
+            est = __ldcg(&ctl->slot[pslot].fedges) + (a.n ? nr * a.m / a.n : 0);
           }
           mode = (est * a.alpha < a.m) ? kModePush : kModePull;
         }
+        // trace slot of this step (every block derives the same index from the tag)
+        const unsigned long long tkk = (unsigned long long)(g - 2u);
+        if (a.trace && lead && tkk < a.trace_cap) a.trace[64u * tkk + 3u] = gtimer();
         if (mode == kModePush) {
-          if (!prev_push) {
-            transition_pass(a, g - 1u, cur, &sh);
-            grid_sync(&ctl->bar, epoch);
-          }
           if (lead) {
-            const unsigned long long fe = __ldcg(&ctl->fedges[pslot]);
+            const unsigned long long fe = __ldcg(&ctl->slot[pslot].fedges);
+            const unsigned long long nr = __ldcg(&ctl->slot[pslot].nraised);
             stat[kResEdges] += fe;
-            stat[kResRows] += __ldcg(&ctl->nraised[pslot]);
-            stat[kResBytes] += 8ull * fe + 12ull * __ldcg(&ctl->nraised[pslot]);
+            stat[kResRows] += nr;
+            stat[kResBytes] += 8ull * fe + 12ull * nr;
             stat[kResPushSteps] += 1;
           }
-          push_step(a, g, cur, &sh);
+          push_step(a, g, cur, &sh, a.trace ? tkk : ~0ull);
         } else {
           CYC_STAT(kResEdges, a.m);
           CYC_STAT(kResRows, a.n);
           CYC_STAT(kResBytes, 8ull * a.m + 12ull * a.n + 4ull);
           CYC_STAT(kResPullSteps, 1);
-          pull_step(a, g, cur, prev_push, &sh);
+          pull_step(a, g, cur, &sh, a.trace ? tkk : ~0ull);
         }
-        grid_sync(&ctl->bar, epoch);
-        if (lead && a.trace) {
-          const unsigned long long k = stat[kResPullSteps] + stat[kResPushSteps] - 1u;
-          if (k < a.trace_cap) {
-            unsigned long long* tr = a.trace + 4u * k;
-            tr[0] = ((unsigned long long)mode << 32) | (uint32_t)steps;
-            tr[1] = mode == kModePush ? __ldcg(&ctl->fedges[pslot]) : a.m;
-            tr[2] = __ldcg(&ctl->nraised[slot]);
-            tr[3] = clock64();
-          }
-        }
-        if (mode == kModePull) cur ^= 1;
+        grid.sync();
+        cur ^= 1;
         prev_push = mode == kModePush;
-        const uint32_t changed = __ldcg(&ctl->changed[slot]);
-        uint32_t w = __ldcg(&ctl->wit[slot]);
-        const uint32_t nc = __ldcg(&ctl->cand_cnt[slot]);
+        const SlotCtl* sl = &ctl->slot[slot];
+        const uint32_t changed = __ldcg(&sl->changed);
+        uint32_t w = __ldcg(&sl->wit);
+        const uint32_t nc = __ldcg(&sl->cand_cnt);
+        if (lead && a.trace && tkk < a.trace_cap) {
+          unsigned long long* tr = a.trace + 64u * tkk;
+          tr[0] = ((unsigned long long)mode << 60) |
+                  ((unsigned long long)__ldcg(&ctl->slot[pslot].nchunk) << 24) | (steps & 0xFFFFFFull);
+          tr[1] = mode == kModePush ? __ldcg(&ctl->slot[pslot].fedges) : a.m;
+          tr[2] = __ldcg(&sl->nraised);
+          tr[7] = gtimer();
+        }
         if (nc && a.early_exit) {
           const uint32_t* Cn = a.C[g & 1u];
-          const unsigned long long* Tc = a.T[g & 1u];
+          const uint32_t* Pn = a.P[cur];
           uint32_t mine = kNone;
           for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
             const uint32_t c = __ldcg(Cn + i);
-            if (__ldcg(Tc + c) == (((unsigned long long)g << 32) | (c + 1u))) mine = min(mine, c);
+            if ((__ldcg(Pn + c) & kCode) == c + 1u) mine = min(mine, c);
           }
           w = min(w, block_min(mine, &sh));
         }
@@ -629,7 +695,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
         break;
       }
       finish_pass(a, cur, t, !cycle, &sh);
-      grid_sync(&ctl->bar, epoch);
+      grid.sync();
       if (!a.early_exit) {
         const uint32_t fw = __ldcg(&ctl->it_finwit[t & 1u]);
         if (fw != kNone) {
@@ -646,7 +712,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
       if (cycle) break;
       if (a.max_iterations && t + 1 >= a.max_iterations) break;
       demote_pass(a, &ctl->it_dcount[t & 1u], &ctl->it_fsize[(t + 1u) & 1u], &sh);
-      grid_sync(&ctl->bar, epoch);
+      grid.sync();
       const uint32_t dc = __ldcg(&ctl->it_dcount[t & 1u]);
       CYC_STAT(kResDemoted, dc);
       if (dc == 0) break;                                      // D empty: no cycle
@@ -655,7 +721,8 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
       ++g;
       if (lead) reset_slot(ctl, (g + 1u) % 3u);
       reset_pass(a, g, &sh);
-      grid_sync(&ctl->bar, epoch);
+      cur = 0;
+      grid.sync();
     }
   }
   if (lead) {
@@ -666,6 +733,19 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
     for (int k = 0; k <= kResTag; ++k) ctl->res[k] = stat[k];
   }
 #undef CYC_STAT
+}
+
+__global__ void k_big_mask(uint32_t n, const uint32_t* __restrict__ poff, uint32_t* __restrict__ bigm) {
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nwords = (n + 31u) / 32u;
+  for (uint32_t wi = gw; wi < nwords; wi += nw) {
+    const uint32_t v = wi * 32u + lane;
+    const bool big = v < n && __ldg(poff + v + 1) - __ldg(poff + v) > kBigDeg;
+    const uint32_t word = __ballot_sync(kFull, big);
+    if (lane == 0) bigm[wi] = word;
+  }
 }
 
 __global__ void k_strip(const uint32_t* __restrict__ P, uint32_t n, uint32_t* __restrict__ out) {
@@ -733,27 +813,35 @@ __global__ void k_demote_list(uint32_t nwords, const uint32_t* __restrict__ acc,
 
 }  // namespace
 
-void RunWs::ensure(uint32_t nn, uint32_t mm, cudaStream_t s) {
+void RunWs::ensure(uint32_t nn, uint32_t mm, const uint32_t* poff, cudaStream_t s) {
   if (ctl.p && n == nn && m == mm) return;
   n = nn;
   m = mm;
-  const size_t n1 = (size_t)nn + 1;
-  const size_t words = ((size_t)nn + 63) / 64 * 2 + 2;
-  // a vertex of push degree d > kBigDeg >= ... yields ceil(d/kChunk) <= d/kChunk + 1 chunks
+  n_pad = (uint32_t)(((uint64_t)nn + kRowPad - 1) / kRowPad * kRowPad);
+  const size_t np1 = (size_t)n_pad + 1;
+  const size_t words = (size_t)n_pad / 32 + 2;
+  const size_t sums = words / 32 + 2;
+  // a vertex of push degree d > kBigDeg yields ceil(d/kChunk) <= d/kChunk + 1 chunks
   chunk_cap = (uint32_t)((uint64_t)mm / kChunk + (uint64_t)mm / (kBigDeg + 1) + 16);
+  for (int k = 0; k < 3; ++k) SB[k].alloc(sums * 4, s);
   for (int k = 0; k < 2; ++k) {
-    P[k].alloc(n1 * 4, s);
-    T[k].alloc(n1 * 8, s);
+    P[k].alloc(np1 * 4, s);
+    CYC_CUDA(cudaMemsetAsync(P[k].p, 0, np1 * 4, s));  // padding rows stay NIL forever
     FB[k].alloc(words * 4, s);
     BC[k].alloc((size_t)chunk_cap * sizeof(uint4), s);
-    C[k].alloc(n1 * 4, s);
-    CYC_CUDA(cudaMemsetAsync(T[k].p, 0, n1 * 8, s));
+    C[k].alloc(np1 * 4, s);
   }
   F.alloc(words * 4, s);
   used.alloc(words * 4, s);
+  bigm.alloc(words * 4, s);
+  CYC_CUDA(cudaMemsetAsync(F.p, 0, words * 4, s));
   CYC_CUDA(cudaMemsetAsync(used.p, 0, words * 4, s));
+  CYC_CUDA(cudaMemsetAsync(bigm.p, 0, words * 4, s));
+  if (nn) {
+    k_big_mask<<<grid_for((uint64_t)nn, 256, 8), 256, 0, s>>>(nn, poff, bigm.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
   ctl.alloc(sizeof(RunCtl), s);
-  tag = 1;
 }
 
 void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early_exit, int mode,
@@ -761,14 +849,9 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
                     uint32_t alpha, unsigned long long cap, uint32_t trace_cap, cudaStream_t s,
                     cudaEvent_t e0, cudaEvent_t e1, RunOut& out) {
   const uint32_t n = gath.n;
-  // Tags are u32: restart them (and clear T) long before they could wrap.
-  if (ws.tag > 0xF0000000u) {
-    for (int k = 0; k < 2; ++k) CYC_CUDA(cudaMemsetAsync(ws.T[k].p, 0, ((size_t)n + 1) * 8, s));
-    ws.tag = 1;
-  }
   RunCtl init;
   std::memset(&init, 0, sizeof init);
-  for (int k = 0; k < 3; ++k) init.wit[k] = kNone;
+  for (int k = 0; k < 3; ++k) init.slot[k].wit = kNone;
   for (int k = 0; k < 2; ++k) init.it_finwit[k] = kNone;
   CYC_CUDA(cudaMemcpyAsync(ws.ctl.p, &init, sizeof init, cudaMemcpyHostToDevice, s));
   CYC_CUDA(cudaMemsetAsync(ws.used.p, 0, ws.used.bytes, s));
@@ -781,21 +864,27 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
   a.m = gath.m;
   a.goff = gath.o();
   a.gcol = gath.c();
+  a.ell = gath.ell.as<uint32_t>();
+  a.ovf = gath.ovf.as<uint32_t>();
+  a.ell_k = gath.ell_k;
+  a.n_pad = ws.n_pad;
   a.poff = snap.o();
   a.pcol = snap.c();
+  a.bigm = ws.bigm.as<uint32_t>();
   a.heavy = gath.heavy.as<uint4>();
   a.n_heavy = gath.n_heavy_chunks;
   a.heavy_deg = gath.heavy_deg ? gath.heavy_deg : 0xFFFFFFFFu;
   for (int k = 0; k < 2; ++k) {
     a.P[k] = ws.P[k].as<uint32_t>();
-    a.T[k] = ws.T[k].as<unsigned long long>();
     a.FB[k] = ws.FB[k].as<uint32_t>();
     a.BC[k] = ws.BC[k].as<uint4>();
     a.C[k] = ws.C[k].as<uint32_t>();
   }
+  for (int k = 0; k < 3; ++k) a.SB[k] = ws.SB[k].as<uint32_t>();
   a.F = ws.F.as<uint32_t>();
   a.used = ws.used.as<uint32_t>();
   a.nwords = (uint32_t)(((uint64_t)n + 31) / 32);
+  a.nsum = (a.nwords + 31) / 32;
   a.chunk_cap = ws.chunk_cap;
   a.ctl = ws.ctl.as<RunCtl>();
   a.iter_hash = cap ? ws.hist.as<unsigned long long>() : nullptr;
@@ -803,16 +892,15 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
   a.cap = cap;
   a.max_iterations = max_iterations;
   a.max_steps = max_steps;
-  a.tag0 = ws.tag;
+  a.alpha = alpha ? alpha : 24u;
+  a.early_exit = early_exit;
+  a.mode = mode;
   if (trace_cap) {
-    if (ws.trace.bytes < (size_t)trace_cap * 32) ws.trace.alloc((size_t)trace_cap * 32, s);
+    if (ws.trace.bytes < (size_t)trace_cap * 512) ws.trace.alloc((size_t)trace_cap * 512, s);
+    CYC_CUDA(cudaMemsetAsync(ws.trace.p, 0, (size_t)trace_cap * 512, s));
     a.trace = ws.trace.as<unsigned long long>();
     a.trace_cap = trace_cap;
   }
-  ws.trace_cap = trace_cap;
-  a.alpha = alpha ? alpha : 16u;
-  a.early_exit = early_exit;
-  a.mode = mode;
 
   static int blocks_per_sm = -1;
   if (blocks_per_sm < 0) {
@@ -833,11 +921,8 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
   CYC_CUDA(cudaEventElapsedTime(&out.ms, e0, e1));
   out.grid = grid.x;
   out.block = block.x;
-  ws.tag = (uint32_t)host.res[kResTag] + 1u;
-  {
-    const unsigned long long k = host.res[kResPullSteps] + host.res[kResPushSteps];
-    ws.trace_len = (uint32_t)(k < trace_cap ? k : trace_cap);
-  }
+  const unsigned long long k = host.res[kResTag];  // trace slots are indexed by step tag
+  ws.trace_len = (uint32_t)(k < trace_cap ? k : trace_cap);
 }
 
 void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream_t s) {

@@ -10,17 +10,22 @@ namespace cyc {
 constexpr uint32_t kBigDeg = 32;
 constexpr uint32_t kChunk = 128;
 
+// Per-step counters (32 bytes, read back with two vector loads).
+struct alignas(32) SlotCtl {
+  unsigned long long fedges;  // push degrees of the vertices first raised in the step
+  unsigned int nraised;       // vertices raised
+  unsigned int changed;
+  unsigned int nchunk;        // big-vertex chunks enlisted for the next step
+  unsigned int cand_cnt;      // self-witness candidates
+  unsigned int wit;           // exact min self-witness (pull rows)
+  unsigned int pad;
+};
+
 // Control block of one k_map_run launch. Per-step counters rotate over three
 // slots (step g writes slot g%3, reads slot (g-1)%3, and clears slot (g+1)%3),
-// per-iteration counters over two. The grid barrier sits on its own lines.
+// per-iteration counters over two.
 struct RunCtl {
-  GridBar bar;
-  unsigned long long fedges[3];  // sum of push degrees of the step's frontier
-  unsigned int nchunk[3];        // big-vertex chunks of the step's frontier
-  unsigned int cand_cnt[3];      // self-witness candidates appended
-  unsigned int wit[3];           // exact min self-witness (pull rows)
-  unsigned int changed[3];
-  unsigned int nraised[3];
+  SlotCtl slot[3];
   unsigned long long it_hash[2];
   unsigned int it_finwit[2];
   unsigned int it_dcount[2];
@@ -39,36 +44,39 @@ struct RunArgs {
   const uint32_t* gcol;
   const uint32_t* poff;  // snapshot relation (push): row u = targets u flows into
   const uint32_t* pcol;
+  const uint32_t* bigm;  // bit v: push degree of v > kBigDeg
+  const uint32_t* ell;   // HYB slab of the gather index (column-major, ell_k wide)
+  const uint32_t* ovf;   // bit v: gather row v is longer than ell_k (or heavy)
+  uint32_t ell_k;
+  uint32_t n_pad;        // rows padded to kRowPad; P[n_pad] is the NIL sentinel slot
   const uint4* heavy;    // gather rows longer than heavy_deg, split into chunks
   uint32_t n_heavy, heavy_deg;
   uint32_t* P[2];                  // packed map words: accepting<<31 | code
-  unsigned long long* T[2];        // (step tag << 32) | value raised in that step
-  uint32_t* FB[2];                 // frontier bitmaps (raised, 0 < push degree <= kBigDeg)
+  uint32_t* FB[2];                 // frontier bitmaps: vertices changed in the step
+  uint32_t* SB[3];                 // summary bitmaps: bit w = FB word w is non-zero
   uint4* BC[2];                    // frontier chunks {v, beg, end} of big-degree vertices
   uint32_t* C[2];                  // self-witness candidates
   uint32_t* F;                     // accepting set, u32 words (demoted in place)
   uint32_t* used;                  // scratch bitmap, zero between iterations
-  uint32_t nwords;
+  uint32_t nwords, nsum;           // FB words, SB words
   uint32_t chunk_cap;
   RunCtl* ctl;
   unsigned long long* iter_hash;
   unsigned long long* iter_steps;
   unsigned long long cap;
   unsigned long long max_iterations, max_steps;
-  uint32_t tag0;                   // first step tag of this launch (tags only grow)
-  unsigned long long* trace;       // optional per-step record {mode|steps, edges, raised, clock}
+  unsigned long long* trace;       // optional per-step record {mode|step, edges, raised, clock}
   uint32_t trace_cap;
   uint32_t alpha;
   int early_exit, mode;
 };
 
 struct RunWs {
-  uint32_t n = 0, m = 0;
-  DevBuf P[2], T[2], FB[2], BC[2], C[2], F, used, ctl, hist, trace;
-  uint32_t trace_cap = 0, trace_len = 0;
+  uint32_t n = 0, m = 0, n_pad = 0;
+  DevBuf P[2], FB[2], SB[3], BC[2], C[2], F, used, bigm, ctl, hist, trace;
   uint32_t chunk_cap = 0;
-  uint32_t tag = 1;
-  void ensure(uint32_t n, uint32_t m, cudaStream_t s);
+  uint32_t trace_len = 0;
+  void ensure(uint32_t n, uint32_t m, const uint32_t* poff, cudaStream_t s);
 };
 
 struct RunOut {
