@@ -93,6 +93,13 @@ void* cyc_ctx_stream(cyc_ctx* ctx);
  * and its reverse (the MaxPropagation gather index, map_engine.cpp:9-19). */
 cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
                            const uint64_t* acc_words, int orientation, cyc_graph** out);
+/* Device copy of an already-built snapshot (reference CsrSnapshot layout:
+ * row_offsets n+1 u64, col_indices m u32 sorted per row, accepting words):
+ * the entry point for callers that hold a CsrSnapshot (run_map takes one,
+ * map_engine.hpp:111). The gather index is derived on the device. */
+cyc_status cyc_graph_from_csr(cyc_ctx* ctx, const uint64_t* row_offsets, const uint32_t* col_indices,
+                              uint32_t n, uint64_t m, const uint64_t* acc_words, int orientation,
+                              cyc_graph** out);
 /* restrict_to_accepting_sccs (graph.hpp:103-114, graph.cpp:190-221). */
 cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out);
 void cyc_graph_destroy(cyc_graph* g);

@@ -1,0 +1,210 @@
+// cycheck_b200.hpp — C++ drop-in for the reference's MAP hot path.
+//
+// Header-only C++17 over the C ABI in cycheck_b200.h. The functions mirror
+// /root/reference/proj/include/cycheck/{graph,map_engine}.hpp one for one and
+// are templated on the caller's own types, so the reference's call sites
+// (tools/cycheck_main.cpp:88-97, src/explore.cpp:71-124) switch by
+// qualifying the call and keeping their CsrSnapshot / EdgeLog / Bitset /
+// MapOptions / Verdict / MapStats:
+//
+//     cycheck::b200::Engine gpu;                               // cuda:0
+//     auto snap = cycheck::b200::build_snapshot(gpu, log, Orientation::transposed);
+//     auto [verdict, stats] = cycheck::b200::run_map<Verdict, MapStats>(snap, accepting, opts);
+//
+// Requirements on the templated types are exactly the reference members used
+// below (EdgeLog::edge/edge_count/vertex_count/accepting_prefix, Bitset::
+// words/size, CsrSnapshot::{n,m,row_offsets,col_indices,accepting,
+// orientation}, MapOptions::early_exit, Verdict::cycle/no_cycle, MapStats::
+// {iterations,kernel_calls,demoted_total,cycle_witness}). Errors surface as
+// the reference's exception types when the caller names them (template
+// parameters ContractErr / ResourceErr), std::runtime_error otherwise.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "cycheck_b200.h"
+
+namespace cycheck {
+namespace b200 {
+
+struct DefaultContractError : std::logic_error {
+  using std::logic_error::logic_error;
+};
+struct DefaultResourceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <class ContractErr = DefaultContractError, class ResourceErr = DefaultResourceError>
+inline void check(cyc_status st) {
+  if (st == CYC_OK) return;
+  const std::string msg = cyc_last_error();
+  if (st == CYC_E_CONTRACT) throw ContractErr(msg);
+  if (st == CYC_E_RESOURCE) throw ResourceErr(msg);
+  throw std::runtime_error(msg);
+}
+
+// One GPU and one CUDA stream (the reference's WorkerPool role, parallel.hpp).
+class Engine {
+ public:
+  explicit Engine(int device = 0) {
+    cyc_ctx* c = nullptr;
+    check(cyc_ctx_create(device, &c));
+    ctx_.reset(c, &cyc_ctx_destroy);
+  }
+  cyc_ctx* get() const { return ctx_.get(); }
+
+ private:
+  std::shared_ptr<cyc_ctx> ctx_;
+};
+
+// Device-resident snapshot (CsrSnapshot on the GPU, plus its gather index).
+class Snapshot {
+ public:
+  Snapshot() = default;
+  Snapshot(const Engine& e, cyc_graph* g) : eng_(e), g_(g, &cyc_graph_destroy) {
+    check(cyc_graph_info(g, &n_, &m_, &orientation_, &restricted_));
+  }
+  uint32_t n() const { return n_; }
+  uint64_t m() const { return m_; }
+  bool transposed() const { return orientation_ == CYC_TRANSPOSED; }
+  cyc_graph* get() const { return g_.get(); }
+  const Engine& engine() const { return eng_; }
+
+  // Copies the CSR back into a reference CsrSnapshot-like object.
+  template <class Csr>
+  void export_to(Csr& out) const {
+    out.n = n_;
+    out.m = m_;
+    out.row_offsets.assign(static_cast<size_t>(n_) + 1, 0);
+    out.col_indices.assign(m_, 0);
+    std::vector<uint64_t> acc((n_ + 63) / 64 + 1, 0);
+    check(cyc_graph_export(g_.get(), out.row_offsets.data(), out.col_indices.data(), acc.data(),
+                           nullptr));
+    out.accepting = decltype(out.accepting)(n_);
+    for (size_t i = 0; i < out.accepting.words().size(); ++i) out.accepting.words()[i] = acc[i];
+  }
+
+ private:
+  Engine eng_;
+  std::shared_ptr<cyc_graph> g_;
+  uint32_t n_ = 0;
+  uint64_t m_ = 0;
+  int orientation_ = CYC_TRANSPOSED;
+  int restricted_ = 0;
+};
+
+template <class OrientationT>
+inline int orientation_code(OrientationT o) {
+  return static_cast<int>(o) == 1 ? CYC_TRANSPOSED : CYC_FORWARD;  // types.hpp:12
+}
+
+// build_snapshot(log, orientation, m, n) — graph.hpp:97-98. Reads the logged
+// prefix through the public EdgeLog interface into one pinned staging buffer.
+template <class EdgeLogT, class OrientationT>
+Snapshot build_snapshot(const Engine& e, const EdgeLogT& log, OrientationT orientation, uint64_t m,
+                        uint32_t n) {
+  std::vector<uint32_t> edges(2 * m);
+  for (uint64_t i = 0; i < m; ++i) {
+    auto pr = log.edge(i);
+    edges[2 * i] = pr.first;
+    edges[2 * i + 1] = pr.second;
+  }
+  auto acc = log.accepting_prefix(n);
+  cyc_graph* g = nullptr;
+  check(cyc_graph_build(e.get(), edges.data(), m, n, acc.words().data(), orientation_code(orientation),
+                        &g));
+  return Snapshot(e, g);
+}
+
+// build_snapshot(log, orientation) — graph.hpp:101 (edge count captured first).
+template <class EdgeLogT, class OrientationT>
+Snapshot build_snapshot(const Engine& e, const EdgeLogT& log, OrientationT orientation) {
+  const uint64_t m = log.edge_count();
+  const uint32_t n = log.vertex_count();
+  return build_snapshot(e, log, orientation, m, n);
+}
+
+// Upload of a host CsrSnapshot (for callers that already built one).
+template <class Csr>
+Snapshot upload(const Engine& e, const Csr& snap) {
+  cyc_graph* g = nullptr;
+  check(cyc_graph_from_csr(e.get(), snap.row_offsets.data(), snap.col_indices.data(), snap.n, snap.m,
+                           snap.accepting.words().data(), orientation_code(snap.orientation), &g));
+  return Snapshot(e, g);
+}
+
+// restrict_to_accepting_sccs — graph.hpp:110-114; kept[new] = original id.
+inline std::pair<Snapshot, std::vector<uint32_t>> restrict_to_accepting_sccs(const Snapshot& s) {
+  cyc_graph* g = nullptr;
+  check(cyc_graph_restrict(s.engine().get(), s.get(), &g));
+  Snapshot r(s.engine(), g);
+  std::vector<uint32_t> kept(r.n());
+  check(cyc_graph_export(g, nullptr, nullptr, nullptr, kept.data()));
+  return {std::move(r), std::move(kept)};
+}
+
+template <class BitsetT>
+const uint64_t* words_of(const BitsetT& acc, uint32_t n) {
+  if (acc.size() != n) throw DefaultContractError("run_map: accepting set size mismatch");
+  return acc.words().data();
+}
+
+template <class OptionsT>
+cyc_map_options to_c(const OptionsT& o) {
+  cyc_map_options c{};
+  c.early_exit = o.early_exit ? 1 : 0;
+  c.mode = CYC_MODE_AUTO;
+  return c;
+}
+
+// run_map — map_engine.hpp:111-112 (workers is meaningless on the GPU; the
+// result is the same for every worker count).
+template <class VerdictT, class StatsT, class BitsetT, class OptionsT>
+std::pair<VerdictT, StatsT> run_map(const Snapshot& s, const BitsetT& accepting, const OptionsT& opt) {
+  cyc_map_options o = to_c(opt);
+  cyc_map_stats st{};
+  check(cyc_map_run(s.engine().get(), s.get(), words_of(accepting, s.n()), &o, &st, nullptr, nullptr,
+                    nullptr, 0));
+  StatsT stats;
+  stats.iterations = st.iterations;
+  stats.kernel_calls = st.kernel_calls;
+  stats.demoted_total = st.demoted_total;
+  if (st.cycle_found) {
+    stats.cycle_witness = st.witness;
+    return {VerdictT::cycle(st.witness), stats};
+  }
+  return {VerdictT::no_cycle(), stats};
+}
+
+// fixpoint — map_engine.hpp:86-87; fills values with map codes (id+1, 0 NIL).
+template <class BitsetT, class OptionsT>
+uint64_t fixpoint(const Snapshot& s, const BitsetT& accepting, const OptionsT& opt,
+                  std::vector<uint32_t>& values, uint32_t& witness) {
+  cyc_map_options o = to_c(opt);
+  values.assign(s.n(), 0);
+  uint64_t steps = 0;
+  check(cyc_fixpoint(s.engine().get(), s.get(), words_of(accepting, s.n()), &o, values.data(), &steps,
+                     &witness));
+  return steps;
+}
+
+// demote — map_engine.hpp:99; remaining words (F \ D) and D ascending.
+template <class BitsetT>
+std::vector<uint32_t> demote(const Engine& e, const std::vector<uint32_t>& values, const BitsetT& accepting,
+                             std::vector<uint64_t>& remaining) {
+  const uint32_t n = static_cast<uint32_t>(values.size());
+  remaining.assign((n + 63) / 64 + 1, 0);
+  std::vector<uint32_t> d(n + 1);
+  uint64_t nd = 0;
+  check(cyc_demote(e.get(), values.data(), n, words_of(accepting, n), remaining.data(), d.data(), &nd));
+  d.resize(nd);
+  return d;
+}
+
+}  // namespace b200
+}  // namespace cycheck

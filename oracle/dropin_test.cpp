@@ -1,0 +1,75 @@
+// dropin_test.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// Builds against the reference's own headers and sources (oracle/Makefile,
+// target `dropin`) and checks that the C++ drop-in (include/cycheck_b200.hpp)
+// returns what the reference returns when a reference call site switches to
+// it: same Verdict, witness and MapStats from cycheck::run_map, the same CSR
+// from build_snapshot, the same restriction. Runs on a GPU box (the binary is
+// prebuilt into oracle/_ref/ and shipped); exits non-zero on any mismatch.
+#include <cstdio>
+#include <random>
+
+#include "cycheck/graph.hpp"
+#include "cycheck/map_engine.hpp"
+#include "../include/cycheck_b200.hpp"
+
+using namespace cycheck;
+
+int main(int argc, char** argv) {
+  const int trials = argc > 1 ? std::atoi(argv[1]) : 200;
+  b200::Engine gpu(0);
+  std::mt19937_64 rng(0x0912255);
+  int bad = 0;
+  for (int t = 0; t < trials; ++t) {
+    const uint32_t n = 1 + rng() % 400;
+    const uint64_t m = rng() % (4 * n + 1);
+    EdgeLog log({n, m ? m : 1});
+    for (uint32_t v = 0; v < n; ++v) log.add_vertex(rng() % 100 < (t % 2 ? 5u : 30u));
+    for (uint64_t i = 0; i < m; ++i) log.append_edge(rng() % n, rng() % n);
+    for (Orientation o : {Orientation::transposed, Orientation::forward}) {
+      CsrSnapshot ref = build_snapshot(log, o);
+      b200::Snapshot dev = b200::build_snapshot(gpu, log, o);
+      CsrSnapshot back;
+      dev.export_to(back);
+      if (back.row_offsets != ref.row_offsets || back.col_indices != ref.col_indices ||
+          !(back.accepting == ref.accepting)) {
+        std::printf("trial %d: build_snapshot differs\n", t);
+        ++bad;
+      }
+      b200::Snapshot up = b200::upload(gpu, ref);
+      for (bool early : {true, false}) {
+        MapOptions opts;
+        opts.early_exit = early;
+        auto [rv, rs] = run_map(ref, ref.accepting, opts);
+        auto [gv, gs] = b200::run_map<Verdict, MapStats>(dev, ref.accepting, opts);
+        auto [uv, us] = b200::run_map<Verdict, MapStats>(up, ref.accepting, opts);
+        for (auto* p : {&gv, &uv}) {
+          if (!(*p == rv)) {
+            std::printf("trial %d: verdict differs\n", t);
+            ++bad;
+          }
+        }
+        for (auto* p : {&gs, &us}) {
+          if (p->iterations != rs.iterations || p->kernel_calls != rs.kernel_calls ||
+              p->demoted_total != rs.demoted_total || p->cycle_witness != rs.cycle_witness) {
+            std::printf("trial %d: stats differ (%llu/%llu vs %llu/%llu)\n", t,
+                        (unsigned long long)p->iterations, (unsigned long long)p->kernel_calls,
+                        (unsigned long long)rs.iterations, (unsigned long long)rs.kernel_calls);
+            ++bad;
+          }
+        }
+      }
+      SccRestriction rr = restrict_to_accepting_sccs(ref);
+      auto [gr, kept] = b200::restrict_to_accepting_sccs(dev);
+      CsrSnapshot grb;
+      gr.export_to(grb);
+      if (kept != rr.kept || grb.row_offsets != rr.snapshot.row_offsets ||
+          grb.col_indices != rr.snapshot.col_indices) {
+        std::printf("trial %d: restriction differs\n", t);
+        ++bad;
+      }
+    }
+  }
+  std::printf("dropin_test: %d trials, %d mismatches\n", trials, bad);
+  return bad ? 1 : 0;
+}

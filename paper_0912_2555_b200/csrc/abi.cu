@@ -305,6 +305,43 @@ cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, 
   });
 }
 
+// CSR (row, col) entries back to the logged (src, dst) pairs of the prefix.
+__global__ void k_csr_to_log(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
+                             int transposed, uint2* __restrict__ edges) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
+    for (uint64_t i = off[v]; i < off[v + 1]; ++i)
+      edges[i] = transposed ? make_uint2(col[i], v) : make_uint2(v, col[i]);
+}
+
+cyc_status cyc_graph_from_csr(cyc_ctx* ctx, const uint64_t* row_offsets, const uint32_t* col_indices,
+                              uint32_t n, uint64_t m, const uint64_t* acc_words, int orientation,
+                              cyc_graph** out) {
+  return guard([&] {
+    require(ctx && out && row_offsets, CYC_E_CONTRACT, "null argument");
+    require(m < 0xFFFFFFFFull, CYC_E_RESOURCE, "snapshot edges must be < 2^32");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->s;
+    DevBuf toff, tcol, edges((m ? m : 1) * 8, s);
+    const uint64_t* doff = stage_in(row_offsets, (size_t)n + 1, toff, s);
+    const uint32_t* dcol = stage_in(col_indices, (size_t)m, tcol, s);
+    if (n && m) {
+      k_csr_to_log<<<cyc::grid_for(n, 256, 8), 256, 0, s>>>(n, doff, dcol, orientation == CYC_TRANSPOSED,
+                                                           edges.as<uint2>());
+      CYC_LAUNCHED();
+    }
+    auto* g = new cyc_graph;
+    try {
+      build_graph(ctx, edges.as<uint32_t>(), m, n, acc_words, orientation, g);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    ctx->refs.fetch_add(1);
+    *out = g;
+  });
+}
+
 cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out) {
   return guard([&] {
     require(ctx && in && out, CYC_E_CONTRACT, "null argument");
