@@ -80,11 +80,50 @@ __device__ __forceinline__ uint32_t cand_of(uint32_t w, uint32_t u) {
 }
 
 // ---------------------------------------------------------- block helpers
+constexpr uint32_t kWlCap = 1024;  // per-CTA list of newly non-zero frontier words
+
+constexpr uint32_t kBigCap = 128;   // per-CTA big vertices awaiting chunk expansion
+
 struct BlockSh {
   unsigned long long w[32][3];
   unsigned long long bcast;
   uint32_t wmin[33];
+  uint32_t wl_n, wl_base;
+  uint32_t wl[kWlCap];
+  uint32_t big_n;
+  uint32_t bigv[kBigCap];
+  uint32_t bigb[kBigCap];   // first edge
+  uint32_t bige[kBigCap];   // end edge
+  uint32_t bigc[kBigCap];   // first chunk slot
 };
+
+// A frontier word became non-zero in this step: remember it for the next
+// push step (block-local, flushed once per CTA by wl_flush).
+__device__ __forceinline__ void note_word(BlockSh* sh, uint32_t wi) {
+  const uint32_t pos = atomicAdd(&sh->wl_n, 1u);
+  if (pos < kWlCap) sh->wl[pos] = wi;
+}
+
+// Appends the CTA's noted words to the step's global word list with one
+// atomic; an overflowing CTA flags the list incomplete (the next push step then
+// scans the whole bitmap). Call with the whole CTA after its notes are done.
+__device__ void wl_flush(BlockSh* sh, SlotCtl* sl, uint32_t* wl, uint32_t wl_cap) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t n = sh->wl_n;
+    const uint32_t cnt = n < kWlCap ? n : kWlCap;
+    uint32_t base = 0;
+    if (cnt) base = atomicAdd(&sl->wl_count, cnt);
+    if (n > kWlCap || base + cnt > wl_cap) *(volatile unsigned int*)&sl->wl_over = 1u;
+    sh->wl_base = base;
+    sh->wl_n = cnt;
+  }
+  __syncthreads();
+  const uint32_t cnt = sh->wl_n, base = sh->wl_base;
+  for (uint32_t i = threadIdx.x; i < cnt && base + i < wl_cap; i += blockDim.x) wl[base + i] = sh->wl[i];
+  __syncthreads();
+  if (threadIdx.x == 0) sh->wl_n = 0;
+}
 
 __device__ unsigned long long block_sum(unsigned long long x, BlockSh* sh) {
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -125,11 +164,16 @@ struct StepAcc {
   unsigned long long fedges = 0;  // their push degrees (when known)
 };
 
-// One fused 3-value reduction, one flag store and two atomics per CTA.
-__device__ void step_flags(const StepAcc& acc, SlotCtl* sl, BlockSh* sh) {
+// One fused 3-value reduction, one flag store and two atomics per CTA, then
+// the CTA's frontier-word list is flushed.
+__device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc,
+                                        unsigned int* nchunk);
+__device__ void step_flags(const RunArgs& a, const StepAcc& acc, SlotCtl* sl, BlockSh* sh,
+                           uint32_t* wl, uint32_t wl_cap, uint4* bc) {
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned long long bigdeg = big_flush(a, sh, bc, &sl->nchunk);
   const unsigned long long r = warp_sum64(acc.raised), f = warp_sum64(acc.first),
-                           e = warp_sum64(acc.fedges);
+                           e = warp_sum64(acc.fedges) + (threadIdx.x == 0 ? bigdeg : 0ull);
   if (lane == 0) {
     sh->w[wid][0] = r;
     sh->w[wid][1] = f;
@@ -149,20 +193,20 @@ __device__ void step_flags(const StepAcc& acc, SlotCtl* sl, BlockSh* sh) {
       if (ee) atomicAdd(&sl->fedges, ee);
     }
   }
-  __syncthreads();
+  wl_flush(sh, sl, wl, wl_cap);
 }
 
 // Sets bit v of the frontier bitmap (and its summary bit); true iff new.
-__device__ __forceinline__ bool mark(uint32_t* fb, uint32_t* sb, uint32_t v) {
+__device__ __forceinline__ bool mark(uint32_t* fb, BlockSh* sh, uint32_t v) {
   const uint32_t w = v >> 5, bit = 1u << (v & 31u);
   const uint32_t old = atomicOr(fb + w, bit);
-  if (old == 0u) atomicOr(sb + (w >> 5), 1u << (w & 31u));
+  if (old == 0u) note_word(sh, w);
   return !(old & bit);
 }
 
-// Chunks of a big-degree vertex for the next push step; returns its degree.
-__device__ __forceinline__ uint32_t enlist(const RunArgs& a, uint32_t v, uint4* bc,
-                                           unsigned int* nchunk) {
+// Chunks of a big-degree vertex for the next push step, written by one lane
+// (fallback when the CTA's list is full); returns the degree.
+__device__ uint32_t enlist_now(const RunArgs& a, uint32_t v, uint4* bc, unsigned int* nchunk) {
   const uint32_t b = __ldg(a.poff + v), e = __ldg(a.poff + v + 1);
   const uint32_t nc = (e - b + kChunk - 1) / kChunk;
   const uint32_t base = atomicAdd(nchunk, nc);
@@ -171,11 +215,61 @@ __device__ __forceinline__ uint32_t enlist(const RunArgs& a, uint32_t v, uint4* 
   return e - b;
 }
 
+// A big-degree vertex entered the next frontier: note it in the CTA's list;
+// the whole CTA writes its chunk descriptors at step end (big_flush), so no
+// single lane serialises hundreds of stores. Returns the degree if it had to
+// be expanded here (list full), else 0 (big_flush accounts it).
+__device__ __forceinline__ uint32_t enlist(const RunArgs& a, uint32_t v, uint4* bc,
+                                           unsigned int* nchunk, BlockSh* sh) {
+  const uint32_t pos = atomicAdd(&sh->big_n, 1u);
+  if (pos < kBigCap) {
+    sh->bigv[pos] = v;
+    return 0u;
+  }
+  return enlist_now(a, v, bc, nchunk);
+}
+
+// Expands the CTA's noted big vertices into chunks (whole CTA); returns the
+// sum of their degrees in thread 0.
+__device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc,
+                                        unsigned int* nchunk) {
+  __syncthreads();
+  const uint32_t nb = min(sh->big_n, kBigCap);
+  unsigned long long deg = 0;
+  if (nb == 0) return 0;
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+    const uint32_t v = sh->bigv[i];
+    sh->bigb[i] = __ldg(a.poff + v);
+    sh->bige[i] = __ldg(a.poff + v + 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t total = 0;
+    for (uint32_t i = 0; i < nb; ++i) {
+      sh->bigc[i] = total;
+      total += (sh->bige[i] - sh->bigb[i] + kChunk - 1) / kChunk;
+      deg += sh->bige[i] - sh->bigb[i];
+    }
+    const uint32_t base = atomicAdd(nchunk, total);
+    for (uint32_t i = 0; i < nb; ++i) sh->bigc[i] += base;
+  }
+  __syncthreads();
+  for (uint32_t i = 0; i < nb; ++i) {
+    const uint32_t v = sh->bigv[i], b = sh->bigb[i], e = sh->bige[i], c0 = sh->bigc[i];
+    const uint32_t nc = (e - b + kChunk - 1) / kChunk;
+    for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x)
+      if (c0 + c < a.chunk_cap) bc[c0 + c] = make_uint4(v, b + c * kChunk, min(e, b + (c + 1) * kChunk), 0u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sh->big_n = 0;
+  return deg;
+}
+
 struct PushCtx {
   const uint32_t* Pc;  // frozen x_{k-1}
   uint32_t* Pn;        // x_k under construction
   uint32_t* fb;        // next frontier
-  uint32_t* sb;
+  BlockSh* sh;
   uint4* bc;
   unsigned int* nchunk;
   uint32_t* Cn;
@@ -200,7 +294,7 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
   }
   bool first[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) first[r] = go[r] && mark(c.fb, c.sb, tgt[r]);
+  for (int r = 0; r < R; ++r) first[r] = go[r] && mark(c.fb, c.sh, tgt[r]);
   uint32_t bw[R], b[R], e[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {  // one round trip for the big bit and the degree
@@ -213,17 +307,9 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
     acc.raised += go[r];
     acc.first += first[r];
     acc.fedges += e[r] - b[r];
-    if ((bw[r] >> (tgt[r] & 31u)) & 1u) enlist(a, tgt[r], c.bc, c.nchunk);
+    if ((bw[r] >> (tgt[r] & 31u)) & 1u) acc.fedges += enlist(a, tgt[r], c.bc, c.nchunk, c.sh);
     if (go[r] && (old[r] & kFlag) && val[r] == tgt[r] + 1u) c.Cn[atomicAdd(c.ccnt, 1u)] = tgt[r];
   }
-}
-
-// Summaries rotate over three buffers: step g reads SB[(g-1)%3], writes
-// SB[g%3] and clears SB[(g+1)%3] (last read in step g-1, next written in g+1).
-__device__ __forceinline__ void clear_summary(const RunArgs& a, uint32_t g) {
-  uint32_t* sz = a.SB[(g + 1u) % 3u];
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.nsum; i += gridDim.x * blockDim.x)
-    sz[i] = 0u;
 }
 
 // ------------------------------------------------------------------ pull
@@ -235,7 +321,7 @@ __device__ __forceinline__ void clear_summary(const RunArgs& a, uint32_t g) {
 // Rows flagged in `ovf` (longer than K, or heavy) take a slow path.
 template <int K, int R>
 __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __restrict__ P,
-                                           uint32_t* __restrict__ Q, uint32_t* fb, uint32_t* sb,
+                                           uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh,
                                            uint32_t* fp, uint4* bc, SlotCtl* sl, StepAcc& acc) {
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -304,7 +390,7 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
       fp[wi] = 0u;
       if (wd) {
         atomicOr(fb + wi, wd);
-        atomicOr(sb + (wi >> 5), 1u << (wi & 31u));
+        note_word(sh, wi);
       }
     }
     // raised vertices of big push degree: chunks for the next push step
@@ -313,7 +399,7 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
     for (int k = 0; k < R; ++k) big[k] = words[k] ? __ldcg(a.bigm + (base >> 5) + k) & words[k] : 0u;
 #pragma unroll
     for (int k = 0; k < R; ++k)
-      if ((big[k] >> lane) & 1u) acc.fedges += enlist(a, base + 32u * k + lane, bc, &sl->nchunk);
+      if ((big[k] >> lane) & 1u) acc.fedges += enlist(a, base + 32u * k + lane, bc, &sl->nchunk, sh);
   }
 }
 
@@ -322,7 +408,6 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   uint32_t* __restrict__ Q = a.P[cur ^ 1];
   SlotCtl* sl = &a.ctl->slot[g % 3u];
   uint32_t* fb = a.FB[g & 1u];
-  uint32_t* sb = a.SB[g % 3u];
   uint32_t* fp = a.FB[(g - 1u) & 1u];
   uint4* bc = a.BC[g & 1u];
   uint32_t* Cn = a.C[g & 1u];
@@ -330,7 +415,6 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
-  clear_summary(a, g);
   // heavy rows first (they are the long poles): one warp per chunk of at
   // most 32*kHeavyPerLane edges, every lane issuing all its loads at once;
   // combined with atomicMax into Q (Q holds x_{k-2}, never larger)
@@ -354,9 +438,9 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
       atomicMax(Q + v, (own & kFlag) | best);
       if (best > (own & kCode)) {
         ++acc.raised;
-        if (mark(fb, sb, v)) {
+        if (mark(fb, sh, v)) {
           ++acc.first;
-          if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk);
+          if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
         }
         if ((own & kFlag) && best == v + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
       }
@@ -364,13 +448,13 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   }
   phase_mark(a, tk, 0);
   switch (a.ell_k) {
-    case 1: pull_light<1, 8>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
-    case 2: pull_light<2, 8>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
-    case 4: pull_light<4, 4>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
-    default: pull_light<8, 4>(a, P, Q, fb, sb, fp, bc, sl, acc); break;
+    case 1: pull_light<1, 8>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
+    case 2: pull_light<2, 8>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
+    case 4: pull_light<4, 4>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
+    default: pull_light<8, 4>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
   }
   phase_mark(a, tk, 1);
-  step_flags(acc, sl, sh);
+  step_flags(a, acc, sl, sh, a.WL[g & 1u], a.wl_cap, a.BC[g & 1u]);
   phase_mark(a, tk, 2);
 }
 
@@ -382,22 +466,21 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   c.Pc = a.P[cur];
   c.Pn = a.P[cur ^ 1];
   c.fb = a.FB[g & 1u];
-  c.sb = a.SB[g % 3u];
+  c.sh = sh;
   c.bc = a.BC[g & 1u];
   c.nchunk = &sl->nchunk;
   c.Cn = a.C[g & 1u];
   c.ccnt = &sl->cand_cnt;
   uint32_t* fp = a.FB[(g - 1u) & 1u];
-  const uint32_t* sp = a.SB[(g - 1u) % 3u];
+  const uint32_t* wlp = a.WL[(g - 1u) & 1u];
   const uint4* bp = a.BC[(g - 1u) & 1u];
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
-  clear_summary(a, g);
   // big frontier vertices first: one warp per kChunk-edge chunk, each lane
   // raising kChunk/32 targets as one batch
-  const uint32_t nch = min(__ldcg(&pl->nchunk), a.chunk_cap);
+  const uint32_t nch = min(__ldca(&pl->nchunk), a.chunk_cap);
   for (uint32_t k = gw; k < nch; k += nw) {
     const uint4 ch = bp[k];
     const uint32_t vv = cand_of(__ldca(c.Pc + ch.x), ch.x);
@@ -412,24 +495,39 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   }
   phase_mark(a, tk, 0);
   // every frontier vertex: max-copy itself into the new buffer, and push its
-  // edges unless it is big (chunks above). Warps take 4 consecutive bitmap
-  // words per iteration, interleaved over the grid (a contiguous wave of
-  // raised ids spreads over many warps); lane i owns bit i of each word.
-  // Words are cleared by their owner; the summary is cleared a step later.
-  for (uint32_t it = gw; it * 4u < a.nwords; it += nw) {
-    const uint32_t w0 = it * 4u;
-    const uint32_t m4 = (__ldca(sp + (w0 >> 5)) >> (w0 & 31u)) & 0xFu;
-    if (!m4) continue;
+  // edges unless it is big (chunks above). Frontier words come from the
+  // previous step's word list (4 per warp iteration, interleaved over the
+  // grid, so a contiguous wave of raised ids spreads over many warps), or from
+  // a scan of the whole bitmap when that list overflowed. Lane i owns bit i of
+  // each word; each word is cleared by the warp that consumes it.
+  const uint32_t wlc = __ldca(&pl->wl_count);
+  const bool scan = __ldca(&pl->wl_over) != 0u;
+  const uint32_t groups = scan ? (a.nwords + 3u) / 4u : (wlc + 3u) / 4u;
+  for (uint32_t it = gw; it < groups; it += nw) {
+    uint32_t wi[kBatch], wd[kBatch];
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const uint32_t e = it * 4u + r;
+      wi[r] = scan ? (e < a.nwords ? e : kNone) : (e < wlc ? __ldcg(wlp + e) : kNone);
+    }
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) wd[r] = wi[r] != kNone ? __ldcg(fp + wi[r]) : 0u;
+    if (!(wd[0] | wd[1] | wd[2] | wd[3])) continue;
+    __syncwarp();
+    {
+      uint32_t mw = 0, mi = kNone;  // lane r < 4 clears word r (select chain, no local memory)
+#pragma unroll
+      for (int r = 0; r < kBatch; ++r)
+        if (lane == (uint32_t)r) {
+          mw = wd[r];
+          mi = wi[r];
+        }
+      if (mw) fp[mi] = 0u;
+    }
     uint32_t v[kBatch], b[kBatch], e[kBatch], val[kBatch];
 #pragma unroll
     for (int r = 0; r < kBatch; ++r) {
-      const uint32_t wd = ((m4 >> r) & 1u) ? __ldcg(fp + w0 + r) : 0u;
-      v[r] = (wd >> lane) & 1u ? (w0 + r) * 32u + lane : kNone;
-    }
-    __syncwarp();
-    if (lane < 4u && ((m4 >> lane) & 1u)) fp[w0 + lane] = 0u;
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r) {
+      v[r] = (wd[r] >> lane) & 1u ? wi[r] * 32u + lane : kNone;
       b[r] = e[r] = 0u;
       val[r] = 0u;
       if (v[r] != kNone) {  // all four loads in one round trip
@@ -455,7 +553,7 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
     }
   }
   phase_mark(a, tk, 1);
-  step_flags(acc, sl, sh);
+  step_flags(a, acc, sl, sh, a.WL[g & 1u], a.wl_cap, a.BC[g & 1u]);
   phase_mark(a, tk, 2);
 }
 
@@ -530,30 +628,24 @@ __device__ void demote_pass(const RunArgs& a, unsigned int* dcount, unsigned lon
 
 // Start of a fixpoint (setup tag g): both map buffers all-NIL with the
 // accepting bit; the initial frontier is the accepting set itself (every
-// accepting u offers cand = u+1), FB[(g+1)&1] / SB[(g+1)&1] cleared.
+// accepting u offers cand = u+1), FB[(g+1)&1] cleared.
 __device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
   uint32_t* fb = a.FB[g & 1u];
-  uint32_t* sb = a.SB[g % 3u];
   uint32_t* fz = a.FB[(g + 1u) & 1u];
-  uint32_t* sz = a.SB[(g + 1u) % 3u];
   SlotCtl* sl = &a.ctl->slot[g % 3u];
   uint4* bc = a.BC[g & 1u];
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   unsigned long long fe = 0;
-  // 32 words (1024 vertices) per warp iteration: one summary word each
-  for (uint32_t s = gw; s < a.nsum; s += nw) {
+  // 32 words (1024 vertices) per warp iteration
+  for (uint32_t s = gw; s * 32u < a.nwords_pad; s += nw) {
     const uint32_t wi = s * 32u + lane;
     const uint32_t f = wi < a.nwords ? __ldcg(a.F + wi) : 0u;
-    if (wi < a.nwords) {
+    if (wi < a.nwords_pad) {
       fb[wi] = f;
       fz[wi] = 0u;
-    }
-    const uint32_t sw = __ballot_sync(kFull, f != 0u);
-    if (lane == 0) {
-      sb[s] = sw;
-      sz[s] = 0u;
+      if (f) note_word(sh, wi);
     }
     for (uint32_t j = 0; j < 32u; ++j) {
       const uint32_t fj = __shfl_sync(kFull, f, j);
@@ -565,7 +657,7 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
         a.P[1][v] = val;
         if (accv) {
           if (bit_of(a.bigm, v)) {
-            fe += enlist(a, v, bc, &sl->nchunk);
+            fe += enlist(a, v, bc, &sl->nchunk, sh);
           } else {
             fe += __ldg(a.poff + v + 1) - __ldg(a.poff + v);
           }
@@ -573,8 +665,10 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
       }
     }
   }
-  fe = block_sum(fe, sh);
+  const unsigned long long bigdeg = big_flush(a, sh, bc, &sl->nchunk);
+  fe = block_sum(fe, sh) + bigdeg;
   if (threadIdx.x == 0 && fe) atomicAdd(&sl->fedges, fe);
+  wl_flush(sh, sl, a.WL[g & 1u], a.wl_cap);
 }
 
 __device__ __forceinline__ void reset_slot(RunCtl* c, uint32_t s) {
@@ -585,6 +679,8 @@ __device__ __forceinline__ void reset_slot(RunCtl* c, uint32_t s) {
   sl.nchunk = 0;
   sl.cand_cnt = 0;
   sl.wit = kNone;
+  sl.wl_count = 0;
+  sl.wl_over = 0;
 }
 
 __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
@@ -600,6 +696,11 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   if (lead)
     for (int k = 0; k <= kResTag; ++k) stat[k] = 0;
+  if (threadIdx.x == 0) {
+    sh.wl_n = 0;
+    sh.big_n = 0;
+  }
+  __syncthreads();
 #define CYC_STAT(k, v) \
   do {                 \
     if (lead) stat[k] += (v); \
@@ -612,7 +713,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
   grid.sync();
   uint64_t t = 0;
   bool truncated = false;
-  if (__ldcg(&ctl->it_fsize[0]) != 0) {
+  if (__ldca(&ctl->it_fsize[0]) != 0) {
     for (;;) {
       unsigned long long steps = 0;
       bool prev_push = true;  // the previous tag's fedges is exact (push or setup)
@@ -625,10 +726,10 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
         if (mode != kModePull && mode != kModePush) {
           unsigned long long est;
           if (prev_push) {
-            est = __ldcg(&ctl->slot[pslot].fedges);
+            est = __ldca(&ctl->slot[pslot].fedges);
           } else {  // pull steps count big-vertex degrees exactly, the rest by average
-            const unsigned long long nr = __ldcg(&ctl->slot[pslot].nraised);
-            est = __ldcg(&ctl->slot[pslot].fedges) + (a.n ? nr * a.m / a.n : 0);
+            const unsigned long long nr = __ldca(&ctl->slot[pslot].nraised);
+            est = __ldca(&ctl->slot[pslot].fedges) + (a.n ? nr * a.m / a.n : 0);
           }
           mode = (est * a.alpha < a.m) ? kModePush : kModePull;
         }
@@ -637,8 +738,8 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
         if (a.trace && lead && tkk < a.trace_cap) a.trace[64u * tkk + 3u] = gtimer();
         if (mode == kModePush) {
           if (lead) {
-            const unsigned long long fe = __ldcg(&ctl->slot[pslot].fedges);
-            const unsigned long long nr = __ldcg(&ctl->slot[pslot].nraised);
+            const unsigned long long fe = __ldca(&ctl->slot[pslot].fedges);
+            const unsigned long long nr = __ldca(&ctl->slot[pslot].nraised);
             stat[kResEdges] += fe;
             stat[kResRows] += nr;
             stat[kResBytes] += 8ull * fe + 12ull * nr;
@@ -656,15 +757,15 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
         cur ^= 1;
         prev_push = mode == kModePush;
         const SlotCtl* sl = &ctl->slot[slot];
-        const uint32_t changed = __ldcg(&sl->changed);
-        uint32_t w = __ldcg(&sl->wit);
-        const uint32_t nc = __ldcg(&sl->cand_cnt);
+        const uint32_t changed = __ldca(&sl->changed);
+        uint32_t w = __ldca(&sl->wit);
+        const uint32_t nc = __ldca(&sl->cand_cnt);
         if (lead && a.trace && tkk < a.trace_cap) {
           unsigned long long* tr = a.trace + 64u * tkk;
           tr[0] = ((unsigned long long)mode << 60) |
-                  ((unsigned long long)__ldcg(&ctl->slot[pslot].nchunk) << 24) | (steps & 0xFFFFFFull);
-          tr[1] = mode == kModePush ? __ldcg(&ctl->slot[pslot].fedges) : a.m;
-          tr[2] = __ldcg(&sl->nraised);
+                  ((unsigned long long)__ldca(&ctl->slot[pslot].nchunk) << 24) | (steps & 0xFFFFFFull);
+          tr[1] = mode == kModePush ? __ldca(&ctl->slot[pslot].fedges) : a.m;
+          tr[2] = __ldca(&sl->nraised);
           tr[7] = gtimer();
         }
         if (nc && a.early_exit) {
@@ -697,14 +798,14 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
       finish_pass(a, cur, t, !cycle, &sh);
       grid.sync();
       if (!a.early_exit) {
-        const uint32_t fw = __ldcg(&ctl->it_finwit[t & 1u]);
+        const uint32_t fw = __ldca(&ctl->it_finwit[t & 1u]);
         if (fw != kNone) {
           cycle = 1;
           witness = fw;
         }
       }
       if (lead && t < a.cap) {
-        if (a.iter_hash) a.iter_hash[t] = __ldcg(&ctl->it_hash[t & 1u]);
+        if (a.iter_hash) a.iter_hash[t] = __ldca(&ctl->it_hash[t & 1u]);
         if (a.iter_steps) a.iter_steps[t] = steps;
       }
       CYC_STAT(kResIterations, 1);
@@ -713,11 +814,11 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
       if (a.max_iterations && t + 1 >= a.max_iterations) break;
       demote_pass(a, &ctl->it_dcount[t & 1u], &ctl->it_fsize[(t + 1u) & 1u], &sh);
       grid.sync();
-      const uint32_t dc = __ldcg(&ctl->it_dcount[t & 1u]);
+      const uint32_t dc = __ldca(&ctl->it_dcount[t & 1u]);
       CYC_STAT(kResDemoted, dc);
       if (dc == 0) break;                                      // D empty: no cycle
       ++t;
-      if (__ldcg(&ctl->it_fsize[t & 1u]) == 0) break;          // F' empty: no cycle
+      if (__ldca(&ctl->it_fsize[t & 1u]) == 0) break;          // F' empty: no cycle
       ++g;
       if (lead) reset_slot(ctl, (g + 1u) % 3u);
       reset_pass(a, g, &sh);
@@ -820,10 +921,10 @@ void RunWs::ensure(uint32_t nn, uint32_t mm, const uint32_t* poff, cudaStream_t 
   n_pad = (uint32_t)(((uint64_t)nn + kRowPad - 1) / kRowPad * kRowPad);
   const size_t np1 = (size_t)n_pad + 1;
   const size_t words = (size_t)n_pad / 32 + 2;
-  const size_t sums = words / 32 + 2;
   // a vertex of push degree d > kBigDeg yields ceil(d/kChunk) <= d/kChunk + 1 chunks
   chunk_cap = (uint32_t)((uint64_t)mm / kChunk + (uint64_t)mm / (kBigDeg + 1) + 16);
-  for (int k = 0; k < 3; ++k) SB[k].alloc(sums * 4, s);
+  wl_cap = (uint32_t)(2 * words + 64);
+  for (int k = 0; k < 2; ++k) WL[k].alloc((size_t)wl_cap * 4, s);
   for (int k = 0; k < 2; ++k) {
     P[k].alloc(np1 * 4, s);
     CYC_CUDA(cudaMemsetAsync(P[k].p, 0, np1 * 4, s));  // padding rows stay NIL forever
@@ -880,11 +981,12 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
     a.BC[k] = ws.BC[k].as<uint4>();
     a.C[k] = ws.C[k].as<uint32_t>();
   }
-  for (int k = 0; k < 3; ++k) a.SB[k] = ws.SB[k].as<uint32_t>();
+  for (int k = 0; k < 2; ++k) a.WL[k] = ws.WL[k].as<uint32_t>();
+  a.wl_cap = ws.wl_cap;
   a.F = ws.F.as<uint32_t>();
   a.used = ws.used.as<uint32_t>();
   a.nwords = (uint32_t)(((uint64_t)n + 31) / 32);
-  a.nsum = (a.nwords + 31) / 32;
+  a.nwords_pad = ws.n_pad / 32u;
   a.chunk_cap = ws.chunk_cap;
   a.ctl = ws.ctl.as<RunCtl>();
   a.iter_hash = cap ? ws.hist.as<unsigned long long>() : nullptr;

@@ -10,15 +10,16 @@ namespace cyc {
 constexpr uint32_t kBigDeg = 32;
 constexpr uint32_t kChunk = 128;
 
-// Per-step counters (32 bytes, read back with two vector loads).
-struct alignas(32) SlotCtl {
+// Per-step counters.
+struct alignas(64) SlotCtl {
   unsigned long long fedges;  // push degrees of the vertices first raised in the step
   unsigned int nraised;       // vertices raised
   unsigned int changed;
   unsigned int nchunk;        // big-vertex chunks enlisted for the next step
   unsigned int cand_cnt;      // self-witness candidates
   unsigned int wit;           // exact min self-witness (pull rows)
-  unsigned int pad;
+  unsigned int wl_count;      // frontier words listed for the next push step
+  unsigned int wl_over;       // the list is incomplete: scan the bitmap instead
 };
 
 // Control block of one k_map_run launch. Per-step counters rotate over three
@@ -53,12 +54,13 @@ struct RunArgs {
   uint32_t n_heavy, heavy_deg;
   uint32_t* P[2];                  // packed map words: accepting<<31 | code
   uint32_t* FB[2];                 // frontier bitmaps: vertices changed in the step
-  uint32_t* SB[3];                 // summary bitmaps: bit w = FB word w is non-zero
+  uint32_t* WL[2];                 // frontier word lists (non-zero FB words of the step)
+  uint32_t wl_cap;
   uint4* BC[2];                    // frontier chunks {v, beg, end} of big-degree vertices
   uint32_t* C[2];                  // self-witness candidates
   uint32_t* F;                     // accepting set, u32 words (demoted in place)
   uint32_t* used;                  // scratch bitmap, zero between iterations
-  uint32_t nwords, nsum;           // FB words, SB words
+  uint32_t nwords, nwords_pad;     // FB words for n and for the padded rows
   uint32_t chunk_cap;
   RunCtl* ctl;
   unsigned long long* iter_hash;
@@ -73,7 +75,8 @@ struct RunArgs {
 
 struct RunWs {
   uint32_t n = 0, m = 0, n_pad = 0;
-  DevBuf P[2], FB[2], SB[3], BC[2], C[2], F, used, bigm, ctl, hist, trace;
+  DevBuf P[2], FB[2], WL[2], BC[2], C[2], F, used, bigm, ctl, hist, trace;
+  uint32_t wl_cap = 0;
   uint32_t chunk_cap = 0;
   uint32_t trace_len = 0;
   void ensure(uint32_t n, uint32_t m, const uint32_t* poff, cudaStream_t s);
