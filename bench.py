@@ -361,6 +361,63 @@ def run_b200(args, rank, world, local):
     return 0
 
 
+def run_b200_sharded(args, rank, world, local):
+    """One graph, rows sharded over the ranks (paper_0912_2555_b200/sharded.py)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_0912_2555_b200 as eng
+    from paper_0912_2555_b200 import _abi, sharded
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=rank, world_size=world)
+    ctx = eng.Context(local)
+    params = make_params(eng, args)
+    n, m_log = int(params.n), int(params.m)
+    e = np.zeros((m_log, 2), np.uint32)
+    a = np.zeros((n + 63) // 64, np.uint64)
+    _abi.check(_abi.lib().cyc_gen_fill(ctx.handle, C.byref(params), _abi.ptr(e), _abi.ptr(a)))
+    snap = eng.build_snapshot((n, e, eng.Bitset.from_words(a, n)), ctx=ctx)
+    off, _ = snap.gather_index()
+    bounds = sharded.plan(off, world)
+    be = sharded.CudaShardBackend(snap, device)
+    words = snap.accepting.words().copy()
+    for _ in range(args.warmup):
+        sharded.run_map_sharded(be, dist, rank, world, bounds, words, True)
+    times = []
+    for _ in range(args.steps):
+        _abi.check(_abi.lib().cyc_flush_l2(ctx.handle, L2_FLUSH_BYTES))
+        dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(device)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        res = sharded.run_map_sharded(be, dist, rank, world, bounds, words, True)
+        t1.record()
+        torch.cuda.synchronize(device)
+        times.append(t0.elapsed_time(t1))
+    ms = max_over_ranks(dist, sum(times) / len(times), device)
+    m = snap.m
+    value = m * res.stats.kernel_calls / (ms * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded include/cyc_gen.h)",
+            "config": {"workload": f"config{args.config}", "n": n, "m": m,
+                       "parallelism": f"rowshard{world}", "exchange": "nccl allgather + allreduce per step"},
+            "verdict": {"cycle_found": res.verdict.cycle_found(), "iterations": res.stats.iterations,
+                        "kernel_calls": res.stats.kernel_calls}}))
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -377,11 +434,16 @@ def main():
     ap.add_argument("--n-override", type=int, default=0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N>1: row-shard one graph over the ranks (NCCL exchange per step) "
+                         "instead of independent replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
+    if args.sharded:
+        return run_b200_sharded(args, rank, world, local)
     return run_b200(args, rank, world, local)
 
 

@@ -84,6 +84,10 @@ uint64_t cyc_launch_count(void);
 cyc_status cyc_ctx_synchronize(cyc_ctx* ctx);
 /* The CUDA stream (cudaStream_t) every call of this context is ordered on. */
 void* cyc_ctx_stream(cyc_ctx* ctx);
+/* external != 0: order the context on `stream` (e.g. the stream NCCL / torch
+ * work is issued on; 0 is the legacy default stream); external == 0 restores
+ * the context's own stream. */
+cyc_status cyc_ctx_set_stream(cyc_ctx* ctx, void* stream, int external);
 
 /* ---- graph (reference graph.hpp:27-42 CsrSnapshot) ---------------------- */
 /* build_snapshot (graph.hpp:97-98, graph.cpp:63-105): edges = 2*m_log u32
@@ -166,6 +170,19 @@ cyc_status cyc_memcpy(cyc_ctx* ctx, void* dst, const void* src, size_t bytes);
 cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes);
 
 /* ---- multi-GPU row sharding (one process per GPU) ------------------------ */
+/* One Jacobi step (MaxPropagation::step) restricted to rows [lo, hi) of the
+ * gather index: out[v - lo] for v in the range, from the full replicated
+ * vector x (n codes, device) and accepting words (device). flags (device,
+ * 2 u32) receive {changed, min self-witness or UINT32_MAX}; asynchronous on
+ * the context's stream (no host sync), for use between collectives. */
+cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi,
+                          const uint32_t* x, const uint64_t* acc_words, uint32_t* out,
+                          uint32_t* flags);
+/* used-bitmap demotion on a full replicated vector, entirely on device:
+ * remaining = F \ D (words, device), counts[0] = |D|, counts[1] = |F'|
+ * (device u64[2]); asynchronous. */
+cyc_status cyc_shard_demote(cyc_ctx* ctx, const uint32_t* x, uint32_t n, const uint64_t* acc_words,
+                            uint64_t* remaining, uint64_t* counts);
 /* Edge-balanced contiguous row ranges, the reference's worker partition rule
  * (map_engine.cpp:35-43): bounds[r] for r in [0, parts], computed on the
  * host from gather row offsets (n+1 u64). */

@@ -103,6 +103,7 @@ _SIGS = {
     "cyc_launch_count": (C.c_uint64, []),
     "cyc_ctx_synchronize": (C.c_int, [_P]),
     "cyc_ctx_stream": (_P, [_P]),
+    "cyc_ctx_set_stream": (C.c_int, [_P, _P, C.c_int]),
     "cyc_graph_build": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.POINTER(_P)]),
     "cyc_graph_from_csr": (C.c_int, [_P, _P, _P, C.c_uint32, C.c_uint64, _P, C.c_int, C.POINTER(_P)]),
     "cyc_graph_restrict": (C.c_int, [_P, _P, C.POINTER(_P)]),
@@ -128,6 +129,8 @@ _SIGS = {
     "cyc_flush_l2": (C.c_int, [_P, C.c_size_t]),
     "cyc_shard_bounds": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
     "cyc_map_trace": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "cyc_shard_step": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, _P, _P, _P, _P]),
+    "cyc_shard_demote": (C.c_int, [_P, _P, C.c_uint32, _P, _P, _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

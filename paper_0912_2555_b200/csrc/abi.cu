@@ -31,6 +31,7 @@ thread_local std::string g_err;
 struct cyc_ctx {
   int device = 0;
   cudaStream_t s = nullptr;
+  cudaStream_t own = nullptr;  // the context's own stream (s may be an external one)
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   cyc::DevBuf flush;
   std::atomic<int> refs{1};
@@ -46,7 +47,7 @@ void ctx_release(cyc_ctx* ctx) {
   cudaEventDestroy(ctx->e1);
   cudaEventDestroy(ctx->e2);
   cudaEventDestroy(ctx->e3);
-  cudaStreamDestroy(ctx->s);
+  cudaStreamDestroy(ctx->own);
   delete ctx;
 }
 }  // namespace
@@ -264,7 +265,8 @@ cyc_status cyc_ctx_create(int device, cyc_ctx** out) {
             "this library is built for sm_100a (B200) only");
     auto* c = new cyc_ctx;
     c->device = device;
-    CYC_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    CYC_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->s = c->own;
     CYC_CUDA(cudaEventCreate(&c->e0));
     CYC_CUDA(cudaEventCreate(&c->e1));
     CYC_CUDA(cudaEventCreate(&c->e2));
@@ -287,6 +289,14 @@ cyc_status cyc_ctx_synchronize(cyc_ctx* ctx) {
 }
 
 void* cyc_ctx_stream(cyc_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
+
+cyc_status cyc_ctx_set_stream(cyc_ctx* ctx, void* stream, int external) {
+  return guard([&] {
+    require(ctx, CYC_E_CONTRACT, "null ctx");
+    CYC_CUDA(cudaStreamSynchronize(ctx->s));
+    ctx->s = external ? static_cast<cudaStream_t>(stream) : ctx->own;
+  });
+}
 
 cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
                            const uint64_t* acc_words, int orientation, cyc_graph** out) {
@@ -654,6 +664,35 @@ cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes) {
     require(ctx, CYC_E_CONTRACT, "null ctx");
     if (ctx->flush.bytes < bytes) ctx->flush.alloc(bytes, ctx->s);
     CYC_CUDA(cudaMemsetAsync(ctx->flush.p, (int)(cyc::g_launches.load() & 0xFF), bytes, ctx->s));
+  });
+}
+
+cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi,
+                          const uint32_t* x, const uint64_t* acc_words, uint32_t* out,
+                          uint32_t* flags) {
+  return guard([&] {
+    require(ctx && g && x && acc_words && flags && (out || hi <= lo), CYC_E_CONTRACT,
+            "shard_step: null argument");
+    require(lo <= hi && hi <= g->n(), CYC_E_CONTRACT, "shard_step: bad row range");
+    require(is_device_ptr(x) && is_device_ptr(acc_words) && is_device_ptr(flags), CYC_E_CONTRACT,
+            "shard_step: vectors must be device memory");
+    cyc::launch_step_range(g->gath, lo, hi, x, reinterpret_cast<const uint32_t*>(acc_words), out, flags,
+                           ctx->s);
+  });
+}
+
+cyc_status cyc_shard_demote(cyc_ctx* ctx, const uint32_t* x, uint32_t n, const uint64_t* acc_words,
+                            uint64_t* remaining, uint64_t* counts) {
+  return guard([&] {
+    require(ctx && (x || !n) && acc_words && remaining && counts, CYC_E_CONTRACT,
+            "shard_demote: null argument");
+    const size_t words = ((size_t)n + 31) / 32 + 2;
+    if (ctx->flush.bytes < words * 4) ctx->flush.alloc(words * 4, ctx->s);  // reused as scratch
+    CYC_CUDA(cudaMemsetAsync(ctx->flush.p, 0, words * 4, ctx->s));
+    cyc::launch_demote_async(x, n, reinterpret_cast<const uint32_t*>(acc_words),
+                             reinterpret_cast<uint32_t*>(remaining),
+                             reinterpret_cast<unsigned long long*>(counts), ctx->flush.as<uint32_t>(),
+                             ctx->s);
   });
 }
 

@@ -878,6 +878,51 @@ __global__ void k_step_pull(uint32_t n, const uint32_t* __restrict__ goff,
   if (wit != kNone) atomicMin(flags + 1, wit);
 }
 
+__global__ void k_step_range(uint32_t lo, uint32_t hi, const uint32_t* __restrict__ goff,
+                             const uint32_t* __restrict__ gcol, const uint32_t* __restrict__ x,
+                             const uint32_t* __restrict__ accw, uint32_t* __restrict__ out,
+                             uint32_t* __restrict__ flags) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  bool ch = false;
+  uint32_t wit = kNone;
+  for (uint32_t v = lo + blockIdx.x * blockDim.x + threadIdx.x; v < hi; v += stride) {
+    uint32_t best = x[v];
+    for (uint32_t i = goff[v]; i < goff[v + 1]; ++i) {
+      const uint32_t u = gcol[i];
+      uint32_t c = x[u];
+      if (((accw[u >> 5] >> (u & 31u)) & 1u) && u + 1u > c) c = u + 1u;
+      best = max(best, c);
+    }
+    out[v - lo] = best;
+    ch |= best != x[v];
+    if (best == v + 1u && ((accw[v >> 5] >> (v & 31u)) & 1u)) wit = min(wit, v);
+  }
+  if (__any_sync(__activemask(), ch) && lane_id() == 0) flags[0] = 1u;
+  if (wit != kNone) atomicMin(flags + 1, wit);
+}
+
+__global__ void k_demote_count(uint32_t nwords, const uint32_t* __restrict__ acc,
+                               uint32_t* __restrict__ used, uint32_t* __restrict__ rem,
+                               unsigned long long* __restrict__ counts) {
+  unsigned long long d = 0, f = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride) {
+    const uint32_t a = acc[i], u = used[i];
+    rem[i] = a & ~u;
+    d += __popc(a & u);
+    f += __popc(a & ~u);
+    used[i] = 0u;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(kFull, d, o);
+    f += __shfl_xor_sync(kFull, f, o);
+  }
+  if (lane_id() == 0) {
+    if (d) atomicAdd(counts, d);
+    if (f) atomicAdd(counts + 1, f);
+  }
+}
+
 __global__ void k_mark_used(const uint32_t* __restrict__ x, uint32_t n, uint32_t* used) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
@@ -1040,6 +1085,27 @@ void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* acc
   if (!gath.n) return;
   k_step_pull<<<grid_for(gath.n, 256, 8), 256, 0, s>>>(gath.n, gath.o(), gath.c(), x, accw, out,
                                                         flags);
+  CYC_LAUNCHED();
+}
+
+void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint32_t* x,
+                       const uint32_t* accw, uint32_t* out, uint32_t* flags, cudaStream_t s) {
+  uint32_t init[2] = {0u, kNone};
+  CYC_CUDA(cudaMemcpyAsync(flags, init, 8, cudaMemcpyHostToDevice, s));
+  if (hi <= lo) return;
+  k_step_range<<<grid_for(hi - lo, 256, 8), 256, 0, s>>>(lo, hi, gath.o(), gath.c(), x, accw, out,
+                                                         flags);
+  CYC_LAUNCHED();
+}
+
+void launch_demote_async(const uint32_t* x, uint32_t n, const uint32_t* accw, uint32_t* remaining,
+                         unsigned long long* counts, uint32_t* used, cudaStream_t s) {
+  const uint32_t nwords = (uint32_t)(((uint64_t)n + 31) / 32);
+  CYC_CUDA(cudaMemsetAsync(counts, 0, 16, s));
+  if (!n) return;
+  k_mark_used<<<grid_for(n, 256, 8), 256, 0, s>>>(x, n, used);
+  CYC_LAUNCHED();
+  k_demote_count<<<grid_for(nwords, 256, 8), 256, 0, s>>>(nwords, accw, used, remaining, counts);
   CYC_LAUNCHED();
 }
 

@@ -101,6 +101,13 @@ void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream
 void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* accw, uint32_t* out,
                       uint32_t* flags, cudaStream_t s);
 
+// Dense step over rows [lo, hi) only (sharded runs); flags as launch_step_pull.
+void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint32_t* x,
+                       const uint32_t* accw, uint32_t* out, uint32_t* flags, cudaStream_t s);
+// Device-only demotion for sharded runs: counts[0] = |D|, counts[1] = |F'|.
+void launch_demote_async(const uint32_t* x, uint32_t n, const uint32_t* accw, uint32_t* remaining,
+                         unsigned long long* counts, uint32_t* used_scratch, cudaStream_t s);
+
 // demote(): remaining = F & ~used(x); demoted ascending; returns |D| on host.
 uint64_t run_demote(const uint32_t* x, uint32_t n, const uint32_t* accw, uint32_t* remaining,
                     uint32_t* demoted, cudaStream_t s);

@@ -1,0 +1,118 @@
+"""CPU (gloo, world_size 2 and 3): the row-sharded MAP protocol
+(paper_0912_2555_b200/sharded.py) reproduces the single-device run_map —
+verdict, witness, MapStats and the final vector — with a host backend doing
+each rank's row-range step (oracle restatement, test-only)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class HostShardBackend:
+    """Row-range Jacobi step on the host (oracle restatement): test backend."""
+
+    def __init__(self, R, gather, n):
+        self.torch = torch
+        self.R = R
+        self.gather = gather
+        self.n = n
+
+    def zeros(self, k):
+        return torch.zeros(max(k, 1), dtype=torch.int32)
+
+    def acc_tensor(self, words):
+        return torch.from_numpy(words.view(np.int64).copy())
+
+    def step(self, x, acc, lo, hi, out):
+        xv = x.numpy().view(np.uint32)[: self.n]
+        words = acc.numpy().view(np.uint64)
+        full, _, _ = self.R.step(self.gather, xv, words)
+        sl = full[lo:hi]
+        out[: hi - lo] = torch.from_numpy(sl.view(np.int32).copy())
+        changed = int(np.any(sl != xv[lo:hi]))
+        accb = np.unpackbits(words.view(np.uint8), bitorder="little")[: self.n].astype(bool)
+        ids = np.arange(lo, hi, dtype=np.int64)
+        w = ids[(sl.astype(np.int64) == ids + 1) & accb[lo:hi]]
+        wit = int(w.min()) if len(w) else 0xFFFFFFFF
+        return torch.tensor([changed, np.int64(wit).astype(np.int32)], dtype=torch.int32)
+
+    def demote(self, x, acc):
+        rem, dem = self.R.demote(x.numpy().view(np.uint32)[: self.n], acc.numpy().view(np.uint64))
+        fsize = int(np.unpackbits(rem.view(np.uint8)).sum())
+        return torch.from_numpy(rem.view(np.int64).copy()), len(dem), fsize
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_0912_2555_b200 import sharded
+
+    R = oracle.Restatement()
+    out = []
+    for n, edges, accw, early in cases:
+        gat = R.transpose(R.build_snapshot(n, edges, True))
+        bounds = sharded.shard_bounds(gat.off, world)
+        be = HostShardBackend(R, gat, n)
+        res = sharded.run_map_sharded(be, dist, rank, world, bounds, accw, early)
+        out.append((res.verdict.cycle_found(), res.verdict.witness, res.stats.iterations,
+                    res.stats.kernel_calls, res.stats.demoted_total,
+                    res.final_values.numpy().view(np.uint32).copy()))
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _cases():
+    import oracle
+
+    R = oracle.Restatement()
+    rng = np.random.default_rng(88)
+    cases = []
+    for t in range(6):
+        n = int(rng.integers(20, 400))
+        e = rng.integers(0, n, size=(int(n * rng.choice([1, 2, 3])), 2)).astype(np.uint32)
+        acc = rng.random(n) < [0.05, 0.3][t % 2]
+        w = np.zeros((n + 63) // 64, np.uint64)
+        idx = np.flatnonzero(acc)
+        np.bitwise_or.at(w, idx >> 6, np.uint64(1) << (idx & 63).astype(np.uint64))
+        cases.append((n, e, w, bool(t % 3)))
+    p = R.preset(2)  # the config-2 family (closed form: (L+1) iterations, (L+1)^2 steps)
+    p.L, p.W, p.S = 6, 8, 4
+    R.prepare(p)
+    n, e, w = R.generate(p)
+    cases.append((n, e, w, True))
+    return R, cases
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_protocol_matches_single_device(world):
+    R, cases = _cases()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for (n, e, w, early), g in zip(cases, got):
+        ref = R.run_map(R.transpose(R.build_snapshot(n, e, True)), w, early)
+        assert g[:5] == (ref.cycle, ref.witness, ref.iterations, ref.kernel_calls, ref.demoted_total)
+        assert np.array_equal(g[5], ref.final_x)
