@@ -5,6 +5,8 @@
 // copies results back. C++ exceptions never cross the ABI: they become
 // status codes plus a thread-local message (errors.hpp:10-22 mapping).
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -34,6 +36,7 @@ struct cyc_ctx {
   cudaStream_t own = nullptr;  // the context's own stream (s may be an external one)
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   cyc::DevBuf flush;
+  cyc::BuildArena arena;  // grow-only build temporaries, reused by every build
   std::atomic<int> refs{1};
 };
 
@@ -42,6 +45,7 @@ void ctx_release(cyc_ctx* ctx) {
   if (ctx->refs.fetch_sub(1) != 1) return;
   cudaSetDevice(ctx->device);
   ctx->flush.release();
+  ctx->arena = cyc::BuildArena();
   cudaStreamSynchronize(ctx->s);
   cudaEventDestroy(ctx->e0);
   cudaEventDestroy(ctx->e1);
@@ -183,8 +187,10 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   g->ctx = ctx;
   g->orientation = orientation;
   const int snap_key_dst = orientation == CYC_TRANSPOSED;
-  cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>());
-  cyc::build_csr(de, m_log, n, !snap_key_dst, s, g->gath, err.as<uint32_t>());
+  cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>(), ctx->arena);
+  cyc::build_csr(de, m_log, n, !snap_key_dst, s, g->gath, err.as<uint32_t>(), ctx->arena);
+  const bool dbg = std::getenv("CYC_DEBUG_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
   uint32_t herr = 0;
   CYC_CUDA(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, s));
   CYC_CUDA(cudaStreamSynchronize(s));
@@ -193,6 +199,11 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   cyc::build_heavy(g->gath, 256, 256, s);
   cyc::build_ell(g->gath, s);
   load_acc(acc_words, n, g->acc, s);
+  if (dbg) {
+    CYC_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "[cyc build] heavy+ell+acc  %9.3f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
 }
 
 void fill_stats(const cyc::RunOut& o, cyc_map_stats* st) {

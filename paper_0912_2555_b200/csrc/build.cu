@@ -12,6 +12,11 @@
 //      network over global memory (larger hub rows)
 //   5. scan of unique counts, compaction into the final CSR.
 // Row offsets are u32 (snapshot edges < 2^32; checked by the caller).
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "build.cuh"
 
 namespace cyc {
@@ -22,6 +27,7 @@ constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr uint32_t kScanTile = kScanThreads * kScanItems;
 constexpr uint32_t kSmallRow = 16;
+constexpr uint32_t kWarpRow = 512;
 constexpr uint32_t kMedRow = 4096;
 constexpr int kMedThreads = 256;
 constexpr uint32_t kBigTile = 4096;
@@ -186,7 +192,8 @@ __device__ __forceinline__ uint32_t sort_small_row(uint32_t* __restrict__ seg, u
 __global__ void k_sort_small(uint32_t n, const uint32_t* __restrict__ roff,
                              uint32_t* __restrict__ raw, uint32_t* __restrict__ ucnt,
                              uint32_t* __restrict__ med, uint32_t* __restrict__ big,
-                             uint32_t* __restrict__ counts /* [0]=med [1]=big */) {
+                             uint32_t* __restrict__ wrows,
+                             uint32_t* __restrict__ counts /* [0]=med [1]=big [2]=warp */) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
     uint32_t b = roff[v], d = roff[v + 1] - b;
@@ -208,6 +215,8 @@ __global__ void k_sort_small(uint32_t n, const uint32_t* __restrict__ roff,
       ucnt[v] = sort_small_row<8>(seg, d);
     } else if (d <= kSmallRow) {
       ucnt[v] = sort_small_row<16>(seg, d);
+    } else if (d <= kWarpRow) {
+      wrows[atomicAdd(counts + 2, 1u)] = v;
     } else if (d <= kMedRow) {
       med[atomicAdd(counts + 0, 1u)] = v;
     } else {
@@ -411,6 +420,195 @@ __global__ void k_max_degree(uint32_t n, const uint32_t* __restrict__ off, uint3
   if ((threadIdx.x & 31u) == 0) atomicMax(out, mx);
 }
 
+// ------------------------------------------------- MSD bucket partition
+// Counting sort by row done as two levels so no atomic or write ever lands in
+// an n-sized random array: (1) bucket = row >> sh histogram in shared memory,
+// (2) partition of the log into buckets, (3) one CTA per bucket counting-sorts
+// its <= 2^sh rows in shared memory and emits the row offsets.
+constexpr int kPartThreads = 1024;
+constexpr uint32_t kBucketLog = 14;  // rows per bucket (pass 3 counters in smem)
+
+__global__ void __launch_bounds__(kPartThreads) k_bucket_hist(const uint2* __restrict__ edges, uint64_t m,
+                                                              uint32_t n, int key_dst, uint32_t sh,
+                                                              uint32_t nb, uint64_t per_block,
+                                                              uint32_t* __restrict__ bcnt,
+                                                              uint32_t* __restrict__ err) {
+  extern __shared__ uint32_t h[];
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const uint64_t lo = blockIdx.x * per_block, hi = min(m, lo + per_block);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint2 e = edges[i];
+    if (e.x >= n || e.y >= n) {
+      *err = 1u;
+      continue;
+    }
+    atomicAdd(&h[(key_dst ? e.y : e.x) >> sh], 1u);
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+    if (h[b]) atomicAdd(bcnt + b, h[b]);
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_bucket_scatter(const uint2* __restrict__ edges, uint64_t m,
+                                                                 uint32_t n, int key_dst, uint32_t sh,
+                                                                 uint32_t nb, uint64_t per_block,
+                                                                 uint32_t* __restrict__ bcur,
+                                                                 unsigned long long* __restrict__ tmp) {
+  extern __shared__ uint32_t h[];  // [0, nb): counts then cursors, [nb, 2nb): bases
+  uint32_t* base = h + nb;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const uint64_t lo = blockIdx.x * per_block, hi = min(m, lo + per_block);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint2 e = edges[i];
+    if (e.x < n && e.y < n) atomicAdd(&h[(key_dst ? e.y : e.x) >> sh], 1u);
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    base[b] = h[b] ? atomicAdd(bcur + b, h[b]) : 0u;
+    h[b] = 0;
+  }
+  __syncthreads();
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint2 e = edges[i];
+    if (e.x >= n || e.y >= n) continue;
+    const uint32_t row = key_dst ? e.y : e.x, other = key_dst ? e.x : e.y;
+    const uint32_t b = row >> sh;
+    const uint32_t pos = base[b] + atomicAdd(&h[b], 1u);
+    tmp[pos] = ((unsigned long long)row << 32) | other;
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_bucket_rows(const unsigned long long* __restrict__ tmp,
+                                                              const uint32_t* __restrict__ bbase,
+                                                              uint32_t n, uint32_t sh, uint32_t nb,
+                                                              uint32_t* __restrict__ roff,
+                                                              uint32_t* __restrict__ raw) {
+  extern __shared__ uint32_t cnt[];  // 2^sh row counters, then row cursors
+  __shared__ uint32_t warp_sums[kPartThreads / 32];
+  const uint32_t rows_per = 1u << sh;
+  const uint32_t per_thread = rows_per / kPartThreads;
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint32_t r0 = b << sh;
+    const uint32_t nr = min(rows_per, n - r0);
+    const uint32_t lo = bbase[b], hi = bbase[b + 1];
+    for (uint32_t j = threadIdx.x; j < rows_per; j += blockDim.x) cnt[j] = 0;
+    __syncthreads();
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+      atomicAdd(&cnt[(uint32_t)(tmp[i] >> 32) - r0], 1u);
+    __syncthreads();
+    // exclusive scan of cnt: each thread owns per_thread consecutive rows
+    uint32_t run = 0;
+    const uint32_t j0 = threadIdx.x * per_thread;
+    for (uint32_t k = 0; k < per_thread; ++k) run += cnt[j0 + k];
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    uint32_t incl = warp_incl_scan(run);
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t w = warp_sums[lane];
+      w = warp_incl_scan(w);
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    uint32_t pre = (wid ? warp_sums[wid - 1] : 0u) + incl - run;
+    for (uint32_t k = 0; k < per_thread; ++k) {
+      const uint32_t c = cnt[j0 + k];
+      cnt[j0 + k] = lo + pre;
+      if (j0 + k < nr) roff[r0 + j0 + k] = lo + pre;
+      pre += c;
+    }
+    __syncthreads();
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const unsigned long long t = tmp[i];
+      const uint32_t pos = atomicAdd(&cnt[(uint32_t)(t >> 32) - r0], 1u);
+      raw[pos] = (uint32_t)t;
+    }
+    if (b == nb - 1 && threadIdx.x == 0) roff[n] = hi;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------- warp sort (17..256 / row)
+// Bitonic network over 32*E register slots of one warp (slot i = r*32 + lane,
+// +inf padding), then in-register dedup; the warp writes the unique values
+// back to the front of its row segment.
+template <int E>
+__device__ uint32_t warp_sort_row(uint32_t* seg, uint32_t d) {
+  constexpr uint32_t N = 32u * E;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t a[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const uint32_t i = r * 32u + lane;
+    a[r] = i < d ? seg[i] : kNone;
+  }
+#pragma unroll
+  for (uint32_t k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int rj = (int)(j >> 5);
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int rp = r ^ rj;
+          if (rp > r) {
+            const uint32_t i = r * 32u + lane;
+            const bool up = (i & k) == 0;
+            const uint32_t x = a[r], y = a[rp];
+            if ((x > y) == up) {
+              a[r] = y;
+              a[rp] = x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const uint32_t i = r * 32u + lane;
+          const bool up = (i & k) == 0;
+          const bool lower = (lane & j) == 0;
+          const uint32_t y = __shfl_xor_sync(kFull, a[r], j);
+          a[r] = (lower == up) ? min(a[r], y) : max(a[r], y);
+        }
+      }
+    }
+  }
+  uint32_t written = 0;
+  uint32_t prev_last = kNone;  // last element of the previous register row (slot r*32-1)
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const uint32_t i = r * 32u + lane;
+    uint32_t prev = __shfl_up_sync(kFull, a[r], 1);
+    if (lane == 0) prev = prev_last;
+    const bool first = i < d && (i == 0 || a[r] != prev);
+    const uint32_t bal = __ballot_sync(kFull, first);
+    if (first) seg[written + __popc(bal & lanemask_lt())] = a[r];
+    written += __popc(bal);
+    prev_last = __shfl_sync(kFull, a[r], 31);
+  }
+  return written;
+}
+
+__global__ void k_sort_warp(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ counts,
+                            const uint32_t* __restrict__ roff, uint32_t* __restrict__ raw,
+                            uint32_t* __restrict__ ucnt) {
+  const uint32_t nrows = counts[2];
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = gw; r < nrows; r += nw) {
+    const uint32_t v = rows[r];
+    const uint32_t b = roff[v], d = roff[v + 1] - b;
+    uint32_t u;
+    if (d <= 64) u = warp_sort_row<2>(raw + b, d);
+    else if (d <= 128) u = warp_sort_row<4>(raw + b, d);
+    else if (d <= 256) u = warp_sort_row<8>(raw + b, d);
+    else u = warp_sort_row<16>(raw + b, d);
+    if ((threadIdx.x & 31u) == 0) ucnt[v] = u;
+  }
+}
+
 // per K in {1,2,4,8}: rows longer than K and the edges beyond K
 __global__ void k_ell_hist(uint32_t n, const uint32_t* __restrict__ off,
                            unsigned long long* __restrict__ out /* [8] */) {
@@ -532,33 +730,107 @@ void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* tot
 }
 
 // Builds a deduplicated, row-sorted CSR keyed by one half of each logged pair.
-void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
-               DevCsr& out, uint32_t* d_err) {
-  out.n = n;
-  out.off.alloc(((size_t)n + 1) * 4, s);
-  DevBuf cnt(((size_t)n + 1) * 4, s), roff(((size_t)n + 1) * 4, s);
-  DevBuf raw((m_log ? m_log : 1) * 4, s), ucnt(((size_t)n + 1) * 4, s);
-  DevBuf lists(((size_t)n + 1) * 4 * 2, s), counts(16, s), scratch;
-  uint32_t* c = cnt.as<uint32_t>();
+// Row offsets (roff, n+1) and the bucketed log (raw) of the counting sort.
+static void count_sort_rows(const uint2* e2, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
+                            uint32_t* roff, uint32_t* raw, uint32_t* d_err, BuildArena& ar) {
+  DevBuf& scratch = ar.scratch;
+  if (n <= (1u << 28) && m_log > 0) {
+    const uint32_t sh = kBucketLog;
+    const uint32_t nb = (uint32_t)(((uint64_t)n + (1u << sh) - 1) >> sh);
+    static bool attr = false;
+    if (!attr) {
+      CYC_CUDA(cudaFuncSetAttribute(k_bucket_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      CYC_CUDA(cudaFuncSetAttribute(k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+      CYC_CUDA(cudaFuncSetAttribute(k_bucket_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      attr = true;
+    }
+    uint32_t* bcnt = ar.get<uint32_t>(ar.bcnt, ((size_t)nb + 1) * 4, s);
+    uint32_t* bbase = ar.get<uint32_t>(ar.bbase, ((size_t)nb + 2) * 4, s);
+    uint32_t* bcur = ar.get<uint32_t>(ar.bcur, ((size_t)nb + 1) * 4, s);
+    unsigned long long* tmp = ar.get<unsigned long long>(ar.tmp, m_log * 8, s);
+    CYC_CUDA(cudaMemsetAsync(bcnt, 0, ((size_t)nb + 1) * 4, s));
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((uint64_t)sm_count() * 2, (m_log + 4095) / 4096);
+    const uint64_t per_block = (m_log + blocks - 1) / blocks;
+    k_bucket_hist<<<blocks, kPartThreads, nb * 4, s>>>(e2, m_log, n, key_dst, sh, nb, per_block,
+                                                       bcnt, d_err);
+    CYC_LAUNCHED();
+    exclusive_scan(bcnt, bbase, nb, nullptr, s, scratch);
+    CYC_CUDA(cudaMemcpyAsync(bcur, bbase, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
+    k_bucket_scatter<<<blocks, kPartThreads, nb * 8, s>>>(e2, m_log, n, key_dst, sh, nb, per_block,
+                                                          bcur, tmp);
+    CYC_LAUNCHED();
+    k_bucket_rows<<<std::min<uint32_t>(nb, sm_count() * 2), kPartThreads, (1u << sh) * 4, s>>>(
+        tmp, bbase, n, sh, nb, roff, raw);
+    CYC_LAUNCHED();
+    return;
+  }
+  uint32_t* c = ar.get<uint32_t>(ar.bcnt, ((size_t)n + 1) * 4, s);
   CYC_CUDA(cudaMemsetAsync(c, 0, ((size_t)n + 1) * 4, s));
-  CYC_CUDA(cudaMemsetAsync(counts.p, 0, 16, s));
-  const uint2* e2 = reinterpret_cast<const uint2*>(d_edges);
   if (m_log) {
     k_hist<<<grid_for(m_log, 256, 16), 256, 0, s>>>(e2, m_log, n, key_dst, c, d_err);
     CYC_LAUNCHED();
   }
-  exclusive_scan(c, roff.as<uint32_t>(), n, nullptr, s, scratch);
+  exclusive_scan(c, roff, n, nullptr, s, scratch);
   if (m_log) {
-    k_scatter<<<grid_for(m_log, 256, 16), 256, 0, s>>>(e2, m_log, n, key_dst, roff.as<uint32_t>(), c,
-                                                        raw.as<uint32_t>());
+    k_scatter<<<grid_for(m_log, 256, 16), 256, 0, s>>>(e2, m_log, n, key_dst, roff, c, raw);
     CYC_LAUNCHED();
   }
+}
+
+// A borrowed arena buffer with DevBuf's accessor.
+struct View {
+  uint32_t* p;
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+// CYC_DEBUG_TIMING=1 prints host-observed phase times of the build (stderr).
+struct PhaseTimer {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(cudaStream_t st) : on(std::getenv("CYC_DEBUG_TIMING") != nullptr), s(st) {
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cyc build] %-14s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
+void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
+               DevCsr& out, uint32_t* d_err, BuildArena& ar) {
+  PhaseTimer pt(s);
+  out.n = n;
+  out.off.alloc(((size_t)n + 1) * 4, s);
+  View roff{ar.get<uint32_t>(ar.roff, ((size_t)n + 1) * 4, s)};
+  View raw{ar.get<uint32_t>(ar.raw, (m_log ? m_log : 1) * 4, s)};
+  View ucnt{ar.get<uint32_t>(ar.ucnt, ((size_t)n + 1) * 4, s)};
+  View lists{ar.get<uint32_t>(ar.lists, ((size_t)n + 1) * 4 * 3, s)};
+  View counts{ar.get<uint32_t>(ar.counts, 16, s)};
+  DevBuf& scratch = ar.scratch;
+  CYC_CUDA(cudaMemsetAsync(counts.p, 0, 16, s));
+  CYC_CUDA(cudaMemsetAsync(roff.p, 0, ((size_t)n + 1) * 4, s));
+  const uint2* e2 = reinterpret_cast<const uint2*>(d_edges);
+  pt.mark("alloc");
+  count_sort_rows(e2, m_log, n, key_dst, s, roff.p, raw.p, d_err, ar);
+  pt.mark("count_sort");
   uint32_t* med = lists.as<uint32_t>();
   uint32_t* big = med + n + 1;
+  uint32_t* wrows = big + n + 1;
   uint32_t* cts = counts.as<uint32_t>();
   if (n) {
     k_sort_small<<<grid_for(n, 256, 16), 256, 0, s>>>(n, roff.as<uint32_t>(), raw.as<uint32_t>(),
-                                                       ucnt.as<uint32_t>(), med, big, cts);
+                                                       ucnt.as<uint32_t>(), med, big, wrows, cts);
+    CYC_LAUNCHED();
+    k_sort_warp<<<sm_count() * 8, 256, 0, s>>>(wrows, cts, roff.as<uint32_t>(), raw.as<uint32_t>(),
+                                               ucnt.as<uint32_t>());
     CYC_LAUNCHED();
     k_sort_med<<<sm_count() * 8, kMedThreads, 0, s>>>(med, cts, roff.as<uint32_t>(),
                                                        raw.as<uint32_t>(), ucnt.as<uint32_t>());
@@ -567,6 +839,7 @@ void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst,
                                                   ucnt.as<uint32_t>());
     CYC_LAUNCHED();
   }
+  pt.mark("row_sort");
   exclusive_scan(ucnt.as<uint32_t>(), out.off.as<uint32_t>(), n, nullptr, s, scratch);
   uint32_t m = 0;
   CYC_CUDA(cudaMemcpyAsync(&m, out.off.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
@@ -577,15 +850,15 @@ void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst,
     k_compact_small<<<grid_for(n, 256, 16), 256, 0, s>>>(n, roff.as<uint32_t>(), out.off.as<uint32_t>(),
                                                          raw.as<uint32_t>(), out.col.as<uint32_t>());
     CYC_LAUNCHED();
-    k_compact_list<<<sm_count() * 4, 256, 0, s>>>(med, cts + 0, roff.as<uint32_t>(),
-                                                  out.off.as<uint32_t>(), raw.as<uint32_t>(),
-                                                  out.col.as<uint32_t>());
-    CYC_LAUNCHED();
-    k_compact_list<<<sm_count() * 4, 256, 0, s>>>(big, cts + 1, roff.as<uint32_t>(),
-                                                  out.off.as<uint32_t>(), raw.as<uint32_t>(),
-                                                  out.col.as<uint32_t>());
-    CYC_LAUNCHED();
+    for (int li = 0; li < 3; ++li) {
+      const uint32_t* lst = li == 0 ? med : li == 1 ? big : wrows;
+      k_compact_list<<<sm_count() * 4, 256, 0, s>>>(lst, cts + li, roff.as<uint32_t>(),
+                                                    out.off.as<uint32_t>(), raw.as<uint32_t>(),
+                                                    out.col.as<uint32_t>());
+      CYC_LAUNCHED();
+    }
   }
+  pt.mark("compact");
 }
 
 void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s) {

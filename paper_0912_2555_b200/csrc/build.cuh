@@ -26,12 +26,23 @@ struct DevCsr {
   const uint32_t* c() const { return col.as<uint32_t>(); }
 };
 
+// Grow-only build temporaries owned by a context and reused by every build
+// (pool allocations of several GB per build cost up to ~1 s of mapping).
+struct BuildArena {
+  DevBuf tmp, raw, roff, ucnt, lists, counts, bcnt, bbase, bcur, scratch;
+  template <class T>
+  T* get(DevBuf& b, size_t bytes, cudaStream_t s) {
+    if (b.bytes < bytes) b.alloc(bytes + bytes / 8, s);
+    return b.as<T>();
+  }
+};
+
 int sm_count();
 uint32_t grid_for(uint64_t items, int threads, int per_sm);
 void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* total,
                     cudaStream_t s, DevBuf& scratch);
 void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
-               DevCsr& out, uint32_t* d_err);
+               DevCsr& out, uint32_t* d_err, BuildArena& ar);
 void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s);
 // Chooses ell_k in {1,2,4,8} minimising per-step pull bytes and builds the slab.
 void build_ell(DevCsr& g, cudaStream_t s);
