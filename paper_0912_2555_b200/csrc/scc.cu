@@ -14,6 +14,9 @@
 // Every SCC found is kept iff it holds an accepting vertex and is cyclic
 // (size >= 2 or a self-loop). Passes are dense; convergence flags are read
 // by the host every few passes.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "scc.cuh"
@@ -38,11 +41,13 @@ __global__ void k_reach_init(uint32_t n, const uint64_t* __restrict__ acc, uint8
 
 // flag |= 1 if any vertex newly reached. rows: for fw use the gather index
 // (predecessors), for bw the snapshot rows (successors).
+// Heavy rows (degree > heavy) are left to the *_chunks kernels, one warp per
+// 256-edge chunk (R-MAT hubs would otherwise serialise a pass on one thread).
 __global__ void k_reach(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                        uint8_t* mark, uint32_t* flag) {
+                        uint32_t heavy, uint8_t* mark, uint32_t* flag) {
   bool ch = false;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (mark[v]) continue;
+    if (mark[v] || off[v + 1] - off[v] > heavy) continue;
     for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
       if (((volatile uint8_t*)mark)[col[i]]) {
         mark[v] = 1;
@@ -52,6 +57,22 @@ __global__ void k_reach(uint32_t n, const uint32_t* __restrict__ off, const uint
     }
   }
   if (ch) *flag = 1;
+}
+
+__global__ void k_reach_chunks(const uint4* __restrict__ chunks, uint32_t nch,
+                               const uint32_t* __restrict__ col, uint8_t* mark, uint32_t* flag) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t c = gw; c < nch; c += nw) {
+    const uint4 ch = chunks[c];
+    if (((volatile uint8_t*)mark)[ch.x]) continue;
+    bool hit = false;
+    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) hit |= ((volatile uint8_t*)mark)[col[i]] != 0;
+    if (__any_sync(kFull, hit) && lane == 0) {
+      mark[ch.x] = 1;
+      *flag = 1;
+    }
+  }
 }
 
 __global__ void k_and(uint32_t n, const uint8_t* fw, const uint8_t* bw, uint8_t* active) {
@@ -88,11 +109,11 @@ __global__ void k_color_init(uint32_t n, const uint8_t* active, uint32_t* color,
 }
 
 __global__ void k_color_prop(uint32_t n, const uint32_t* __restrict__ goff,
-                             const uint32_t* __restrict__ gcol, const uint8_t* active,
+                             const uint32_t* __restrict__ gcol, uint32_t heavy, const uint8_t* active,
                              uint32_t* color, uint32_t* flag) {
   bool ch = false;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (!active[v]) continue;
+    if (!active[v] || goff[v + 1] - goff[v] > heavy) continue;
     uint32_t c = ((volatile uint32_t*)color)[v], best = c;
     for (uint32_t i = goff[v]; i < goff[v + 1]; ++i) {
       uint32_t u = gcol[i];
@@ -104,6 +125,27 @@ __global__ void k_color_prop(uint32_t n, const uint32_t* __restrict__ goff,
     }
   }
   if (ch) *flag = 1;
+}
+
+__global__ void k_color_chunks(const uint4* __restrict__ chunks, uint32_t nch,
+                               const uint32_t* __restrict__ gcol, const uint8_t* active,
+                               uint32_t* color, uint32_t* flag) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t c = gw; c < nch; c += nw) {
+    const uint4 ch = chunks[c];
+    if (!active[ch.x]) continue;
+    uint32_t best = 0;
+    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) {
+      const uint32_t u = gcol[i];
+      if (active[u]) best = max(best, ((volatile uint32_t*)color)[u]);
+    }
+    best = __reduce_max_sync(kFull, best);
+    if (lane == 0 && best > ((volatile uint32_t*)color)[ch.x]) {
+      atomicMax(color + ch.x, best);
+      *flag = 1;
+    }
+  }
 }
 
 __global__ void k_roots(uint32_t n, const uint8_t* active, const uint32_t* color, uint8_t* inscc,
@@ -118,11 +160,11 @@ __global__ void k_roots(uint32_t n, const uint8_t* active, const uint32_t* color
 }
 
 __global__ void k_bw_color(uint32_t n, const uint32_t* __restrict__ soff,
-                           const uint32_t* __restrict__ scol, const uint8_t* active,
+                           const uint32_t* __restrict__ scol, uint32_t heavy, const uint8_t* active,
                            const uint32_t* color, uint8_t* inscc, uint32_t* flag) {
   bool ch = false;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (!active[v] || inscc[v]) continue;
+    if (!active[v] || inscc[v] || soff[v + 1] - soff[v] > heavy) continue;
     const uint32_t c = color[v];
     for (uint32_t i = soff[v]; i < soff[v + 1]; ++i) {
       uint32_t w = scol[i];
@@ -134,6 +176,28 @@ __global__ void k_bw_color(uint32_t n, const uint32_t* __restrict__ soff,
     }
   }
   if (ch) *flag = 1;
+}
+
+__global__ void k_bw_chunks(const uint4* __restrict__ chunks, uint32_t nch,
+                            const uint32_t* __restrict__ scol, const uint8_t* active,
+                            const uint32_t* color, uint8_t* inscc, uint32_t* flag) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t c = gw; c < nch; c += nw) {
+    const uint4 ch = chunks[c];
+    const uint32_t v = ch.x;
+    if (!active[v] || ((volatile uint8_t*)inscc)[v]) continue;
+    const uint32_t cv = color[v];
+    bool hit = false;
+    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) {
+      const uint32_t w = scol[i];
+      hit |= active[w] && color[w] == cv && ((volatile uint8_t*)inscc)[w];
+    }
+    if (__any_sync(kFull, hit) && lane == 0) {
+      inscc[v] = 1;
+      *flag = 1;
+    }
+  }
 }
 
 __device__ bool has_self_loop(const uint32_t* off, const uint32_t* col, uint32_t v) {
@@ -187,23 +251,37 @@ __global__ void k_kept_list(uint32_t n, const uint8_t* keep, const uint32_t* new
     if (keep[v]) kept[newid[v]] = v;
 }
 
+// One warp per kept row (rows of R-MAT hubs are long): count, then an
+// order-preserving ballot compaction of the kept columns.
 __global__ void k_filter_count(uint32_t k, const uint32_t* kept, const uint32_t* __restrict__ off,
                                const uint32_t* __restrict__ col, const uint8_t* keep, uint32_t* cnt) {
-  for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < k; a += gridDim.x * blockDim.x) {
-    uint32_t v = kept[a], c = 0;
-    for (uint32_t i = off[v]; i < off[v + 1]; ++i) c += keep[col[i]];
-    cnt[a] = c;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t a = gw; a < k; a += nw) {
+    const uint32_t v = kept[a];
+    uint32_t c = 0;
+    for (uint32_t i = off[v] + lane; i < off[v + 1]; i += 32u) c += keep[col[i]];
+    c = __reduce_add_sync(kFull, c);
+    if (lane == 0) cnt[a] = c;
   }
 }
 
 __global__ void k_filter_fill(uint32_t k, const uint32_t* kept, const uint32_t* __restrict__ off,
                               const uint32_t* __restrict__ col, const uint8_t* keep,
                               const uint32_t* newid, const uint32_t* noff, uint32_t* ncol) {
-  for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < k; a += gridDim.x * blockDim.x) {
-    uint32_t v = kept[a], o = noff[a];
-    for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
-      uint32_t w = col[i];
-      if (keep[w]) ncol[o++] = newid[w];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t a = gw; a < k; a += nw) {
+    const uint32_t v = kept[a];
+    uint32_t o = noff[a];
+    const uint32_t b = off[v], e = off[v + 1];
+    for (uint32_t i0 = b; i0 < e; i0 += 32u) {
+      const uint32_t i = i0 + lane;
+      const uint32_t w = i < e ? col[i] : 0u;
+      const bool in = i < e && keep[w];
+      const uint32_t bal = __ballot_sync(kFull, in);
+      if (in) ncol[o + __popc(bal & lanemask_lt())] = newid[w];
+      o += __popc(bal);
     }
   }
 }
@@ -221,18 +299,33 @@ __global__ void k_pack_acc(uint32_t k, const uint32_t* kept, const uint64_t* __r
   }
 }
 
-// Runs `pass` until it leaves the flag clear.
+// Runs `pass` until it leaves the flag clear; returns the number of passes.
 template <class F>
-void until_stable(uint32_t* dflag, cudaStream_t s, F&& pass) {
+int until_stable(uint32_t* dflag, cudaStream_t s, F&& pass) {
+  int k = 0;
   for (;;) {
     uint32_t h = 0;
     CYC_CUDA(cudaMemsetAsync(dflag, 0, 4, s));
     pass();
+    ++k;
     CYC_CUDA(cudaMemcpyAsync(&h, dflag, 4, cudaMemcpyDeviceToHost, s));
     CYC_CUDA(cudaStreamSynchronize(s));
     if (!h) break;
   }
+  return k;
 }
+
+struct SccLog {
+  bool on = std::getenv("CYC_DEBUG_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, int passes) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cyc scc] %-12s passes %5d %9.3f ms\n", what, passes,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 void filter_csr(const DevCsr& in, const uint8_t* keep, const uint32_t* newid, const uint32_t* kept,
                 uint32_t k, cudaStream_t s, DevCsr& out) {
@@ -240,7 +333,7 @@ void filter_csr(const DevCsr& in, const uint8_t* keep, const uint32_t* newid, co
   out.off.alloc(((size_t)k + 1) * 4, s);
   DevBuf cnt(((size_t)k + 1) * 4, s), scratch;
   if (k) {
-    k_filter_count<<<grid_for(k, kT, 8), kT, 0, s>>>(k, kept, in.o(), in.c(), keep, cnt.as<uint32_t>());
+    k_filter_count<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), keep, cnt.as<uint32_t>());
     CYC_LAUNCHED();
   }
   exclusive_scan(cnt.as<uint32_t>(), out.off.as<uint32_t>(), k, nullptr, s, scratch);
@@ -250,8 +343,8 @@ void filter_csr(const DevCsr& in, const uint8_t* keep, const uint32_t* newid, co
   out.m = m;
   out.col.alloc(((size_t)m + 1) * 4, s);
   if (k) {
-    k_filter_fill<<<grid_for(k, kT, 8), kT, 0, s>>>(k, kept, in.o(), in.c(), keep, newid,
-                                                    out.off.as<uint32_t>(), out.col.as<uint32_t>());
+    k_filter_fill<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), keep, newid,
+                                                out.off.as<uint32_t>(), out.col.as<uint32_t>());
     CYC_LAUNCHED();
   }
 }
@@ -268,38 +361,69 @@ void scc_keep_mask(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc, 
   DevBuf flag(16, s);
   uint32_t* f = flag.as<uint32_t>();
   const uint32_t grid = grid_for(n, kT, 8);
+  SccLog lg;
   k_reach_init<<<grid, kT, 0, s>>>(n, acc, fw.as<uint8_t>(), bw.as<uint8_t>());
   CYC_LAUNCHED();
-  until_stable(f, s, [&] {
-    k_reach<<<grid, kT, 0, s>>>(n, gath.o(), gath.c(), fw.as<uint8_t>(), f);
+  const uint32_t hg = gath.heavy_deg ? gath.heavy_deg : kNone, hs = snap.heavy_deg ? snap.heavy_deg : kNone;
+  const uint32_t cgrid = sm_count() * 8;
+  int np = until_stable(f, s, [&] {
+    k_reach<<<grid, kT, 0, s>>>(n, gath.o(), gath.c(), hg, fw.as<uint8_t>(), f);
     CYC_LAUNCHED();
+    if (gath.n_heavy_chunks) {
+      k_reach_chunks<<<cgrid, kT, 0, s>>>(gath.heavy.as<uint4>(), gath.n_heavy_chunks, gath.c(),
+                                          fw.as<uint8_t>(), f);
+      CYC_LAUNCHED();
+    }
   });
-  until_stable(f, s, [&] {
-    k_reach<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), bw.as<uint8_t>(), f);
+  lg.mark("reach-fw", np);
+  np = until_stable(f, s, [&] {
+    k_reach<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), hs, bw.as<uint8_t>(), f);
     CYC_LAUNCHED();
+    if (snap.n_heavy_chunks) {
+      k_reach_chunks<<<cgrid, kT, 0, s>>>(snap.heavy.as<uint4>(), snap.n_heavy_chunks, snap.c(),
+                                          bw.as<uint8_t>(), f);
+      CYC_LAUNCHED();
+    }
   });
+  lg.mark("reach-bw", np);
   k_and<<<grid, kT, 0, s>>>(n, fw.as<uint8_t>(), bw.as<uint8_t>(), active.as<uint8_t>());
   CYC_LAUNCHED();
+  int rounds = 0;
   for (;;) {
-    until_stable(f, s, [&] {
+    ++rounds;
+    np = until_stable(f, s, [&] {
       k_trim<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), gath.o(), gath.c(), active.as<uint8_t>(), f);
       CYC_LAUNCHED();
     });
+    lg.mark("trim", np);
     k_color_init<<<grid, kT, 0, s>>>(n, active.as<uint8_t>(), color.as<uint32_t>(), inscc.as<uint8_t>());
     CYC_LAUNCHED();
-    until_stable(f, s, [&] {
-      k_color_prop<<<grid, kT, 0, s>>>(n, gath.o(), gath.c(), active.as<uint8_t>(),
+    np = until_stable(f, s, [&] {
+      k_color_prop<<<grid, kT, 0, s>>>(n, gath.o(), gath.c(), hg, active.as<uint8_t>(),
                                        color.as<uint32_t>(), f);
       CYC_LAUNCHED();
+      if (gath.n_heavy_chunks) {
+        k_color_chunks<<<cgrid, kT, 0, s>>>(gath.heavy.as<uint4>(), gath.n_heavy_chunks, gath.c(),
+                                            active.as<uint8_t>(), color.as<uint32_t>(), f);
+        CYC_LAUNCHED();
+      }
     });
+    lg.mark("color", np);
     k_roots<<<grid, kT, 0, s>>>(n, active.as<uint8_t>(), color.as<uint32_t>(), inscc.as<uint8_t>(),
                                 rsize.as<uint32_t>(), rflag.as<uint32_t>());
     CYC_LAUNCHED();
-    until_stable(f, s, [&] {
-      k_bw_color<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), active.as<uint8_t>(),
+    np = until_stable(f, s, [&] {
+      k_bw_color<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), hs, active.as<uint8_t>(),
                                      color.as<uint32_t>(), inscc.as<uint8_t>(), f);
       CYC_LAUNCHED();
+      if (snap.n_heavy_chunks) {
+        k_bw_chunks<<<cgrid, kT, 0, s>>>(snap.heavy.as<uint4>(), snap.n_heavy_chunks, snap.c(),
+                                         active.as<uint8_t>(), color.as<uint32_t>(),
+                                         inscc.as<uint8_t>(), f);
+        CYC_LAUNCHED();
+      }
     });
+    lg.mark("bw-color", np);
     k_scc_stats<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), acc, inscc.as<uint8_t>(),
                                     color.as<uint32_t>(), rsize.as<uint32_t>(), rflag.as<uint32_t>());
     CYC_LAUNCHED();
