@@ -146,6 +146,28 @@ cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_wor
  * latest any warp reached that point; take the max over the slots). */
 cyc_status cyc_map_trace(const cyc_graph* g, uint64_t* out, uint32_t cap, uint32_t* len);
 
+/* scc_verdict (reference oracle.cpp:32-98) on the device: cycle iff some
+ * accepting vertex lies in a cyclic SCC; cyclic_accepting (nullable,
+ * capacity n) receives those vertices ascending, witness the smallest. An
+ * independent verdict at scales the reference's Tarjan cannot reach. */
+cyc_status cyc_scc_verdict(cyc_ctx* ctx, const cyc_graph* g, int32_t* cycle, uint32_t* witness,
+                           uint32_t* cyclic_accepting, uint64_t* count);
+
+/* run_owcty (reference owcty.hpp:12-31, owcty.cpp:56-87) on the device over
+ * the snapshot relation (the reference runs it on a forward snapshot,
+ * cycheck_main.cpp:98-106): alternate proper reachability from accepting
+ * vertices and in-degree-0 elimination until the set is empty or unchanged.
+ * witness = min accepting survivor (UINT32_MAX when none). acc_words NULL =
+ * the snapshot's accepting set. */
+typedef struct cyc_owcty_stats {
+  uint64_t outer_iterations;
+  uint64_t final_size;
+  double reach_ms;
+  double elim_ms;
+} cyc_owcty_stats;
+cyc_status cyc_owcty(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words, int32_t* cycle,
+                     uint32_t* witness, cyc_owcty_stats* stats);
+
 /* ---- one-call pipeline: edge log -> verdict ----------------------------- */
 /* cycheck graph / explore final round (cycheck_main.cpp:88-97,
  * explore.cpp:71-124): build_snapshot [+ restrict] + run_map. Timings in

@@ -110,6 +110,8 @@ class Restatement:
         L.cyo_demote.argtypes = [_P, C.c_uint32, _P, _P, _P]
         L.cyo_demote.restype = C.c_uint64
         L.cyo_run_map.argtypes = [C.POINTER(_Csr), _P, C.c_int, _P, _P, _P, _P, C.c_uint64]
+        L.cyo_run_owcty.argtypes = [C.POINTER(_Csr), _P, C.POINTER(C.c_int), C.POINTER(C.c_uint32),
+                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.cyo_vector_hash.argtypes = [_P, C.c_uint32]
         L.cyo_vector_hash.restype = C.c_uint64
         L.cyo_generate.argtypes = [_P, _P, _P]
@@ -235,6 +237,14 @@ class Restatement:
             raise ValueError("bad generator params")
         return p
 
+    def run_owcty(self, snap: Csr, acc):
+        """owcty.cpp:56-87 over the rows of `snap` -> (cycle, witness|None, outer_iterations, final_size)."""
+        c, w, it, fs = C.c_int(), C.c_uint32(), C.c_uint64(), C.c_uint64()
+        aw = _words(acc, snap.n)
+        self.lib.cyo_run_owcty(C.byref(self._to_c(snap)), aw.ctypes.data, C.byref(c), C.byref(w),
+                               C.byref(it), C.byref(fs))
+        return bool(c.value), (w.value if c.value else None), int(it.value), int(fs.value)
+
     def generate(self, p):
         e = np.zeros((int(p.m), 2), np.uint32)
         acc = np.zeros(max((int(p.n) + 63) // 64, 1), np.uint64)
@@ -263,6 +273,7 @@ class Reference:
         L.ref_demote.argtypes = [_P, C.c_uint32, _P, _P, _P, C.POINTER(C.c_uint64)]
         L.ref_run_map.argtypes = [_P, _P, C.c_int, C.c_int, _P, _P, _P, _P, C.c_uint64, C.c_int]
         L.ref_scc_verdict.argtypes = [_P, C.POINTER(C.c_int)]
+        L.ref_run_owcty.argtypes = [_P, _P, _P]
         L.ref_time_steps.argtypes = [_P, C.c_int, C.c_uint64, C.c_double, _P, C.POINTER(C.c_uint64)]
         L.ref_time_build.argtypes = [_P, C.c_int, C.POINTER(C.c_double)]
         L.ref_hw_threads.restype = C.c_int
@@ -369,6 +380,14 @@ class RefSnapshot:
         c = C.c_int()
         self.ref._ok(self.ref.lib.ref_scc_verdict(self.h, C.byref(c)))
         return bool(c.value)
+
+    def run_owcty(self, acc=None):
+        """run_owcty (owcty.cpp:56-87) -> (cycle, witness|None, outer_iterations, final_size)."""
+        out = np.zeros(4, np.uint64)
+        aw = None if acc is None else _words(acc, self.n)
+        self.ref._ok(self.ref.lib.ref_run_owcty(self.h, None if aw is None else aw.ctypes.data,
+                                                out.ctypes.data))
+        return bool(out[0]), (int(out[1]) if out[0] else None), int(out[2]), int(out[3])
 
     def time_steps(self, workers: int, max_steps: int, max_seconds: float):
         t = np.zeros(2, np.float64)

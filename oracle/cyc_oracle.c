@@ -309,3 +309,90 @@ int cyo_gen_preset(int index, void* gen_params) {
 }
 
 int cyo_gen_prepare(void* gen_params) { return cyc_gen_init((cyc_gen_params*)gen_params); }
+
+/* owcty.cpp:14-33 — vertices of `in` reachable by >= 1 edge, through `in`,
+ * from an accepting member of `in` (explicit stack, any visiting order). */
+static void owcty_reach(const cyo_csr* g, const uint8_t* in, const uint64_t* acc, uint8_t* out,
+                        uint32_t* stack) {
+  const uint32_t n = g->n;
+  size_t top = 0;
+  memset(out, 0, n);
+  for (uint32_t v = 0; v < n; ++v)
+    if (in[v] && ((acc[v >> 6] >> (v & 63)) & 1)) stack[top++] = v;
+  /* sources are expanded once even if never re-reached */
+  while (top) {
+    const uint32_t u = stack[--top];
+    for (uint64_t i = g->off[u]; i < g->off[u + 1]; ++i) {
+      const uint32_t c = g->col[i];
+      if (in[c] && !out[c]) {
+        out[c] = 1;
+        if (!((acc[c >> 6] >> (c & 63)) & 1)) stack[top++] = c; /* accepting c already seeded */
+      }
+    }
+  }
+}
+
+/* owcty.cpp:35-54 — drop members without a predecessor in the set, repeatedly. */
+static void owcty_elim(const cyo_csr* g, uint8_t* set, uint32_t* indeg, uint32_t* queue) {
+  const uint32_t n = g->n;
+  size_t head = 0, tail = 0;
+  memset(indeg, 0, (size_t)n * 4);
+  for (uint32_t u = 0; u < n; ++u)
+    if (set[u])
+      for (uint64_t i = g->off[u]; i < g->off[u + 1]; ++i)
+        if (set[g->col[i]]) indeg[g->col[i]]++;
+  for (uint32_t v = 0; v < n; ++v)
+    if (set[v] && !indeg[v]) queue[tail++] = v;
+  while (head < tail) {
+    const uint32_t v = queue[head++];
+    set[v] = 0;
+    for (uint64_t i = g->off[v]; i < g->off[v + 1]; ++i) {
+      const uint32_t c = g->col[i];
+      if (set[c] && --indeg[c] == 0) queue[tail++] = c;
+    }
+  }
+}
+
+void cyo_run_owcty(const cyo_csr* g, const uint64_t* acc, int* cycle, uint32_t* witness,
+                   uint64_t* outer_iterations, uint64_t* final_size) {
+  const uint32_t n = g->n;
+  *cycle = 0;
+  *witness = 0xFFFFFFFFu;
+  *outer_iterations = 0;
+  *final_size = 0;
+  if (n == 0) return;
+  uint8_t* set = (uint8_t*)malloc(n);
+  uint8_t* nxt = (uint8_t*)malloc(n);
+  uint32_t* a = (uint32_t*)malloc((size_t)n * 4);
+  uint32_t* b = (uint32_t*)malloc((size_t)n * 4);
+  memset(set, 1, n);
+  uint64_t live = n;
+  for (;;) {
+    /* a vertex may sit on the reach stack at most twice (seed + reached) */
+    uint32_t* stack = (uint32_t*)malloc((size_t)n * 8);
+    owcty_reach(g, set, acc, nxt, stack);
+    free(stack);
+    owcty_elim(g, nxt, a, b);
+    ++*outer_iterations;
+    uint64_t cnt = 0;
+    int same = 1;
+    for (uint32_t v = 0; v < n; ++v) {
+      cnt += nxt[v];
+      same &= nxt[v] == set[v];
+    }
+    memcpy(set, nxt, n);
+    live = cnt;
+    if (cnt == 0 || same) break;
+  }
+  *final_size = live;
+  for (uint32_t v = 0; v < n && live; ++v)
+    if (set[v] && ((acc[v >> 6] >> (v & 63)) & 1)) {
+      *cycle = 1;
+      *witness = v;
+      break;
+    }
+  free(set);
+  free(nxt);
+  free(a);
+  free(b);
+}

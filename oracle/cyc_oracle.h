@@ -78,6 +78,12 @@ uint64_t cyo_demote(const uint32_t* x, uint32_t n, const uint64_t* acc, uint64_t
 void cyo_run_map(const cyo_csr* gather, const uint64_t* acc, int early_exit, cyo_map_stats* st,
                  uint32_t* final_x, uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap);
 
+/* owcty.cpp:14-87 — OWCTY over the rows of g (row u = successors of u):
+ * approx = V; repeat { reach; elim } until empty or unchanged. witness =
+ * min accepting survivor (0xFFFFFFFF when none), final_size = |approx|. */
+void cyo_run_owcty(const cyo_csr* g, const uint64_t* acc, int* cycle, uint32_t* witness,
+                   uint64_t* outer_iterations, uint64_t* final_size);
+
 /* Order-independent 64-bit hash of a map vector (sum of mixed (v, x[v])). */
 uint64_t cyo_vector_hash(const uint32_t* x, uint32_t n);
 

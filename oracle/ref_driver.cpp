@@ -20,6 +20,7 @@
 #include "cycheck/graph.hpp"
 #include "cycheck/map_engine.hpp"
 #include "cycheck/oracle.hpp"
+#include "cycheck/owcty.hpp"
 #include "cycheck/parallel.hpp"
 #include "../include/cyc_gen.h"
 
@@ -249,6 +250,21 @@ int ref_scc_verdict(void* h, int* cycle) {
   auto edges = s->snap.edge_list();
   OracleVerdict ov = scc_verdict(edges, s->snap.n, s->snap.accepting, ~0ull);
   *cycle = ov.verdict.cycle_found();
+  return 0;
+  REF_CATCH
+}
+
+// run_owcty (owcty.cpp:56-87) on the snapshot: out = {cycle, witness,
+// outer_iterations, final_size}.
+int ref_run_owcty(void* h, const uint64_t* acc, uint64_t* out) {
+  REF_TRY
+  auto* s = static_cast<Snap*>(h);
+  Bitset a = acc ? bitset_from(acc, s->snap.n) : s->snap.accepting;
+  auto [v, st] = run_owcty(s->snap, a);
+  out[0] = v.cycle_found();
+  out[1] = v.witness ? *v.witness : 0xFFFFFFFFull;
+  out[2] = st.outer_iterations;
+  out[3] = st.final_size;
   return 0;
   REF_CATCH
 }

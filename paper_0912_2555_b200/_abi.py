@@ -48,6 +48,15 @@ class MapOptionsC(C.Structure):
     ]
 
 
+class OwctyStatsC(C.Structure):
+    _fields_ = [
+        ("outer_iterations", C.c_uint64),
+        ("final_size", C.c_uint64),
+        ("reach_ms", C.c_double),
+        ("elim_ms", C.c_double),
+    ]
+
+
 class MapStatsC(C.Structure):
     _fields_ = [
         ("cycle_found", C.c_int32),
@@ -118,6 +127,8 @@ _SIGS = {
                               C.c_uint64]),
     "cyc_check": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.c_int,
                             C.POINTER(MapOptionsC), C.POINTER(MapStatsC), C.POINTER(C.c_double)]),
+    "cyc_scc_verdict": (C.c_int, [_P, _P, C.POINTER(C.c_int32), _U32P, _P, _U64P]),
+    "cyc_owcty": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int32), _U32P, C.POINTER(OwctyStatsC)]),
     "cyc_gen_fill": (C.c_int, [_P, C.POINTER(GenParams), _P, _P]),
     "cyc_gen_preset": (C.c_int, [C.c_int, C.POINTER(GenParams)]),
     "cyc_gen_prepare": (C.c_int, [C.POINTER(GenParams)]),

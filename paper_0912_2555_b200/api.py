@@ -634,6 +634,45 @@ def check_graph(n: int, edges, accepting, orientation: Orientation = Orientation
     return verdict, stats
 
 
+@dataclass
+class OracleVerdict:
+    """oracle.hpp:20-23."""
+
+    verdict: Verdict
+    cyclic_accepting: np.ndarray
+
+
+def scc_verdict(snap: CsrSnapshot) -> OracleVerdict:
+    """scc_verdict (oracle.cpp:32-98) on the device, over the snapshot relation
+    (SCCs do not depend on orientation)."""
+    cyc_, w, cnt = C.c_int32(), C.c_uint32(), C.c_uint64()
+    out = np.zeros(max(snap.n, 1), dtype=np.uint32)
+    check(_abi.lib().cyc_scc_verdict(snap.context.handle, snap.handle, C.byref(cyc_), C.byref(w),
+                                     ptr(out), C.byref(cnt)))
+    v = Verdict.cycle(w.value) if cyc_.value else Verdict.no_cycle()
+    return OracleVerdict(v, out[: cnt.value].copy())
+
+
+@dataclass
+class OwctyStats:
+    """OwctyStats (owcty.hpp:12-17)."""
+    outer_iterations: int = 0
+    reach_ms: float = 0.0
+    elim_ms: float = 0.0
+    final_size: int = 0
+
+
+def run_owcty(snap: CsrSnapshot, accepting=None) -> "tuple[Verdict, OwctyStats]":
+    """run_owcty (owcty.hpp:28-31, owcty.cpp:56-87) on the device over the
+    snapshot relation; the reference runs it on a forward snapshot."""
+    cyc_, w, st = C.c_int32(), C.c_uint32(), _abi.OwctyStatsC()
+    aw = None if accepting is None else _acc_words(accepting, snap.n)
+    check(_abi.lib().cyc_owcty(snap.context.handle, snap.handle, None if aw is None else ptr(aw),
+                               C.byref(cyc_), C.byref(w), C.byref(st)))
+    v = Verdict.cycle(w.value) if cyc_.value else Verdict.no_cycle()
+    return v, OwctyStats(st.outer_iterations, st.reach_ms, st.elim_ms, st.final_size)
+
+
 def shard_bounds(row_offsets: Sequence[int], parts: int) -> np.ndarray:
     """Edge-balanced contiguous row ranges (map_engine.cpp:35-43)."""
     off = np.ascontiguousarray(np.asarray(row_offsets, dtype=np.uint64))
@@ -649,5 +688,6 @@ __all__ = [
     "Orientation", "Outcome", "ResourceLimitError", "SccRestriction", "StepResult", "Verdict",
     "as_bitset", "build_snapshot", "check_graph", "default_context", "demote", "fixpoint",
     "init_vector", "launch_count", "propagate_step", "restrict_to_accepting_sccs", "run_map",
-    "run_map_detailed", "shard_bounds", "map_trace",
+    "run_map_detailed", "shard_bounds", "map_trace", "scc_verdict", "OracleVerdict", "OwctyStats",
+    "run_owcty",
 ]

@@ -14,6 +14,7 @@
 
 #include "../../include/cyc_gen.h"
 #include "map_run.cuh"
+#include "owcty.cuh"
 #include "scc.cuh"
 
 std::atomic<uint64_t> cyc::g_launches{0};
@@ -539,6 +540,45 @@ cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_wor
     if (iter_hash && rec) copy_out(iter_hash, (uint64_t*)gg->ws.hist.p, rec, ctx->s);
     if (iter_steps && rec) copy_out(iter_steps, (uint64_t*)gg->ws.hist.p + hcap, rec, ctx->s);
     CYC_CUDA(cudaStreamSynchronize(ctx->s));
+  });
+}
+
+cyc_status cyc_scc_verdict(cyc_ctx* ctx, const cyc_graph* g, int32_t* cycle, uint32_t* witness,
+                           uint32_t* cyclic_accepting, uint64_t* count) {
+  return guard([&] {
+    require(ctx && g, CYC_E_CONTRACT, "scc_verdict: null argument");
+    DevBuf list;
+    const uint32_t k = cyc::scc_cyclic_accepting(g->snap, g->gath, g->acc.as<uint64_t>(), ctx->s, list);
+    uint32_t first = cyc::kNone;
+    if (k) CYC_CUDA(cudaMemcpyAsync(&first, list.p, 4, cudaMemcpyDeviceToHost, ctx->s));
+    if (cyclic_accepting && k) copy_out(cyclic_accepting, list.as<uint32_t>(), k, ctx->s);
+    CYC_CUDA(cudaStreamSynchronize(ctx->s));
+    if (cycle) *cycle = k > 0;
+    if (witness) *witness = first;
+    if (count) *count = k;
+  });
+}
+
+cyc_status cyc_owcty(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words, int32_t* cycle,
+                     uint32_t* witness, cyc_owcty_stats* stats) {
+  return guard([&] {
+    require(ctx && g, CYC_E_CONTRACT, "run_owcty: null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    DevBuf accb;
+    const uint64_t* dacc = g->acc.as<uint64_t>();
+    if (acc_words) {
+      load_acc(acc_words, g->n(), accb, ctx->s);
+      dacc = accb.as<uint64_t>();
+    }
+    const cyc::OwctyResult r = cyc::run_owcty_device(g->gath, dacc, ctx->s);
+    if (cycle) *cycle = r.cycle;
+    if (witness) *witness = r.witness;
+    if (stats) {
+      stats->outer_iterations = r.outer_iterations;
+      stats->final_size = r.final_size;
+      stats->reach_ms = r.reach_ms;
+      stats->elim_ms = r.elim_ms;
+    }
   });
 }
 

@@ -240,6 +240,17 @@ __global__ void k_scc_apply(uint32_t n, const uint32_t* color, const uint32_t* r
   if (any) *flag = 1;
 }
 
+__global__ void k_keep_acc32(uint32_t n, const uint8_t* keep, const uint64_t* __restrict__ acc,
+                             uint32_t* k32) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    k32[v] = keep[v] && accb(acc, v);
+}
+
+__global__ void k_list_from_flags(uint32_t n, const uint32_t* flags, const uint32_t* pos, uint32_t* out) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (flags[v]) out[pos[v]] = v;
+}
+
 // ---- compaction of the kept subgraph
 __global__ void k_keep32(uint32_t n, const uint8_t* keep, uint32_t* k32) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
@@ -437,6 +448,29 @@ void scc_keep_mask(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc, 
     CYC_CUDA(cudaStreamSynchronize(s));
     if (!any) break;
   }
+}
+
+uint32_t scc_cyclic_accepting(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc,
+                              cudaStream_t s, DevBuf& list) {
+  const uint32_t n = snap.n;
+  DevBuf keep((size_t)n + 1, s), f32(((size_t)n + 1) * 4, s), pos(((size_t)n + 2) * 4, s), scratch;
+  scc_keep_mask(snap, gath, acc, s, keep.as<uint8_t>());
+  if (n) {
+    k_keep_acc32<<<grid_for(n, kT, 8), kT, 0, s>>>(n, keep.as<uint8_t>(), acc, f32.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
+  exclusive_scan(f32.as<uint32_t>(), pos.as<uint32_t>(), n, nullptr, s, scratch);
+  uint32_t k = 0;
+  CYC_CUDA(cudaMemcpyAsync(&k, pos.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  list.alloc(((size_t)k + 1) * 4, s);
+  if (n && k) {
+    k_list_from_flags<<<grid_for(n, kT, 8), kT, 0, s>>>(n, f32.as<uint32_t>(), pos.as<uint32_t>(),
+                                                        list.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
+  CYC_CUDA(cudaStreamSynchronize(s));
+  return k;
 }
 
 void restrict_graph(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc, cudaStream_t s,

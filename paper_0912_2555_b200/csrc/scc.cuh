@@ -14,4 +14,8 @@ void restrict_graph(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc,
 void scc_keep_mask(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc, cudaStream_t s,
                    uint8_t* keep);
 
+// Accepting vertices of cyclic SCCs, ascending (scc_verdict, oracle.cpp:32-98).
+uint32_t scc_cyclic_accepting(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc,
+                              cudaStream_t s, DevBuf& list);
+
 }  // namespace cyc

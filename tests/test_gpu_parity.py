@@ -326,3 +326,130 @@ def test_monotone_and_idempotent(eng, R):
     # idempotence at the fixpoint
     x2, ch = eng.propagate_step(s, fr.values, acc)
     assert not ch and np.array_equal(x2, fr.values)
+
+
+# ------------------------------------------------------- larger instances
+@pytest.mark.parametrize("scale", [14, 16])
+def test_rmat_parity(eng, R, scale):
+    """R-MAT (config 3 family) with real hubs: build (all row classes incl. the
+    tiled hub sort), gather index, run_map in both modes and all step kinds,
+    restriction."""
+    p = R.preset(3)
+    p.scale = scale
+    R.prepare(p)
+    n, e, accw = R.generate(p)
+    acc = eng.Bitset.from_words(accw, n)
+    s = snap_of(eng, n, e, acc)
+    g = R.build_snapshot(n, e, True)
+    assert np.array_equal(s.row_offsets, g.off) and np.array_equal(s.col_indices, g.col)
+    gat = R.transpose(g)
+    off, col = s.gather_index()
+    assert np.array_equal(off, gat.off) and np.array_equal(col, gat.col)
+    for early in (True, False):
+        ref = R.run_map(gat, accw, early)
+        for mode in MODES:
+            assert_same_run(eng.run_map_detailed(s, acc, eng.MapOptions(early_exit=early, mode=mode)), ref)
+    rg, racc, kept = R.restrict(g, accw)
+    r = eng.restrict_to_accepting_sccs(s)
+    assert np.array_equal(r.kept, kept)
+    assert np.array_equal(r.snapshot.row_offsets, rg.off) and np.array_equal(r.snapshot.col_indices, rg.col)
+
+
+def test_chain_family_closed_form(eng, R):
+    """Config 5 family (only the sink connector accepting, ring exits from
+    member S/2): one MAP iteration of L*(S/2+2)+7-ish dense-equivalent steps,
+    equal to the oracle in every step kind."""
+    p = R.preset(5)
+    p.L, p.W, p.S = 12, 16, 32
+    R.prepare(p)
+    n, e, accw = R.generate(p)
+    s = snap_of(eng, n, e, eng.Bitset.from_words(accw, n))
+    ref = R.run_map(R.transpose(R.build_snapshot(n, e, True)), accw, True)
+    assert ref.iterations == 1 and not ref.cycle
+    for mode in MODES:
+        assert_same_run(eng.run_map_detailed(s, eng.Bitset.from_words(accw, n), eng.MapOptions(mode=mode)), ref)
+
+
+def test_forward_orientation_with_restriction(eng, R):
+    """The explorer's map_orientation may be forward (explore.hpp:40): the
+    whole pipeline (build, restrict, run_map, witness back-mapping) in the
+    forward orientation."""
+    p = R.preset(1)
+    p.n = 1 << 14
+    R.prepare(p)
+    n, e, accw = R.generate(p)
+    acc = eng.Bitset.from_words(accw, n)
+    for restrict in (False, True):
+        v, st = eng.check_graph(n, e, acc, eng.Orientation.forward, restrict)
+        g = R.build_snapshot(n, e, False)
+        if restrict:
+            rg, racc, kept = R.restrict(g, accw)
+            ref = R.run_map(R.transpose(rg), racc, True)
+            wit = int(kept[ref.witness]) if ref.cycle else None
+        else:
+            ref = R.run_map(R.transpose(g), accw, True)
+            wit = ref.witness
+        assert (v.cycle_found(), v.witness, st.iterations, st.kernel_calls) == (
+            ref.cycle, wit, ref.iterations, ref.kernel_calls)
+
+
+def test_device_scc_verdict(eng, R, REF):
+    """scc_verdict on the device equals the reference's (oracle.cpp:32-98):
+    verdict, witness (smallest) and the sorted cyclic accepting vertices; and
+    agrees with MAP's verdict."""
+    rng = np.random.default_rng(404)
+    for t in range(12):
+        n = int(rng.integers(2, 3000))
+        e = random_graph(rng, n, int(n * rng.choice([1, 2])), hubs=t % 2)
+        acc = rng.random(n) < rng.choice([0.01, 0.1, 0.4])
+        s = snap_of(eng, n, e, acc)
+        ov = eng.scc_verdict(s)
+        keep = R.keep_mask(R.build_snapshot(n, e, True), acc)
+        want = np.flatnonzero(keep & acc).astype(np.uint32)
+        assert np.array_equal(ov.cyclic_accepting, want)
+        assert ov.verdict.cycle_found() == (len(want) > 0)
+        if len(want):
+            assert ov.verdict.witness == int(want[0])
+        rs = REF.snapshot(n, e, acc, True)
+        assert ov.verdict.cycle_found() == rs.scc_verdict()
+        v, _ = eng.run_map(s, s.accepting)
+        assert v.cycle_found() == ov.verdict.cycle_found()
+
+
+def test_device_owcty(eng, R, REF):
+    """run_owcty on the device (owcty.cpp:56-87) equals the reference's on
+    forward snapshots — verdict, witness, outer_iterations, final_size — and
+    the restatement's on transposed ones; the verdict equals MAP's."""
+    rng = np.random.default_rng(606)
+    for t in range(16):
+        n = int(rng.integers(2, 4000))
+        e = random_graph(rng, n, int(n * rng.choice([1, 2])), hubs=2 * (t % 2))
+        acc = rng.random(n) < rng.choice([0.01, 0.1, 0.4])
+        fwd = t % 4 != 3
+        s = snap_of(eng, n, e, acc, transposed=not fwd)
+        v, st = eng.run_owcty(s)
+        got = (v.cycle_found(), v.witness, st.outer_iterations, st.final_size)
+        want = R.run_owcty(R.build_snapshot(n, e, not fwd), acc)
+        assert got == want
+        if fwd:
+            assert got == REF.snapshot(n, e, acc, False).run_owcty()
+        mv, _ = eng.run_map(s, s.accepting)
+        assert mv.cycle_found() == v.cycle_found()
+    # explicit accepting override and the C2 family (L+1 layers, no cycle)
+    n = 50
+    e = np.array([[i, (i + 1) % n] for i in range(n)], np.uint32)
+    s = snap_of(eng, n, e, np.zeros(n, bool), transposed=False)
+    assert not eng.run_owcty(s)[0].cycle_found()
+    acc = np.zeros(n, bool)
+    acc[[7, 30]] = True
+    v, st = eng.run_owcty(s, acc)
+    assert (v.witness, st.final_size, st.outer_iterations) == (7, n, 1)
+    p = eng.preset(2)
+    p.L, p.W, p.S = 8, 64, 8
+    eng.prepare(p)
+    gn, ge, ga = R.generate(p)
+    s = eng.build_snapshot((gn, ge, eng.Bitset.from_words(ga, gn)), eng.Orientation.forward)
+    v, st = eng.run_owcty(s)
+    gacc = np.unpackbits(ga.view(np.uint8), bitorder="little")[:gn].astype(bool)
+    want = REF.snapshot(gn, ge, gacc, False).run_owcty()
+    assert (v.cycle_found(), v.witness, st.outer_iterations, st.final_size) == want

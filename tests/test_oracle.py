@@ -211,6 +211,26 @@ def test_random_differential_reference(R, REF):
             assert R.run_map(gat, acc, True).cycle == rs.scc_verdict()
 
 
+def test_owcty_restatement_vs_reference(R, REF):
+    # owcty.cpp:56-87 on forward snapshots (cycheck_main.cpp:98-106): verdict,
+    # witness, outer_iterations and final_size agree; verdict equals MAP's
+    rng = np.random.default_rng(1999)
+    for t in range(300):
+        n = int(rng.integers(1, 60))
+        m = int(rng.integers(0, 3 * n))
+        e = rng.integers(0, n, size=(m, 2)).astype(np.uint32)
+        acc = rng.random(n) < [0.05, 0.3][t % 2]
+        rs = REF.snapshot(n, e, acc, False)
+        g = R.build_snapshot(n, e, False)
+        got = R.run_owcty(g, acc)
+        assert got == rs.run_owcty()
+        assert got[0] == R.run_map(R.build_snapshot(n, e, True), acc, True).cycle
+    # SPEC.md:182-183 shapes: self loop, DAG
+    assert R.run_owcty(R.build_snapshot(1, [[0, 0]], False), [True])[:2] == (True, 0)
+    assert not R.run_owcty(R.build_snapshot(3, [[0, 1], [1, 2]], False), [True] * 3)[0]
+    assert R.run_owcty(R.build_snapshot(0, np.zeros((0, 2), np.uint32), False), [])[2] == 0
+
+
 def test_reference_step_worker_invariance(REF):
     # map_engine.hpp:46-49: bitwise identical for every worker count
     rng = np.random.default_rng(7)
