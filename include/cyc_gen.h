@@ -11,6 +11,10 @@
  *       layer, every ring member -> c_{l+1}); iterations = L+1,
  *       kernel_calls = (L+1)^2
  *   C3  R-MAT (Graph500 a,b,c = .57,.19,.19), seeded vertex permutation
+ *   C4  product state space: a token on a 2^g x 2^g torus (moves +x, +y)
+ *       times a 4-state Buechi automaton, planted accepting cycle in one
+ *       region; ids in BFS discovery order from the initial state (the
+ *       explorer's interner order, reference graph.cpp:223-230)
  *   C5  chain of small SCCs (C2 layout, only the sink connector accepting,
  *       ring exit from member S/2)
  * Vertex ids are VertexId = uint32_t (reference types.hpp:9); the log is the
@@ -38,7 +42,8 @@ extern "C" {
 enum cyc_gen_kind {
   CYC_GEN_UNIFORM = 1, /* C1 */
   CYC_GEN_LAYERED = 2, /* C2 (exit_all = 1, acc_all = 1), C5 (exit_all = 0, acc_all = 0) */
-  CYC_GEN_RMAT = 3     /* C3 */
+  CYC_GEN_RMAT = 3,    /* C3 */
+  CYC_GEN_PRODUCT = 4  /* C4 */
 };
 
 typedef struct cyc_gen_params {
@@ -58,6 +63,11 @@ typedef struct cyc_gen_params {
   uint32_t scale, edgefactor;
   uint64_t thr_a, thr_ab, thr_abc;
   uint64_t perm_mul1, perm_mul2; /* odd multipliers of the vertex permutation */
+  /* product (C4) */
+  uint32_t grid_bits;  /* torus side G = 2^grid_bits, n = 4 G^2 */
+  uint32_t region;     /* side of the square region R (clamped to G/2) */
+  uint32_t plant;      /* 1: reset move from R's far corner back to its near corner */
+  uint32_t reserved;
 } cyc_gen_params;
 
 CYC_HD uint64_t cyc_splitmix64(uint64_t x) {
@@ -102,7 +112,49 @@ CYC_HD uint32_t cyc_permute_bits(uint32_t v, uint32_t bits, uint64_t mul1, uint6
 CYC_HD uint32_t cyc_layer_stride(const cyc_gen_params* p) { return p->W * p->S + 1u; }
 CYC_HD uint32_t cyc_layer_exits(const cyc_gen_params* p) { return p->exit_all ? p->S : 1u; }
 
-/* Edge i of the log. */
+/* ---- C4 product graph ------------------------------------------------------
+ * System state (x, y) on a G x G torus; moves E: x+1, N: y+1 (mod G), plus,
+ * when planted, a reset move from R's far corner (rx+k-1, ry+k-1) to its near
+ * corner (rx, ry); R = [rx, rx+k) x [ry, ry+k), rx = ry = G/4.
+ * Automaton (q2 accepting), guards read the source state's label inR:
+ *   q0 -true-> q0, q0 -true-> q1, q1 -true-> q1, q1 -true-> q2,
+ *   q2 -inR-> q2, q2 -!inR-> q3, q3 -true-> q3.
+ * Product move (s,q) -> (s',q') for each system move s -> s' and each enabled
+ * automaton transition q -> q', in that nesting order. Accepting cycles exist
+ * only inside R x {q2}, and only through the planted reset. Every one of the
+ * 4 G^2 product states is reachable from (0,0,q0) (k < G).
+ * State key = q << 2g | y << g | x; vertex id = BFS discovery index. */
+CYC_HD uint32_t cyc_prod_side(const cyc_gen_params* p) { return 1u << p->grid_bits; }
+CYC_HD uint32_t cyc_prod_k(const cyc_gen_params* p) {
+  uint32_t half = cyc_prod_side(p) / 2u;
+  return p->region < 1u ? 1u : (p->region > half ? half : p->region);
+}
+/* Successors of `key` in canonical order into out[0..5]; returns the count. */
+CYC_HD uint32_t cyc_prod_succ(const cyc_gen_params* p, uint32_t key, uint32_t* out) {
+  const uint32_t g = p->grid_bits, G = 1u << g, mask = G - 1u;
+  const uint32_t x = key & mask, y = (key >> g) & mask, q = key >> (2u * g);
+  const uint32_t k = cyc_prod_k(p), r0 = G / 4u;
+  const int in_r = x >= r0 && x < r0 + k && y >= r0 && y < r0 + k;
+  uint32_t qs[2], nq = 0;
+  if (q == 0u) { qs[0] = 0u; qs[1] = 1u; nq = 2u; }
+  else if (q == 1u) { qs[0] = 1u; qs[1] = 2u; nq = 2u; }
+  else if (q == 2u) { qs[0] = in_r ? 2u : 3u; nq = 1u; }
+  else { qs[0] = 3u; nq = 1u; }
+  uint32_t mv[3], nm = 0;
+  mv[nm++] = (y << g) | ((x + 1u) & mask);
+  mv[nm++] = (((y + 1u) & mask) << g) | x;
+  if (p->plant && x == r0 + k - 1u && y == r0 + k - 1u) mv[nm++] = (r0 << g) | r0;
+  uint32_t c = 0;
+  for (uint32_t a = 0; a < nm; ++a)
+    for (uint32_t b = 0; b < nq; ++b) out[c++] = (qs[b] << (2u * g)) | mv[a];
+  return c;
+}
+CYC_HD int cyc_prod_accepting_key(const cyc_gen_params* p, uint32_t key) {
+  return (key >> (2u * p->grid_bits)) == 2u;
+}
+
+/* Edge i of the log (index-addressable kinds; C4 needs the BFS order, see
+ * cyc_prod_generate_host and the library's device generator). */
 CYC_HD void cyc_gen_edge(const cyc_gen_params* p, uint64_t i, uint32_t* src, uint32_t* dst) {
   if (p->kind == CYC_GEN_UNIFORM) {
     *src = (uint32_t)(i / p->deg);
@@ -173,6 +225,13 @@ CYC_HD int cyc_gen_init(cyc_gen_params* p) {
     p->m = (uint64_t)p->L * p->W * (1ull + p->S + cyc_layer_exits(p));
     return 0;
   }
+  if (p->kind == CYC_GEN_PRODUCT) {
+    if (p->grid_bits < 2 || p->grid_bits > 14) return -1;
+    const uint64_t G = 1ull << p->grid_bits;
+    p->n = (uint32_t)(4ull * G * G);
+    p->m = 12ull * G * G + (p->plant ? 6ull : 0ull);
+    return 0;
+  }
   if (p->kind == CYC_GEN_RMAT) {
     if (p->scale == 0 || p->scale > 30) return -1;
     p->n = 1u << p->scale;
@@ -209,6 +268,9 @@ CYC_HD int cyc_gen_config(cyc_gen_params* p, int index) {
     case 3:
       p->kind = CYC_GEN_RMAT; p->scale = 26; p->edgefactor = 16; p->acc_thr = cyc_bp_threshold(100);
       break;
+    case 4:
+      p->kind = CYC_GEN_PRODUCT; p->grid_bits = 13; p->region = 64; p->plant = 1;
+      break;
     case 5:
       p->kind = CYC_GEN_LAYERED; p->L = 64; p->W = 512; p->S = 512; p->exit_all = 0; p->acc_all = 0;
       break;
@@ -217,6 +279,44 @@ CYC_HD int cyc_gen_config(cyc_gen_params* p, int index) {
   }
   return cyc_gen_init(p);
 }
+
+/* Host generation of C4 (sequential BFS queue = the interner's discovery
+ * order): key_of_id / id_of_key are caller arrays of p->n entries; edges
+ * (2 p->m) and acc_words (ceil(n/64)) may be NULL. Returns 0, or -1 if some
+ * state is unreachable. */
+#ifndef __CUDA_ARCH__
+static inline int cyc_prod_generate_host(const cyc_gen_params* p, uint32_t* key_of_id,
+                                         uint32_t* id_of_key, uint32_t* edges, uint64_t* acc_words) {
+  const uint32_t n = p->n;
+  uint32_t succ[6];
+  uint64_t tail = 1, e = 0;
+  for (uint32_t k = 0; k < n; ++k) id_of_key[k] = 0xFFFFFFFFu;
+  key_of_id[0] = 0u;
+  id_of_key[0] = 0u;
+  for (uint64_t head = 0; head < tail; ++head) {
+    const uint32_t c = cyc_prod_succ(p, key_of_id[head], succ);
+    for (uint32_t j = 0; j < c; ++j)
+      if (id_of_key[succ[j]] == 0xFFFFFFFFu) {
+        id_of_key[succ[j]] = (uint32_t)tail;
+        key_of_id[tail++] = succ[j];
+      }
+  }
+  if (tail != n) return -1;
+  for (uint32_t v = 0; v < n; ++v) {
+    const uint32_t c = cyc_prod_succ(p, key_of_id[v], succ);
+    for (uint32_t j = 0; j < c && edges; ++j, ++e) {
+      edges[2 * e] = v;
+      edges[2 * e + 1] = id_of_key[succ[j]];
+    }
+  }
+  if (acc_words) {
+    for (uint64_t w = 0; w < ((uint64_t)n + 63u) / 64u; ++w) acc_words[w] = 0;
+    for (uint32_t v = 0; v < n; ++v)
+      if (cyc_prod_accepting_key(p, key_of_id[v])) acc_words[v >> 6] |= 1ull << (v & 63u);
+  }
+  return 0;
+}
+#endif
 
 #ifdef __cplusplus
 }

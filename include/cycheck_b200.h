@@ -192,14 +192,26 @@ cyc_status cyc_memcpy(cyc_ctx* ctx, void* dst, const void* src, size_t bytes);
 cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes);
 
 /* ---- multi-GPU row sharding (one process per GPU) ------------------------ */
+/* Device-side state of one sharded fixpoint (int64[4], device memory):
+ * [0] done, [1] steps taken, [2] witness (UINT32_MAX = none), [3] early_exit.
+ * Every rank holds an identical copy; all updates happen on the device from
+ * all-reduced records, so ranks stay in lockstep without host syncs. */
 /* One Jacobi step (MaxPropagation::step) restricted to rows [lo, hi) of the
  * gather index: out[v - lo] for v in the range, from the full replicated
- * vector x (n codes, device) and accepting words (device). flags (device,
- * 2 u32) receive {changed, min self-witness or UINT32_MAX}; asynchronous on
- * the context's stream (no host sync), for use between collectives. */
+ * vector x (n codes, device) and accepting words (device). rec (device
+ * int64[2]) receives {changed, UINT32_MAX - min self-witness} (MAX-reducible;
+ * 0 = no witness). A no-op when state[0] (done) is set. Asynchronous on the
+ * context's stream (no host sync), for use between collectives. */
 cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi,
                           const uint32_t* x, const uint64_t* acc_words, uint32_t* out,
-                          uint32_t* flags);
+                          int64_t* rec, const int64_t* state);
+/* After the all-gather of the padded slices (x_pad: world * maxrows codes)
+ * and the MAX all-reduce of rec: x[bounds[r] + i] = x_pad[r*maxrows + i]
+ * (bounds: device u32[world+1]) and, unless done, state advances: steps++,
+ * and the fixpoint ends (done, witness) on a witness with early_exit or on
+ * no change (map_engine.cpp:94-121). Asynchronous. */
+cyc_status cyc_shard_post(cyc_ctx* ctx, const int64_t* rec, int64_t* state, const uint32_t* x_pad,
+                          const uint32_t* bounds, int world, uint32_t maxrows, uint32_t* x);
 /* used-bitmap demotion on a full replicated vector, entirely on device:
  * remaining = F \ D (words, device), counts[0] = |D|, counts[1] = |F'|
  * (device u64[2]); asynchronous. */

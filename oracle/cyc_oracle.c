@@ -296,6 +296,14 @@ void cyo_run_map(const cyo_csr* gather, const uint64_t* acc, int early_exit, cyo
 
 int cyo_generate(const void* gen_params, uint32_t* edges, uint64_t* acc_words) {
   const cyc_gen_params* p = (const cyc_gen_params*)gen_params;
+  if (p->kind == CYC_GEN_PRODUCT) {
+    uint32_t* a = (uint32_t*)malloc(((size_t)p->n + 1) * 4);
+    uint32_t* b = (uint32_t*)malloc(((size_t)p->n + 1) * 4);
+    int rc = a && b ? cyc_prod_generate_host(p, a, b, edges, acc_words) : -1;
+    free(a);
+    free(b);
+    return rc;
+  }
   for (uint64_t i = 0; i < p->m; ++i) cyc_gen_edge(p, i, &edges[2 * i], &edges[2 * i + 1]);
   size_t words = ((size_t)p->n + 63) / 64;
   memset(acc_words, 0, words * sizeof(uint64_t));

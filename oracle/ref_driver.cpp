@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
@@ -90,6 +91,29 @@ int ref_snapshot_new(const uint32_t* edges, uint64_t m, uint32_t n, const uint64
   REF_CATCH
 }
 
+}  // extern "C"
+
+// Appends a generated configuration to the reference's own EdgeLog.
+static void fill_log(const cyc_gen_params* p, EdgeLog& log) {
+  if (p->kind == CYC_GEN_PRODUCT) {  // BFS-ordered product graph (cyc_gen.h)
+    std::vector<uint32_t> a(p->n), b(p->n), e(2 * p->m);
+    std::vector<uint64_t> w((p->n + 63) / 64);
+    if (cyc_prod_generate_host(p, a.data(), b.data(), e.data(), w.data()) != 0)
+      throw std::runtime_error("product generator: unreachable states");
+    for (uint32_t v = 0; v < p->n; ++v) log.add_vertex((w[v >> 6] >> (v & 63)) & 1);
+    for (uint64_t i = 0; i < p->m; ++i) log.append_edge(e[2 * i], e[2 * i + 1]);
+    return;
+  }
+  for (uint32_t v = 0; v < p->n; ++v) log.add_vertex(cyc_gen_accepting(p, v) != 0);
+  for (uint64_t i = 0; i < p->m; ++i) {
+    uint32_t s, d;
+    cyc_gen_edge(p, i, &s, &d);
+    log.append_edge(s, d);
+  }
+}
+
+extern "C" {
+
 int ref_snapshot_gen(const void* params, int transposed, void** out) {
   REF_TRY
   const auto* p = static_cast<const cyc_gen_params*>(params);
@@ -97,12 +121,7 @@ int ref_snapshot_gen(const void* params, int transposed, void** out) {
   lim.max_vertices = p->n > 0 ? p->n : 1;
   lim.max_edges = p->m > 0 ? p->m : 1;
   EdgeLog log(lim);
-  for (uint32_t v = 0; v < p->n; ++v) log.add_vertex(cyc_gen_accepting(p, v) != 0);
-  for (uint64_t i = 0; i < p->m; ++i) {
-    uint32_t s, d;
-    cyc_gen_edge(p, i, &s, &d);
-    log.append_edge(s, d);
-  }
+  fill_log(p, log);
   auto* s = new Snap;
   s->snap = build_snapshot(log, transposed ? Orientation::transposed : Orientation::forward);
   *out = s;
@@ -309,12 +328,7 @@ int ref_time_build(const void* params, int transposed, double* seconds) {
   lim.max_vertices = p->n > 0 ? p->n : 1;
   lim.max_edges = p->m > 0 ? p->m : 1;
   EdgeLog log(lim);
-  for (uint32_t v = 0; v < p->n; ++v) log.add_vertex(cyc_gen_accepting(p, v) != 0);
-  for (uint64_t i = 0; i < p->m; ++i) {
-    uint32_t s, d;
-    cyc_gen_edge(p, i, &s, &d);
-    log.append_edge(s, d);
-  }
+  fill_log(p, log);
   auto t0 = std::chrono::steady_clock::now();
   CsrSnapshot snap = build_snapshot(log, transposed ? Orientation::transposed : Orientation::forward);
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -98,6 +98,10 @@ class GenParams(C.Structure):
         ("thr_abc", C.c_uint64),
         ("perm_mul1", C.c_uint64),
         ("perm_mul2", C.c_uint64),
+        ("grid_bits", C.c_uint32),
+        ("region", C.c_uint32),
+        ("plant", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -140,7 +144,8 @@ _SIGS = {
     "cyc_flush_l2": (C.c_int, [_P, C.c_size_t]),
     "cyc_shard_bounds": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
     "cyc_map_trace": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
-    "cyc_shard_step": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, _P, _P, _P, _P]),
+    "cyc_shard_step": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, _P, _P, _P, _P, _P]),
+    "cyc_shard_post": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_uint32, _P]),
     "cyc_shard_demote": (C.c_int, [_P, _P, C.c_uint32, _P, _P, _P]),
 }
 

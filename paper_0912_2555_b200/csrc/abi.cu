@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/cyc_gen.h"
+#include "gen.cuh"
 #include "map_run.cuh"
 #include "owcty.cuh"
 #include "scc.cuh"
@@ -306,7 +307,9 @@ void* cyc_ctx_stream(cyc_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
 cyc_status cyc_ctx_set_stream(cyc_ctx* ctx, void* stream, int external) {
   return guard([&] {
     require(ctx, CYC_E_CONTRACT, "null ctx");
-    CYC_CUDA(cudaStreamSynchronize(ctx->s));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CYC_CUDA(cudaStreamIsCapturing(ctx->s, &cs));
+    if (cs == cudaStreamCaptureStatusNone) CYC_CUDA(cudaStreamSynchronize(ctx->s));
     ctx->s = external ? static_cast<cudaStream_t>(stream) : ctx->own;
   });
 }
@@ -665,10 +668,14 @@ cyc_status cyc_gen_fill(cyc_ctx* ctx, const void* gen_params, uint32_t* edges,
       ta.alloc(nw * 8 + 8, s);
       da = ta.as<uint64_t>();
     }
-    cyc_gen_params q = p;
-    if (!edges) q.m = 0;
-    k_gen<<<cyc::grid_for(p.m > nw ? p.m : nw, 256, 16), 256, 0, s>>>(q, de, da, nw);
-    CYC_LAUNCHED();
+    if (p.kind == CYC_GEN_PRODUCT) {
+      cyc::gen_product_device(p, edges ? de : nullptr, acc_words ? da : nullptr, s);
+    } else {
+      cyc_gen_params q = p;
+      if (!edges) q.m = 0;
+      k_gen<<<cyc::grid_for(p.m > nw ? p.m : nw, 256, 16), 256, 0, s>>>(q, de, da, nw);
+      CYC_LAUNCHED();
+    }
     if (edges && !dev_e) copy_out(edges, de, p.m * 2, s);
     if (acc_words && !dev_a) copy_out(acc_words, da, nw, s);
     CYC_CUDA(cudaStreamSynchronize(s));
@@ -722,16 +729,28 @@ cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes) {
 }
 
 cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi,
-                          const uint32_t* x, const uint64_t* acc_words, uint32_t* out,
-                          uint32_t* flags) {
+                          const uint32_t* x, const uint64_t* acc_words, uint32_t* out, int64_t* rec,
+                          const int64_t* state) {
   return guard([&] {
-    require(ctx && g && x && acc_words && flags && (out || hi <= lo), CYC_E_CONTRACT,
+    require(ctx && g && x && acc_words && rec && (out || hi <= lo), CYC_E_CONTRACT,
             "shard_step: null argument");
     require(lo <= hi && hi <= g->n(), CYC_E_CONTRACT, "shard_step: bad row range");
-    require(is_device_ptr(x) && is_device_ptr(acc_words) && is_device_ptr(flags), CYC_E_CONTRACT,
-            "shard_step: vectors must be device memory");
-    cyc::launch_step_range(g->gath, lo, hi, x, reinterpret_cast<const uint32_t*>(acc_words), out, flags,
+    require(is_device_ptr(x) && is_device_ptr(acc_words) && is_device_ptr(rec) &&
+                (!state || is_device_ptr(state)),
+            CYC_E_CONTRACT, "shard_step: vectors must be device memory");
+    cyc::launch_step_range(g->gath, lo, hi, x, reinterpret_cast<const uint32_t*>(acc_words), out,
+                           reinterpret_cast<long long*>(rec), reinterpret_cast<const long long*>(state),
                            ctx->s);
+  });
+}
+
+cyc_status cyc_shard_post(cyc_ctx* ctx, const int64_t* rec, int64_t* state, const uint32_t* x_pad,
+                          const uint32_t* bounds, int world, uint32_t maxrows, uint32_t* x) {
+  return guard([&] {
+    require(ctx && rec && state && bounds && world >= 1 && (x_pad || !maxrows) && (x || !maxrows),
+            CYC_E_CONTRACT, "shard_post: bad argument");
+    cyc::launch_shard_post(reinterpret_cast<const long long*>(rec), reinterpret_cast<long long*>(state),
+                           x_pad, bounds, world, maxrows, x, ctx->s);
   });
 }
 

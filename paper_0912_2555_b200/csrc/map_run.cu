@@ -878,27 +878,136 @@ __global__ void k_step_pull(uint32_t n, const uint32_t* __restrict__ goff,
   if (wit != kNone) atomicMin(flags + 1, wit);
 }
 
-__global__ void k_step_range(uint32_t lo, uint32_t hi, const uint32_t* __restrict__ goff,
+// Sharded dense step over rows [lo, hi). Rows longer than `heavy` start from
+// x[v] here and are finished by k_step_range_chunks (one warp per 256-edge
+// chunk, atomicMax into out) and k_step_range_heavy (their flags).
+__device__ __forceinline__ uint32_t cand_of(uint32_t u, const uint32_t* __restrict__ x,
+                                            const uint32_t* __restrict__ accw) {
+  uint32_t c = x[u];
+  if (((accw[u >> 5] >> (u & 31u)) & 1u) && u + 1u > c) c = u + 1u;
+  return c;
+}
+
+__device__ __forceinline__ void shard_flags(bool ch, uint32_t wit, unsigned long long* rec) {
+  wit = __reduce_min_sync(__activemask(), wit);
+  if (__any_sync(__activemask(), ch) && lane_id() == 0) atomicMax(rec, 1ull);
+  if (wit != kNone && lane_id() == 0) atomicMax(rec + 1, (unsigned long long)(kNone - wit));
+}
+
+__global__ void k_step_range(uint32_t lo, uint32_t hi, uint32_t heavy, const uint32_t* __restrict__ goff,
                              const uint32_t* __restrict__ gcol, const uint32_t* __restrict__ x,
                              const uint32_t* __restrict__ accw, uint32_t* __restrict__ out,
-                             uint32_t* __restrict__ flags) {
+                             unsigned long long* __restrict__ rec, const long long* __restrict__ state) {
+  if (state && state[0]) return;  // fixpoint already decided on every rank
   const uint32_t stride = gridDim.x * blockDim.x;
   bool ch = false;
   uint32_t wit = kNone;
   for (uint32_t v = lo + blockIdx.x * blockDim.x + threadIdx.x; v < hi; v += stride) {
+    const uint32_t b = goff[v], e = goff[v + 1];
     uint32_t best = x[v];
-    for (uint32_t i = goff[v]; i < goff[v + 1]; ++i) {
-      const uint32_t u = gcol[i];
-      uint32_t c = x[u];
-      if (((accw[u >> 5] >> (u & 31u)) & 1u) && u + 1u > c) c = u + 1u;
-      best = max(best, c);
+    if (e - b > heavy) {
+      out[v - lo] = best;
+      continue;
     }
+    for (uint32_t i = b; i < e; ++i) best = max(best, cand_of(gcol[i], x, accw));
     out[v - lo] = best;
     ch |= best != x[v];
     if (best == v + 1u && ((accw[v >> 5] >> (v & 31u)) & 1u)) wit = min(wit, v);
   }
-  if (__any_sync(__activemask(), ch) && lane_id() == 0) flags[0] = 1u;
-  if (wit != kNone) atomicMin(flags + 1, wit);
+  shard_flags(ch, wit, rec);
+}
+
+// Same step reading each row's first K columns from the column-major HYB slab
+// (coalesced across lanes; sentinel entries >= n are NIL); rows flagged in
+// ovf continue from column K in the CSR, heavy ones are left to the chunks.
+template <int K>
+__global__ void k_step_range_ell(uint32_t lo, uint32_t hi, uint32_t n, uint32_t np, uint32_t heavy,
+                                 const uint32_t* __restrict__ ell, const uint32_t* __restrict__ ovf,
+                                 const uint32_t* __restrict__ goff, const uint32_t* __restrict__ gcol,
+                                 const uint32_t* __restrict__ x, const uint32_t* __restrict__ accw,
+                                 uint32_t* __restrict__ out, unsigned long long* __restrict__ rec,
+                                 const long long* __restrict__ state) {
+  if (state && state[0]) return;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  bool ch = false;
+  uint32_t wit = kNone;
+  for (uint32_t v = lo + blockIdx.x * blockDim.x + threadIdx.x; v < hi; v += stride) {
+    const uint32_t own = x[v];
+    uint32_t u[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) u[j] = __ldg(ell + (size_t)j * np + v);
+    uint32_t best = own;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (u[j] < n) best = max(best, cand_of(u[j], x, accw));
+    if ((__ldg(ovf + (v >> 5)) >> (v & 31u)) & 1u) {
+      const uint32_t b = goff[v], e = goff[v + 1];
+      if (e - b > heavy) {
+        out[v - lo] = own;
+        continue;
+      }
+      for (uint32_t i = b + K; i < e; ++i) best = max(best, cand_of(gcol[i], x, accw));
+    }
+    out[v - lo] = best;
+    ch |= best != own;
+    if (best == v + 1u && ((accw[v >> 5] >> (v & 31u)) & 1u)) wit = min(wit, v);
+  }
+  shard_flags(ch, wit, rec);
+}
+
+__global__ void k_step_range_chunks(const uint4* __restrict__ chunks, uint32_t nch, uint32_t lo, uint32_t hi,
+                                    const uint32_t* __restrict__ gcol, const uint32_t* __restrict__ x,
+                                    const uint32_t* __restrict__ accw, uint32_t* __restrict__ out,
+                                    const long long* __restrict__ state) {
+  if (state && state[0]) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = gw; k < nch; k += nw) {
+    const uint4 ch = chunks[k];
+    if (ch.x < lo || ch.x >= hi) continue;
+    uint32_t best = 0;
+    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) best = max(best, cand_of(gcol[i], x, accw));
+    best = __reduce_max_sync(kFull, best);
+    if (lane == 0 && best > x[ch.x]) atomicMax(out + (ch.x - lo), best);
+  }
+}
+
+__global__ void k_step_range_heavy(const uint4* __restrict__ chunks, uint32_t nch, uint32_t lo, uint32_t hi,
+                                   const uint32_t* __restrict__ goff, const uint32_t* __restrict__ x,
+                                   const uint32_t* __restrict__ accw, const uint32_t* __restrict__ out,
+                                   unsigned long long* __restrict__ rec, const long long* __restrict__ state) {
+  if (state && state[0]) return;
+  bool chg = false;
+  uint32_t wit = kNone;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nch; k += gridDim.x * blockDim.x) {
+    const uint4 ch = chunks[k];
+    const uint32_t v = ch.x;
+    if (v < lo || v >= hi || ch.y != goff[v]) continue;  // first chunk of an in-range row
+    const uint32_t best = out[v - lo];
+    chg |= best != x[v];
+    if (best == v + 1u && ((accw[v >> 5] >> (v & 31u)) & 1u)) wit = min(wit, v);
+  }
+  shard_flags(chg, wit, rec);
+}
+
+__global__ void k_shard_post(const long long* __restrict__ rec, long long* state,
+                             const uint32_t* __restrict__ x_pad, const uint32_t* __restrict__ bounds,
+                             int world, uint32_t maxrows, uint32_t* __restrict__ x) {
+  const uint64_t total = (uint64_t)world * maxrows;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(e / maxrows), i = (uint32_t)(e % maxrows);
+    const uint32_t lo = bounds[r];
+    if (lo + i < bounds[r + 1]) x[lo + i] = x_pad[e];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !state[0]) {
+    const uint32_t wit = kNone - (uint32_t)rec[1];
+    state[1] += 1;
+    if ((state[3] && wit != kNone) || !rec[0]) {
+      state[0] = 1;
+      state[2] = wit;
+    }
+  }
 }
 
 __global__ void k_demote_count(uint32_t nwords, const uint32_t* __restrict__ acc,
@@ -1089,12 +1198,39 @@ void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* acc
 }
 
 void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint32_t* x,
-                       const uint32_t* accw, uint32_t* out, uint32_t* flags, cudaStream_t s) {
-  uint32_t init[2] = {0u, kNone};
-  CYC_CUDA(cudaMemcpyAsync(flags, init, 8, cudaMemcpyHostToDevice, s));
+                       const uint32_t* accw, uint32_t* out, long long* rec, const long long* state,
+                       cudaStream_t s) {
+  CYC_CUDA(cudaMemsetAsync(rec, 0, 16, s));
   if (hi <= lo) return;
-  k_step_range<<<grid_for(hi - lo, 256, 8), 256, 0, s>>>(lo, hi, gath.o(), gath.c(), x, accw, out,
-                                                         flags);
+  auto* r = reinterpret_cast<unsigned long long*>(rec);
+  const uint32_t heavy = gath.n_heavy_chunks ? gath.heavy_deg : kNone;
+  const uint32_t g = grid_for(hi - lo, 256, 8);
+  const uint32_t n = gath.n, np = gath.ell_n;
+  const uint32_t* ell = gath.ell.as<uint32_t>();
+  const uint32_t* ovf = gath.ovf.as<uint32_t>();
+  switch (gath.ell_k) {
+    case 1: k_step_range_ell<1><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
+    case 2: k_step_range_ell<2><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
+    case 4: k_step_range_ell<4><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
+    case 8: k_step_range_ell<8><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
+    default: k_step_range<<<g, 256, 0, s>>>(lo, hi, heavy, gath.o(), gath.c(), x, accw, out, r, state); break;
+  }
+  CYC_LAUNCHED();
+  if (gath.n_heavy_chunks) {
+    const uint32_t nch = gath.n_heavy_chunks;
+    k_step_range_chunks<<<grid_for((uint64_t)nch * 32, 256, 8), 256, 0, s>>>(
+        gath.heavy.as<uint4>(), nch, lo, hi, gath.c(), x, accw, out, state);
+    CYC_LAUNCHED();
+    k_step_range_heavy<<<grid_for(nch, 256, 4), 256, 0, s>>>(gath.heavy.as<uint4>(), nch, lo, hi, gath.o(), x,
+                                                             accw, out, r, state);
+    CYC_LAUNCHED();
+  }
+}
+
+void launch_shard_post(const long long* rec, long long* state, const uint32_t* x_pad,
+                       const uint32_t* bounds, int world, uint32_t maxrows, uint32_t* x, cudaStream_t s) {
+  k_shard_post<<<grid_for((uint64_t)world * maxrows + 1, 256, 8), 256, 0, s>>>(rec, state, x_pad, bounds,
+                                                                               world, maxrows, x);
   CYC_LAUNCHED();
 }
 

@@ -101,9 +101,14 @@ void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream
 void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* accw, uint32_t* out,
                       uint32_t* flags, cudaStream_t s);
 
-// Dense step over rows [lo, hi) only (sharded runs); flags as launch_step_pull.
+// Dense step over rows [lo, hi) only (sharded runs): rec = {changed,
+// UINT32_MAX - min witness} as int64 (MAX-reducible); no-op when state[0].
 void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint32_t* x,
-                       const uint32_t* accw, uint32_t* out, uint32_t* flags, cudaStream_t s);
+                       const uint32_t* accw, uint32_t* out, long long* rec, const long long* state,
+                       cudaStream_t s);
+// Unpads the gathered slices into x and advances the sharded fixpoint state.
+void launch_shard_post(const long long* rec, long long* state, const uint32_t* x_pad,
+                       const uint32_t* bounds, int world, uint32_t maxrows, uint32_t* x, cudaStream_t s);
 // Device-only demotion for sharded runs: counts[0] = |D|, counts[1] = |F'|.
 void launch_demote_async(const uint32_t* x, uint32_t n, const uint32_t* accw, uint32_t* remaining,
                          unsigned long long* counts, uint32_t* used_scratch, cudaStream_t s);

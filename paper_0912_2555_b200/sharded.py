@@ -9,10 +9,15 @@ final vector bit for bit.
 Per Jacobi step every rank computes the new values of its rows from the
 replicated vector, then
   * all-gather of the row slices (equal-size padded slices), and
-  * all-reduce(MAX) of {changed, -min self-witness},
-so all ranks take the same stop / early-exit decision at the same step
-(kernel_calls identical to one device). Demotion (map_engine.cpp:123-137) is
-replicated on every rank from the gathered vector — no collective needed.
+  * all-reduce(MAX) of the record {changed, UINT32_MAX - min self-witness},
+and a post step on the device unpads the slices into the vector and advances
+a device-resident fixpoint state {done, steps, witness, early_exit}. All
+ranks see the same reduced record, so they take the same stop / early-exit
+decision at the same step (kernel_calls identical to one device) without any
+host round trip: the host enqueues a batch of steps and reads the state once
+per batch; steps enqueued after the decision are no-ops on every rank.
+Demotion (map_engine.cpp:123-137) is replicated on every rank from the
+gathered vector — no collective needed.
 
 The protocol is backend-agnostic: the product runs `CudaShardBackend` (the
 sm_100a step kernel through the C ABI, torch.distributed NCCL for the
@@ -46,7 +51,9 @@ def plan(gather_offsets, world: int) -> np.ndarray:
 
 
 class CudaShardBackend:
-    """Dense step over this rank's rows with the engine's kernel (device only)."""
+    """Row-range step and post kernels through the C ABI (device only); the
+    library is ordered on torch's current stream so NCCL collectives and
+    kernels interleave without host synchronisation."""
 
     def __init__(self, snap: CsrSnapshot, device):
         import torch
@@ -55,26 +62,38 @@ class CudaShardBackend:
         self.snap = snap
         self.n = snap.n
         self.device = device
-        self.flags = torch.zeros(2, dtype=torch.int32, device=device)
         self.counts = torch.zeros(2, dtype=torch.int64, device=device)
-        stream = torch.cuda.current_stream(device).cuda_stream
-        _abi.check(_abi.lib().cyc_ctx_set_stream(snap.context.handle, C.c_void_p(stream), 1))
+        self.bounds = None
+        self.graphs = True  # step batches may be captured into CUDA graphs
+        self.bind()
+
+    def bind(self):
+        """Orders the library on torch's current stream (also inside a capture)."""
+        stream = self.torch.cuda.current_stream(self.device).cuda_stream
+        _abi.check(_abi.lib().cyc_ctx_set_stream(self.snap.context.handle, C.c_void_p(stream), 1))
 
     def release(self):
         """Back to the context's own stream."""
         _abi.check(_abi.lib().cyc_ctx_set_stream(self.snap.context.handle, None, 0))
 
-    def zeros(self, k: int):
-        return self.torch.zeros(max(k, 1), dtype=self.torch.int32, device=self.device)
+    def zeros(self, k: int, dtype=None):
+        return self.torch.zeros(max(k, 1), dtype=dtype or self.torch.int32, device=self.device)
 
     def acc_tensor(self, words: np.ndarray):
         return self.torch.from_numpy(words.view(np.int64).copy()).to(self.device)
 
-    def step(self, x, acc, lo: int, hi: int, out):
+    def prepare(self, bounds):
+        self.bounds = self.torch.tensor(np.asarray(bounds, np.int64).astype(np.int32), device=self.device)
+
+    def step(self, x, acc, lo: int, hi: int, out, rec, state=None):
         _abi.check(_abi.lib().cyc_shard_step(self.snap.context.handle, self.snap.handle, lo, hi,
-                                             _abi.ptr(x), _abi.ptr(acc), _abi.ptr(out),
-                                             _abi.ptr(self.flags)))
-        return self.flags
+                                             _abi.ptr(x), _abi.ptr(acc), _abi.ptr(out), _abi.ptr(rec),
+                                             None if state is None else _abi.ptr(state)))
+
+    def post(self, rec, state, x_pad, world: int, maxrows: int, x):
+        _abi.check(_abi.lib().cyc_shard_post(self.snap.context.handle, _abi.ptr(rec), _abi.ptr(state),
+                                             _abi.ptr(x_pad), _abi.ptr(self.bounds), world, maxrows,
+                                             _abi.ptr(x)))
 
     def demote(self, x, acc):
         rem = self.torch.zeros_like(acc)
@@ -84,53 +103,118 @@ class CudaShardBackend:
         return rem, d, f
 
 
+class _StepGraphs:
+    """CUDA graphs of 2^j consecutive protocol steps (kernels + NCCL
+    collectives), captured lazily; run(k) replays exactly k steps."""
+
+    def __init__(self, backend, one_step):
+        self.be = backend
+        self.one = one_step
+        self.g = {}
+
+    def _get(self, b: int):
+        if b not in self.g:
+            torch = self.be.torch
+            g = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize(self.be.device)
+            with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                self.be.bind()
+                for _ in range(b):
+                    self.one()
+            self.be.bind()
+            self.g[b] = g
+        return self.g[b]
+
+    def run(self, k: int) -> None:
+        b = 1
+        while k:
+            if k & 1:
+                self._get(b).replay()
+            k >>= 1
+            b <<= 1
+
+
+class _Runner:
+    """Persistent buffers (and captured step graphs) of one rank's shard."""
+
+    def __init__(self, backend, dist, rank, world, bounds, group, graphs):
+        torch = backend.torch
+        self.be, self.dist, self.group = backend, dist, group
+        self.world = world
+        self.lo, self.hi = bounds[rank], bounds[rank + 1]
+        self.maxrows = max(max(bounds[r + 1] - bounds[r] for r in range(world)), 1)
+        backend.prepare(bounds)
+        self.x = backend.zeros(backend.n)
+        self.send = backend.zeros(self.maxrows)
+        self.x_pad = backend.zeros(world * self.maxrows)
+        self.rec = backend.zeros(2, torch.int64)
+        self.state = backend.zeros(4, torch.int64)
+        self.acc = backend.zeros((backend.n + 63) // 64, torch.int64)
+        self.graphs = _StepGraphs(backend, self.one_step) if graphs else None
+
+    def one_step(self):
+        be, d = self.be, self.dist
+        be.step(self.x, self.acc, self.lo, self.hi, self.send, self.rec, self.state)
+        d.all_gather_into_tensor(self.x_pad, self.send[: self.maxrows], group=self.group)
+        d.all_reduce(self.rec, op=d.ReduceOp.MAX, group=self.group)
+        be.post(self.rec, self.state, self.x_pad, self.world, self.maxrows, self.x)
+
+    def steps(self, k: int):
+        if self.graphs is not None:
+            self.graphs.run(k)
+        else:
+            for _ in range(k):
+                self.one_step()
+
+
 def run_map_sharded(backend, dist, rank: int, world: int, bounds, acc_words: np.ndarray,
-                    early_exit: bool = True, group=None) -> ShardedResult:
-    """run_map (map_engine.cpp:139-162) with rows sharded over `world` ranks."""
-    torch = backend.torch
+                    early_exit: bool = True, group=None, max_batch: int = 64,
+                    graphs: Optional[bool] = None) -> ShardedResult:
+    """run_map (map_engine.cpp:139-162) with rows sharded over `world` ranks.
+
+    Steps are enqueued in batches; the first batch of a fixpoint is the
+    previous fixpoint's step count (exact on families like config 2), later
+    ones double up to `max_batch`. The host reads the device state once per
+    batch. With `graphs` (default: the backend's choice) every batch is a
+    replay of captured CUDA graphs, so a step costs no host launches; the
+    buffers and graphs persist on the backend across calls."""
     n = backend.n
     bounds = [int(b) for b in bounds]
-    lo, hi = bounds[rank], bounds[rank + 1]
-    maxrows = max(bounds[r + 1] - bounds[r] for r in range(world))
-    x = backend.zeros(n)
-    send = backend.zeros(maxrows)
-    gathered = [backend.zeros(maxrows) for _ in range(world)]
-    acc = backend.acc_tensor(np.ascontiguousarray(acc_words, dtype=np.uint64))
-    red = torch.zeros(2, dtype=torch.int64, device=x.device)
+    use_graphs = getattr(backend, "graphs", False) if graphs is None else graphs
+    key = (tuple(bounds), rank, world, id(group), bool(use_graphs))
+    cache = backend.__dict__.setdefault("_runners", {})
+    if key not in cache:
+        cache[key] = _Runner(backend, dist, rank, world, bounds, group, use_graphs)
+    rn = cache[key]
+    words = np.ascontiguousarray(acc_words, dtype=np.uint64)
+    rn.acc.copy_(backend.acc_tensor(words))
+    x, state = rn.x, rn.state
     stats = MapStats()
     verdict = Verdict.no_cycle()
-    fsize = int(np.unpackbits(np.ascontiguousarray(acc_words, dtype=np.uint64).view(np.uint8)).sum())
+    fsize = int(np.bitwise_count(words).sum())
+    guess = 4
     while fsize > 0:  # front.any()
         x.zero_()
-        steps = 0
-        witness = _NONE
+        state.zero_()
+        state[2] = _NONE
+        state[3] = int(early_exit)
+        batch = max(guess, 1)
         while True:
-            flags = backend.step(x, acc, lo, hi, send)
-            dist.all_gather(gathered, send, group=group)
-            for r in range(world):
-                k = bounds[r + 1] - bounds[r]
-                if k:
-                    x[bounds[r]: bounds[r + 1]].copy_(gathered[r][:k])
-            red[0] = flags[0].to(torch.int64)
-            red[1] = -(flags[1].to(torch.int64) & 0xFFFFFFFF)
-            dist.all_reduce(red, op=dist.ReduceOp.MAX, group=group)
-            changed, wit = (int(v) for v in red.cpu())
-            wit = -wit
-            steps += 1
-            if early_exit and wit != _NONE:
-                witness = wit
+            rn.steps(batch)
+            done, steps, witness, _ = (int(v) for v in state.cpu())
+            if done:
                 break
-            if not changed:
-                witness = wit
-                break
+            batch = min(max(batch * 2, 4), max_batch)
+        guess = steps
         stats.iterations += 1
         stats.kernel_calls += steps
         if witness != _NONE:
             stats.cycle_witness = witness
             verdict = Verdict.cycle(witness)
             break
-        acc, dcount, fsize = backend.demote(x, acc)
+        rem, dcount, fsize = backend.demote(x, rn.acc)
+        rn.acc.copy_(rem)  # in place: captured graphs read this buffer
         stats.demoted_total += dcount
         if dcount == 0:
             break
-    return ShardedResult(verdict, stats, x[:n] if n else x[:0])
+    return ShardedResult(verdict, stats, x[:n].clone() if n else x[:0].clone())

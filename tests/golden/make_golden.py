@@ -42,12 +42,13 @@ def main():
     F = oracle.Reference()
     R = oracle.Restatement()
     out = {"generator": "tests/golden/make_golden.py", "reference": "/root/reference/proj @ src/"
-           "{graph,map_engine,parallel,errors,oracle}.cpp (graph.hpp:56 patched copy, see oracle/Makefile)",
+           "{graph,map_engine,parallel,errors,oracle,owcty}.cpp (graph.hpp:56 patched copy, see oracle/Makefile)",
            "configs": {}, "random": []}
     arrays = {}
     # canonical configurations at full or scaled-down size
     cases = [("c1", 1, {}), ("c2_L16", 2, {"L": 16, "W": 64, "S": 8}),
-             ("c5_L16", 5, {"L": 16, "W": 4, "S": 16}), ("c3_s12", 3, {"scale": 12})]
+             ("c5_L16", 5, {"L": 16, "W": 4, "S": 16}), ("c3_s12", 3, {"scale": 12}),
+             ("c4_g6", 4, {"grid_bits": 6, "region": 16})]
     for name, idx, over in cases:
         p = R.preset(idx)
         for k, v in over.items():
@@ -61,6 +62,9 @@ def main():
             csr, acc, _ = rs.export()
             key = "transposed" if tr else "forward"
             entry[key] = {"m": csr.m, "off_digest": digest(csr.off), "col_digest": digest(csr.col)}
+            # run_owcty (owcty.cpp:56-87) on the same snapshot
+            oc, ow, oit, ofs = rs.run_owcty()
+            entry[key]["owcty"] = {"cycle": oc, "witness": ow, "outer_iterations": oit, "final_size": ofs}
             for early in (True, False):
                 rec, fx = record(rs, accw, early)
                 entry[key]["early" if early else "full"] = rec

@@ -142,7 +142,7 @@ def test_golden_random(eng, golden):
                 assert [int(h) for h in run.iter_hash] == want["iter_hash"]
 
 
-@pytest.mark.parametrize("name", ["c1", "c2_L16", "c5_L16", "c3_s12"])
+@pytest.mark.parametrize("name", ["c1", "c2_L16", "c5_L16", "c3_s12", "c4_g6"])
 def test_golden_configs(eng, R, golden, name):
     cfg = golden["configs"][name]
     p = R.preset(cfg["config"])
@@ -173,6 +173,10 @@ def test_golden_configs(eng, R, golden, name):
                     orient, mode, key)
                 assert digest(run.final_values) == w["final_x_digest"]
                 assert [int(h) for h in run.iter_hash[:256]] == w["iter_hash"]
+        wo = want["owcty"]
+        v, st = eng.run_owcty(s)
+        assert (v.cycle_found(), v.witness, st.outer_iterations, st.final_size) == (
+            wo["cycle"], wo["witness"], wo["outer_iterations"], wo["final_size"])
         r = eng.restrict_to_accepting_sccs(s)
         wr = want["restricted"]
         assert (r.snapshot.n, r.snapshot.m) == (wr["n"], wr["m"])

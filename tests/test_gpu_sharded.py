@@ -57,7 +57,8 @@ def test_cuda_shard_backend_matches_run_map(eng, R, nccl):
         be = sharded.CudaShardBackend(snap, torch.device("cuda", 0))
         off, _ = snap.gather_index()
         for early in (True, False):
-            res = sharded.run_map_sharded(be, nccl, 0, 1, [0, n], words, early)
+            # eager launches and captured CUDA-graph batches give the same run
+            res = sharded.run_map_sharded(be, nccl, 0, 1, [0, n], words, early, graphs=bool(t % 2))
             ref = R.run_map(R.transpose(R.build_snapshot(n, e, True)), words, early)
             got = (res.verdict.cycle_found(), res.verdict.witness, res.stats.iterations,
                    res.stats.kernel_calls, res.stats.demoted_total)
@@ -67,11 +68,23 @@ def test_cuda_shard_backend_matches_run_map(eng, R, nccl):
         b = sharded.plan(off, 3)
         x = torch.from_numpy(rng.integers(0, n + 1, size=n).astype(np.int32)).cuda()
         accd = be.acc_tensor(words)
-        outs = []
+        outs, recs = [], []
         for r in range(3):
             o = be.zeros(int(b[r + 1] - b[r]))
-            be.step(x, accd, int(b[r]), int(b[r + 1]), o)
+            rec = be.zeros(2, torch.int64)
+            be.step(x, accd, int(b[r]), int(b[r + 1]), o, rec)
             outs.append(o[: int(b[r + 1] - b[r])].cpu().numpy())
-        full, _, _ = R.step(R.transpose(R.build_snapshot(n, e, True)), x.cpu().numpy().view(np.uint32), words)
+            recs.append(rec.cpu().numpy())
+        full, ch, wit = R.step(R.transpose(R.build_snapshot(n, e, True)), x.cpu().numpy().view(np.uint32), words)
         assert np.array_equal(np.concatenate(outs).view(np.uint32), full)
+        red = np.max(np.stack(recs), axis=0)
+        assert bool(red[0]) == bool(ch)
+        assert (0xFFFFFFFF - int(red[1])) == (0xFFFFFFFF if wit is None else wit)
+        # a decided fixpoint turns the step into a no-op
+        done = be.zeros(4, torch.int64)
+        done[0] = 1
+        o = be.zeros(n)
+        o.fill_(-1)
+        be.step(x, accd, 0, n, o, rec, done)
+        assert bool((o == -1).all())
         be.release()

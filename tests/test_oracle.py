@@ -146,7 +146,7 @@ def test_golden_random_graphs(R, golden):
         assert r.cycle == case["scc_cycle"]
 
 
-@pytest.mark.parametrize("name", ["c1", "c2_L16", "c5_L16", "c3_s12"])
+@pytest.mark.parametrize("name", ["c1", "c2_L16", "c5_L16", "c3_s12", "c4_g6"])
 def test_golden_configs(R, golden, name):
     cfg = golden["configs"][name]
     p = R.preset(cfg["config"])
@@ -171,6 +171,8 @@ def test_golden_configs(R, golden, name):
             key = f"{name}_{orient}_{mode}_final_x"
             if key in vec:
                 assert np.array_equal(vec[key], r.final_x)
+        wo = want["owcty"]
+        assert R.run_owcty(g, accw) == (wo["cycle"], wo["witness"], wo["outer_iterations"], wo["final_size"])
         rg, racc, kept = R.restrict(g, accw)
         wr = want["restricted"]
         assert rg.n == wr["n"] and rg.m == wr["m"] and digest(kept) == wr["kept_digest"]
@@ -242,6 +244,31 @@ def test_reference_step_worker_invariance(REF):
     outs = [rs.step(x, None, w) for w in (1, 2, 4)]
     for o in outs[1:]:
         assert np.array_equal(o[0], outs[0][0]) and o[1:] == outs[0][1:]
+
+
+def test_product_generator_shape(R):
+    # C4 (cyc_gen.h): every one of the 4 G^2 product states is reachable and
+    # ids follow BFS discovery order; accepting = automaton state q2 (1/4);
+    # accepting cycles exist only with the planted reset (verdict by SCC)
+    for gb, k, plant in ((2, 1, 1), (3, 2, 1), (4, 3, 0), (5, 8, 1), (5, 8, 0)):
+        p = R.preset(4)
+        p.grid_bits, p.region, p.plant = gb, k, plant
+        R.prepare(p)
+        n, e, aw = R.generate(p)
+        G = 1 << gb
+        assert n == 4 * G * G and len(e) == 12 * G * G + 6 * plant
+        acc = np.unpackbits(aw.view(np.uint8), bitorder="little")[:n].astype(bool)
+        assert acc.sum() == G * G and e[0].tolist() == [0, 1]
+        # BFS order: sources appear in id order, every id > 0 is first named
+        # as a destination before it appears as a source
+        assert np.all(np.diff(e[:, 0].astype(np.int64)) >= 0)
+        first = {}
+        for i, d in enumerate(e[:, 1].tolist()):
+            first.setdefault(d, i)
+        starts = np.searchsorted(e[:, 0], np.arange(1, n))
+        assert all(first[v] < starts[v - 1] for v in range(1, n))
+        keep = R.keep_mask(R.build_snapshot(n, e, True), acc)
+        assert bool((keep & acc).any()) == bool(plant)
 
 
 def test_generators_deterministic(R):

@@ -13,32 +13,52 @@ import torch.multiprocessing as mp
 
 
 class HostShardBackend:
-    """Row-range Jacobi step on the host (oracle restatement): test backend."""
+    """Row-range Jacobi step on the host (oracle restatement): test backend
+    with the same step / post / demote contract as CudaShardBackend."""
+
+    NONE = 0xFFFFFFFF
 
     def __init__(self, R, gather, n):
         self.torch = torch
         self.R = R
         self.gather = gather
         self.n = n
+        self.bounds = None
 
-    def zeros(self, k):
-        return torch.zeros(max(k, 1), dtype=torch.int32)
+    def zeros(self, k, dtype=None):
+        return torch.zeros(max(k, 1), dtype=dtype or torch.int32)
 
     def acc_tensor(self, words):
         return torch.from_numpy(words.view(np.int64).copy())
 
-    def step(self, x, acc, lo, hi, out):
+    def prepare(self, bounds):
+        self.bounds = [int(b) for b in bounds]
+
+    def step(self, x, acc, lo, hi, out, rec, state=None):
+        rec.zero_()
+        if state is not None and int(state[0]):
+            return
         xv = x.numpy().view(np.uint32)[: self.n]
         words = acc.numpy().view(np.uint64)
         full, _, _ = self.R.step(self.gather, xv, words)
         sl = full[lo:hi]
         out[: hi - lo] = torch.from_numpy(sl.view(np.int32).copy())
-        changed = int(np.any(sl != xv[lo:hi]))
         accb = np.unpackbits(words.view(np.uint8), bitorder="little")[: self.n].astype(bool)
         ids = np.arange(lo, hi, dtype=np.int64)
         w = ids[(sl.astype(np.int64) == ids + 1) & accb[lo:hi]]
-        wit = int(w.min()) if len(w) else 0xFFFFFFFF
-        return torch.tensor([changed, np.int64(wit).astype(np.int32)], dtype=torch.int32)
+        rec[0] = int(np.any(sl != xv[lo:hi]))
+        rec[1] = (self.NONE - int(w.min())) if len(w) else 0
+
+    def post(self, rec, state, x_pad, world, maxrows, x):
+        for r in range(world):
+            k = self.bounds[r + 1] - self.bounds[r]
+            x[self.bounds[r]: self.bounds[r + 1]] = x_pad[r * maxrows: r * maxrows + k]
+        if not int(state[0]):
+            wit = self.NONE - int(rec[1])
+            state[1] += 1
+            if (int(state[3]) and wit != self.NONE) or not int(rec[0]):
+                state[0] = 1
+                state[2] = wit
 
     def demote(self, x, acc):
         rem, dem = self.R.demote(x.numpy().view(np.uint32)[: self.n], acc.numpy().view(np.uint64))
