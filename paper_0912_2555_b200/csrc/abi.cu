@@ -573,7 +573,7 @@ cyc_status cyc_owcty(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words
       load_acc(acc_words, g->n(), accb, ctx->s);
       dacc = accb.as<uint64_t>();
     }
-    const cyc::OwctyResult r = cyc::run_owcty_device(g->gath, dacc, ctx->s);
+    const cyc::OwctyResult r = cyc::run_owcty_device(g->snap, g->gath, dacc, ctx->s);
     if (cycle) *cycle = r.cycle;
     if (witness) *witness = r.witness;
     if (stats) {

@@ -14,8 +14,8 @@ struct OwctyResult {
   double elim_ms = 0.0;
 };
 
-// run_owcty (owcty.cpp:56-87) over the relation whose reverse is `gath`
-// (gath row v = predecessors of v); acc = u64 accepting words.
-OwctyResult run_owcty_device(const DevCsr& gath, const uint64_t* acc, cudaStream_t s);
+// run_owcty (owcty.cpp:56-87) over the relation of `snap` (row u = successors
+// of u), `gath` its reverse; acc = u64 accepting words.
+OwctyResult run_owcty_device(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc, cudaStream_t s);
 
 }  // namespace cyc

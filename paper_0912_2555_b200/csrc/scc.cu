@@ -4,21 +4,26 @@
 //
 // Tarjan is inherently sequential. The kept set is set-defined, so any
 // correct SCC decomposition reproduces it; on the device we use:
-//   1. reachability pruning: a kept vertex is reachable from F and reaches F
-//      (both computed by dense OR-propagation over the CSR pair);
+//   0. orientation: colours flow along whichever of the two relations (the
+//      snapshot relation or its reverse) has mostly ascending edges, so a
+//      vertex's ancestors tend to have smaller ids and most SCCs are found in
+//      the first colouring round (config 2 transposed: 65 rounds -> 1);
+//   1. reachability pruning: a kept vertex is reachable from F and reaches F;
 //   2. trimming: a vertex with no active predecessor or successor is a
-//      trivial acyclic SCC;
+//      trivial acyclic SCC (dense passes, usually two);
 //   3. max-colour rounds (Orzan / Barnat et al.'s coloring): colour[v] = max
 //      active id reaching v; each root r (colour[r] == r) owns the SCC of
 //      vertices with colour r that reach r through colour-r vertices.
+// Steps 1 and 3 are closures computed by the frontier engine (frontier.cuh):
+// one persistent kernel per closure, levels touch only changed vertices.
 // Every SCC found is kept iff it holds an accepting vertex and is cyclic
-// (size >= 2 or a self-loop). Passes are dense; convergence flags are read
-// by the host every few passes.
+// (size >= 2 or a self-loop).
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 
+#include "frontier.cuh"
 #include "scc.cuh"
 
 namespace cyc {
@@ -26,58 +31,68 @@ namespace cyc {
 namespace {
 
 constexpr int kT = 256;
+constexpr uint32_t kNoColor = 0xFFFFFFFFu;  // inactive: never raised, never equal
 
 __device__ __forceinline__ bool accb(const uint64_t* acc, uint32_t v) {
   return (acc[v >> 6] >> (v & 63u)) & 1ull;
 }
+__device__ __forceinline__ bool bit(const uint32_t* b, uint32_t v) { return (b[v >> 5] >> (v & 31u)) & 1u; }
 
-__global__ void k_reach_init(uint32_t n, const uint64_t* __restrict__ acc, uint8_t* fw, uint8_t* bw) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    uint8_t a = accb(acc, v) ? 1 : 0;
-    fw[v] = a;
-    bw[v] = a;
+// ---- frontier ops
+struct OpReach {  // mark = vertices reached so far (seeds included)
+  uint32_t* mark;
+  __device__ uint32_t token(uint32_t) const { return 0u; }
+  __device__ bool relax(uint32_t, uint32_t, uint32_t w, uint32_t) const { return test_and_set_bit(mark, w); }
+};
+
+struct OpColor {  // colour[w] = max(colour[w], colour[u]) along the relation
+  uint32_t* color;
+  uint32_t* stamp;  // level + 1 at which w was last queued (zeroed per round)
+  __device__ uint32_t token(uint32_t u) const { return __ldcg(color + u); }
+  __device__ bool relax(uint32_t, uint32_t tok, uint32_t w, uint32_t L) const {
+    if (__ldcg(color + w) >= tok) return false;  // also every inactive w
+    if (atomicMax(color + w, tok) >= tok) return false;
+    return atomicMax(stamp + w, L + 1u) < L + 1u;
   }
-}
+};
 
-// flag |= 1 if any vertex newly reached. rows: for fw use the gather index
-// (predecessors), for bw the snapshot rows (successors).
-// Heavy rows (degree > heavy) are left to the *_chunks kernels, one warp per
-// 256-edge chunk (R-MAT hubs would otherwise serialise a pass on one thread).
-__global__ void k_reach(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                        uint32_t heavy, uint8_t* mark, uint32_t* flag) {
-  bool ch = false;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (mark[v] || off[v + 1] - off[v] > heavy) continue;
-    for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
-      if (((volatile uint8_t*)mark)[col[i]]) {
-        mark[v] = 1;
-        ch = true;
-        break;
-      }
-    }
+struct OpSameColor {  // backward reach from roots through equal colours
+  const uint32_t* color;
+  uint32_t* inscc;
+  __device__ uint32_t token(uint32_t w) const { return __ldcg(color + w); }
+  __device__ bool relax(uint32_t, uint32_t tok, uint32_t v, uint32_t) const {
+    return __ldcg(color + v) == tok && test_and_set_bit(inscc, v);
   }
-  if (ch) *flag = 1;
-}
+};
 
-__global__ void k_reach_chunks(const uint4* __restrict__ chunks, uint32_t nch,
-                               const uint32_t* __restrict__ col, uint8_t* mark, uint32_t* flag) {
+struct SeedBits {
+  const uint32_t* b;
+  __device__ bool operator()(uint32_t v) const { return bit(b, v); }
+};
+struct SeedActive {
+  const uint8_t* a;
+  __device__ bool operator()(uint32_t v) const { return a[v] != 0; }
+};
+struct SeedRoots {
+  const uint32_t* color;
+  __device__ bool operator()(uint32_t v) const { return color[v] == v + 1u; }
+};
+
+// ---- dense kernels
+__global__ void k_count_ascending(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                                  unsigned long long* cnt) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t c = gw; c < nch; c += nw) {
-    const uint4 ch = chunks[c];
-    if (((volatile uint8_t*)mark)[ch.x]) continue;
-    bool hit = false;
-    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) hit |= ((volatile uint8_t*)mark)[col[i]] != 0;
-    if (__any_sync(kFull, hit) && lane == 0) {
-      mark[ch.x] = 1;
-      *flag = 1;
-    }
-  }
+  unsigned long long c = 0;
+  for (uint32_t v = gw; v < n; v += nw)
+    for (uint32_t i = off[v] + lane; i < off[v + 1]; i += 32u) c += col[i] > v;
+  c = __reduce_add_sync(kFull, (uint32_t)c);
+  if (lane == 0 && c) atomicAdd(cnt, c);
 }
 
-__global__ void k_and(uint32_t n, const uint8_t* fw, const uint8_t* bw, uint8_t* active) {
+__global__ void k_and_bits(uint32_t n, const uint32_t* fw, const uint32_t* bw, uint8_t* active) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    active[v] = fw[v] & bw[v];
+    active[v] = bit(fw, v) & bit(bw, v);
 }
 
 __device__ __forceinline__ bool any_active(const uint32_t* off, const uint32_t* col, uint32_t v,
@@ -101,103 +116,9 @@ __global__ void k_trim(uint32_t n, const uint32_t* __restrict__ soff, const uint
   if (ch) *flag = 1;
 }
 
-__global__ void k_color_init(uint32_t n, const uint8_t* active, uint32_t* color, uint8_t* inscc) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    color[v] = active[v] ? v : 0xFFFFFFFFu;
-    inscc[v] = 0;
-  }
-}
-
-__global__ void k_color_prop(uint32_t n, const uint32_t* __restrict__ goff,
-                             const uint32_t* __restrict__ gcol, uint32_t heavy, const uint8_t* active,
-                             uint32_t* color, uint32_t* flag) {
-  bool ch = false;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (!active[v] || goff[v + 1] - goff[v] > heavy) continue;
-    uint32_t c = ((volatile uint32_t*)color)[v], best = c;
-    for (uint32_t i = goff[v]; i < goff[v + 1]; ++i) {
-      uint32_t u = gcol[i];
-      if (active[u]) best = max(best, ((volatile uint32_t*)color)[u]);
-    }
-    if (best != c) {
-      atomicMax(color + v, best);
-      ch = true;
-    }
-  }
-  if (ch) *flag = 1;
-}
-
-__global__ void k_color_chunks(const uint4* __restrict__ chunks, uint32_t nch,
-                               const uint32_t* __restrict__ gcol, const uint8_t* active,
-                               uint32_t* color, uint32_t* flag) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t c = gw; c < nch; c += nw) {
-    const uint4 ch = chunks[c];
-    if (!active[ch.x]) continue;
-    uint32_t best = 0;
-    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) {
-      const uint32_t u = gcol[i];
-      if (active[u]) best = max(best, ((volatile uint32_t*)color)[u]);
-    }
-    best = __reduce_max_sync(kFull, best);
-    if (lane == 0 && best > ((volatile uint32_t*)color)[ch.x]) {
-      atomicMax(color + ch.x, best);
-      *flag = 1;
-    }
-  }
-}
-
-__global__ void k_roots(uint32_t n, const uint8_t* active, const uint32_t* color, uint8_t* inscc,
-                        uint32_t* rsize, uint32_t* rflag) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (active[v] && color[v] == v) {
-      inscc[v] = 1;
-      rsize[v] = 0;
-      rflag[v] = 0;
-    }
-  }
-}
-
-__global__ void k_bw_color(uint32_t n, const uint32_t* __restrict__ soff,
-                           const uint32_t* __restrict__ scol, uint32_t heavy, const uint8_t* active,
-                           const uint32_t* color, uint8_t* inscc, uint32_t* flag) {
-  bool ch = false;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (!active[v] || inscc[v] || soff[v + 1] - soff[v] > heavy) continue;
-    const uint32_t c = color[v];
-    for (uint32_t i = soff[v]; i < soff[v + 1]; ++i) {
-      uint32_t w = scol[i];
-      if (active[w] && color[w] == c && ((volatile uint8_t*)inscc)[w]) {
-        inscc[v] = 1;
-        ch = true;
-        break;
-      }
-    }
-  }
-  if (ch) *flag = 1;
-}
-
-__global__ void k_bw_chunks(const uint4* __restrict__ chunks, uint32_t nch,
-                            const uint32_t* __restrict__ scol, const uint8_t* active,
-                            const uint32_t* color, uint8_t* inscc, uint32_t* flag) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t c = gw; c < nch; c += nw) {
-    const uint4 ch = chunks[c];
-    const uint32_t v = ch.x;
-    if (!active[v] || ((volatile uint8_t*)inscc)[v]) continue;
-    const uint32_t cv = color[v];
-    bool hit = false;
-    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) {
-      const uint32_t w = scol[i];
-      hit |= active[w] && color[w] == cv && ((volatile uint8_t*)inscc)[w];
-    }
-    if (__any_sync(kFull, hit) && lane == 0) {
-      inscc[v] = 1;
-      *flag = 1;
-    }
-  }
+__global__ void k_color_init(uint32_t n, const uint8_t* active, uint32_t* color) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    color[v] = active[v] ? v + 1u : kNoColor;
 }
 
 __device__ bool has_self_loop(const uint32_t* off, const uint32_t* col, uint32_t v) {
@@ -211,33 +132,187 @@ __device__ bool has_self_loop(const uint32_t* off, const uint32_t* col, uint32_t
   return false;
 }
 
+// per root r (colour r+1): size and {has accepting, has self-loop}
 __global__ void k_scc_stats(uint32_t n, const uint32_t* __restrict__ soff,
                             const uint32_t* __restrict__ scol, const uint64_t* __restrict__ acc,
-                            const uint8_t* inscc, const uint32_t* color, uint32_t* rsize,
+                            const uint32_t* inscc, const uint32_t* color, uint32_t* rsize,
                             uint32_t* rflag) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (!inscc[v]) continue;
-    uint32_t r = color[v];
+    if (!bit(inscc, v)) continue;
+    const uint32_t r = color[v] - 1u;
     atomicAdd(rsize + r, 1u);
-    uint32_t f = (accb(acc, v) ? 1u : 0u) | (has_self_loop(soff, scol, v) ? 2u : 0u);
+    const uint32_t f = (accb(acc, v) ? 1u : 0u) | (has_self_loop(soff, scol, v) ? 2u : 0u);
     if (f) atomicOr(rflag + r, f);
   }
 }
 
-__global__ void k_scc_apply(uint32_t n, const uint32_t* color, const uint32_t* rsize,
-                            const uint32_t* rflag, uint8_t* inscc, uint8_t* active, uint8_t* keep,
-                            uint32_t* flag) {
+__global__ void k_scc_apply(uint32_t n, const uint32_t* color, uint32_t* rsize, uint32_t* rflag,
+                            const uint32_t* inscc, uint8_t* active, uint8_t* keep, uint32_t* flag) {
   bool any = false;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (inscc[v]) {
-      uint32_t r = color[v];
+    if (bit(inscc, v)) {
+      const uint32_t r = color[v] - 1u;
       keep[v] = (rflag[r] & 1u) && (rsize[r] >= 2u || (rflag[r] & 2u));
       active[v] = 0;
-      inscc[v] = 0;
     }
     any |= active[v] != 0;
   }
   if (any) *flag = 1;
+}
+
+// ---- dense pull passes (Gauss-Seidel) with epoch stamps: ep[v] = p when v
+// changed in pass p; *cnt += changes. Heavy rows (deg > heavy) are done by the
+// *_chunks kernels, one warp per 256-edge chunk.
+__device__ __forceinline__ void count_changes(uint32_t c, unsigned long long* cnt) {
+  c = __reduce_add_sync(kFull, c);
+  if ((threadIdx.x & 31u) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
+
+__global__ void k_reach_pull(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                             uint32_t heavy, uint32_t* mark, uint8_t* ep, uint8_t p, unsigned long long* cnt) {
+  uint32_t c = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; w0 < n; w0 += stride) {
+    const uint32_t w = w0 + lane_id();
+    if (w >= n || bit(mark, w) || off[w + 1] - off[w] > heavy) continue;
+    for (uint32_t i = off[w]; i < off[w + 1]; ++i) {
+      if (bit(mark, col[i])) {
+        atomicOr(mark + (w >> 5), 1u << (w & 31u));
+        ep[w] = p;
+        ++c;
+        break;
+      }
+    }
+  }
+  count_changes(c, cnt);
+}
+
+__global__ void k_reach_pull_chunks(const uint4* __restrict__ chunks, uint32_t nch,
+                                    const uint32_t* __restrict__ col, uint32_t* mark, uint8_t* ep, uint8_t p,
+                                    unsigned long long* cnt) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  uint32_t c = 0;
+  for (uint32_t k = gw; k < nch; k += nw) {
+    const uint4 ch = chunks[k];
+    if (bit(mark, ch.x)) continue;
+    bool hit = false;
+    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) hit |= bit(mark, col[i]);
+    if (__any_sync(kFull, hit) && lane == 0 && test_and_set_bit(mark, ch.x)) {
+      ep[ch.x] = p;
+      ++c;
+    }
+  }
+  count_changes(c, cnt);
+}
+
+__global__ void k_color_pull(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                             uint32_t heavy, uint32_t* color, uint8_t* ep, uint8_t p, unsigned long long* cnt) {
+  uint32_t c = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; w0 < n; w0 += stride) {
+    const uint32_t w = w0 + lane_id();
+    if (w >= n) continue;
+    const uint32_t own = ((volatile uint32_t*)color)[w];
+    if (own == kNoColor || off[w + 1] - off[w] > heavy) continue;
+    uint32_t best = own;
+    for (uint32_t i = off[w]; i < off[w + 1]; ++i) {
+      const uint32_t cu = ((volatile uint32_t*)color)[col[i]];
+      if (cu != kNoColor) best = max(best, cu);
+    }
+    if (best > own) {
+      atomicMax(color + w, best);
+      ep[w] = p;
+      ++c;
+    }
+  }
+  count_changes(c, cnt);
+}
+
+__global__ void k_color_pull_chunks(const uint4* __restrict__ chunks, uint32_t nch,
+                                    const uint32_t* __restrict__ col, uint32_t* color, uint8_t* ep, uint8_t p,
+                                    unsigned long long* cnt) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  uint32_t c = 0;
+  for (uint32_t k = gw; k < nch; k += nw) {
+    const uint4 ch = chunks[k];
+    const uint32_t own = ((volatile uint32_t*)color)[ch.x];
+    if (own == kNoColor) continue;
+    uint32_t best = 0;
+    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) {
+      const uint32_t cu = ((volatile uint32_t*)color)[col[i]];
+      if (cu != kNoColor) best = max(best, cu);
+    }
+    best = __reduce_max_sync(kFull, best);
+    if (lane == 0 && best > own && atomicMax(color + ch.x, best) < best) {
+      ep[ch.x] = p;
+      ++c;
+    }
+  }
+  count_changes(c, cnt);
+}
+
+// v joins its root's SCC if a successor (in A) of the same colour has joined
+__global__ void k_same_pull(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                            uint32_t heavy, const uint32_t* color, uint32_t* inscc, uint8_t* ep, uint8_t p,
+                            unsigned long long* cnt) {
+  uint32_t c = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane_id();
+    if (v >= n) continue;
+    const uint32_t cv = color[v];
+    if (cv == kNoColor || bit(inscc, v) || off[v + 1] - off[v] > heavy) continue;
+    for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
+      const uint32_t w = col[i];
+      if (color[w] == cv && bit(inscc, w)) {
+        atomicOr(inscc + (v >> 5), 1u << (v & 31u));
+        ep[v] = p;
+        ++c;
+        break;
+      }
+    }
+  }
+  count_changes(c, cnt);
+}
+
+__global__ void k_same_pull_chunks(const uint4* __restrict__ chunks, uint32_t nch,
+                                   const uint32_t* __restrict__ col, const uint32_t* color, uint32_t* inscc,
+                                   uint8_t* ep, uint8_t p, unsigned long long* cnt) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  uint32_t c = 0;
+  for (uint32_t k = gw; k < nch; k += nw) {
+    const uint4 ch = chunks[k];
+    const uint32_t cv = color[ch.x];
+    if (cv == kNoColor || bit(inscc, ch.x)) continue;
+    bool hit = false;
+    for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) {
+      const uint32_t w = col[i];
+      hit |= color[w] == cv && bit(inscc, w);
+    }
+    if (__any_sync(kFull, hit) && lane == 0 && test_and_set_bit(inscc, ch.x)) {
+      ep[ch.x] = p;
+      ++c;
+    }
+  }
+  count_changes(c, cnt);
+}
+
+struct SeedEpoch {
+  const uint8_t* ep;
+  uint8_t p;
+  __device__ bool operator()(uint32_t v) const { return ep[v] == p; }
+};
+
+__global__ void k_clear_roots(uint32_t n, const uint32_t* color, const uint32_t* inscc, uint32_t* rsize,
+                              uint32_t* rflag) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (bit(inscc, v) && color[v] == v + 1u) {
+      rsize[v] = 0;
+      rflag[v] = 0;
+    }
 }
 
 __global__ void k_keep_acc32(uint32_t n, const uint8_t* keep, const uint64_t* __restrict__ acc,
@@ -338,6 +413,31 @@ struct SccLog {
   }
 };
 
+// A closure: Gauss-Seidel pull passes while they change many vertices (cheap
+// per edge, no queue traffic; R-MAT converges in a handful), then the
+// frontier engine from the vertices the last pass changed (long chains).
+constexpr uint32_t kSwitchDiv = 64;  // frontier once a pass changes < n/64
+constexpr int kMaxDense = 250;       // epochs are u8
+
+template <class Dense, class Op>
+int hybrid_closure(uint32_t n, uint8_t* ep, unsigned long long* dcnt, Dense&& dense, const DevCsr& push,
+                   const FrontierBufs& fb, const Op& op, cudaStream_t s) {
+  CYC_CUDA(cudaMemsetAsync(ep, 0, n, s));
+  for (int p = 1;; ++p) {
+    unsigned long long c = 0;
+    CYC_CUDA(cudaMemsetAsync(dcnt, 0, 8, s));
+    dense((uint8_t)p);
+    CYC_CUDA(cudaMemcpyAsync(&c, dcnt, 8, cudaMemcpyDeviceToHost, s));
+    CYC_CUDA(cudaStreamSynchronize(s));
+    if (c == 0) return p;
+    if (c < n / kSwitchDiv || p == kMaxDense) {
+      seed_frontier(n, SeedEpoch{ep, (uint8_t)p}, fb, nullptr, s);
+      run_frontier(push.o(), push.c(), fb, op, s);
+      return -p;  // negative: finished on the frontier engine
+    }
+  }
+}
+
 void filter_csr(const DevCsr& in, const uint8_t* keep, const uint32_t* newid, const uint32_t* kept,
                 uint32_t k, cudaStream_t s, DevCsr& out) {
   out.n = k;
@@ -362,90 +462,104 @@ void filter_csr(const DevCsr& in, const uint8_t* keep, const uint32_t* newid, co
 
 }  // namespace
 
-void scc_keep_mask(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc, cudaStream_t s,
+void scc_keep_mask(const DevCsr& snap_in, const DevCsr& gath_in, const uint64_t* acc, cudaStream_t s,
                    uint8_t* keep) {
-  const uint32_t n = snap.n;
+  const uint32_t n = snap_in.n;
   CYC_CUDA(cudaMemsetAsync(keep, 0, (size_t)n + 1, s));
   if (!n) return;
-  DevBuf fw((size_t)n + 1, s), bw((size_t)n + 1, s), active((size_t)n + 1, s), inscc((size_t)n + 1, s);
-  DevBuf color(((size_t)n + 1) * 4, s), rsize(((size_t)n + 1) * 4, s), rflag(((size_t)n + 1) * 4, s);
-  DevBuf flag(16, s);
-  uint32_t* f = flag.as<uint32_t>();
-  const uint32_t grid = grid_for(n, kT, 8);
   SccLog lg;
-  k_reach_init<<<grid, kT, 0, s>>>(n, acc, fw.as<uint8_t>(), bw.as<uint8_t>());
+  const uint32_t grid = grid_for(n, kT, 8);
+  DevBuf flag(32, s);
+  uint32_t* f = flag.as<uint32_t>();
+  // 0. colours flow along A, the relation with mostly ascending edges
+  unsigned long long asc = 0;
+  CYC_CUDA(cudaMemsetAsync(f, 0, 8, s));
+  k_count_ascending<<<sm_count() * 8, kT, 0, s>>>(n, snap_in.o(), snap_in.c(), (unsigned long long*)f);
   CYC_LAUNCHED();
-  const uint32_t hg = gath.heavy_deg ? gath.heavy_deg : kNone, hs = snap.heavy_deg ? snap.heavy_deg : kNone;
-  const uint32_t cgrid = sm_count() * 8;
-  int np = until_stable(f, s, [&] {
-    k_reach<<<grid, kT, 0, s>>>(n, gath.o(), gath.c(), hg, fw.as<uint8_t>(), f);
-    CYC_LAUNCHED();
-    if (gath.n_heavy_chunks) {
-      k_reach_chunks<<<cgrid, kT, 0, s>>>(gath.heavy.as<uint4>(), gath.n_heavy_chunks, gath.c(),
-                                          fw.as<uint8_t>(), f);
+  CYC_CUDA(cudaMemcpyAsync(&asc, f, 8, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  const bool flip = 2 * asc < (unsigned long long)snap_in.m;
+  const DevCsr& A = flip ? gath_in : snap_in;  // row u = successors of u in A
+  const DevCsr& B = flip ? snap_in : gath_in;  // reverse of A
+  const size_t words = (size_t)n / 32 + 2;
+  DevBuf fw(words * 4, s), bw(words * 4, s), inscc(words * 4, s), active((size_t)n + 1, s);
+  DevBuf color(((size_t)n + 1) * 4, s), stamp(((size_t)n + 1) * 4, s);
+  DevBuf rsize(((size_t)n + 1) * 4, s), rflag(((size_t)n + 1) * 4, s);
+  FrontierWs ws;
+  const FrontierBufs fb = ws.bufs(n, (uint64_t)snap_in.m, s);
+  lg.mark(flip ? "orient-rev" : "orient-fwd", 1);
+  // 1. reach from F along A and along B (seeds: F, marked)
+  CYC_CUDA(cudaMemsetAsync(fw.p, 0, words * 4, s));
+  CYC_CUDA(cudaMemsetAsync(bw.p, 0, words * 4, s));
+  CYC_CUDA(cudaMemcpyAsync(fw.p, acc, ((size_t)n + 63) / 64 * 8, cudaMemcpyDeviceToDevice, s));
+  CYC_CUDA(cudaMemcpyAsync(bw.p, acc, ((size_t)n + 63) / 64 * 8, cudaMemcpyDeviceToDevice, s));
+  DevBuf ep((size_t)n + 1, s);
+  unsigned long long* dc = reinterpret_cast<unsigned long long*>(f + 4);
+  const uint32_t cg = sm_count() * 8;
+  auto hv = [](const DevCsr& g) { return g.n_heavy_chunks ? g.heavy_deg : kNone; };
+  auto reach = [&](const DevCsr& push, const DevCsr& pull, DevBuf& mark) {
+    return hybrid_closure(n, ep.as<uint8_t>(), dc, [&](uint8_t p) {
+      k_reach_pull<<<grid, kT, 0, s>>>(n, pull.o(), pull.c(), hv(pull), mark.as<uint32_t>(), ep.as<uint8_t>(), p, dc);
       CYC_LAUNCHED();
-    }
-  });
-  lg.mark("reach-fw", np);
-  np = until_stable(f, s, [&] {
-    k_reach<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), hs, bw.as<uint8_t>(), f);
-    CYC_LAUNCHED();
-    if (snap.n_heavy_chunks) {
-      k_reach_chunks<<<cgrid, kT, 0, s>>>(snap.heavy.as<uint4>(), snap.n_heavy_chunks, snap.c(),
-                                          bw.as<uint8_t>(), f);
-      CYC_LAUNCHED();
-    }
-  });
-  lg.mark("reach-bw", np);
-  k_and<<<grid, kT, 0, s>>>(n, fw.as<uint8_t>(), bw.as<uint8_t>(), active.as<uint8_t>());
+      if (pull.n_heavy_chunks) {
+        k_reach_pull_chunks<<<cg, kT, 0, s>>>(pull.heavy.as<uint4>(), pull.n_heavy_chunks, pull.c(),
+                                              mark.as<uint32_t>(), ep.as<uint8_t>(), p, dc);
+        CYC_LAUNCHED();
+      }
+    }, push, fb, OpReach{mark.as<uint32_t>()}, s);
+  };
+  int np = reach(A, B, fw);
+  lg.mark("reach-A", np);
+  np = reach(B, A, bw);
+  lg.mark("reach-B", np);
+  k_and_bits<<<grid, kT, 0, s>>>(n, fw.as<uint32_t>(), bw.as<uint32_t>(), active.as<uint8_t>());
   CYC_LAUNCHED();
-  int rounds = 0;
-  for (;;) {
-    ++rounds;
+  for (int round = 0;; ++round) {
     np = until_stable(f, s, [&] {
-      k_trim<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), gath.o(), gath.c(), active.as<uint8_t>(), f);
+      k_trim<<<grid, kT, 0, s>>>(n, A.o(), A.c(), B.o(), B.c(), active.as<uint8_t>(), f);
       CYC_LAUNCHED();
     });
     lg.mark("trim", np);
-    k_color_init<<<grid, kT, 0, s>>>(n, active.as<uint8_t>(), color.as<uint32_t>(), inscc.as<uint8_t>());
+    k_color_init<<<grid, kT, 0, s>>>(n, active.as<uint8_t>(), color.as<uint32_t>());
     CYC_LAUNCHED();
-    np = until_stable(f, s, [&] {
-      k_color_prop<<<grid, kT, 0, s>>>(n, gath.o(), gath.c(), hg, active.as<uint8_t>(),
-                                       color.as<uint32_t>(), f);
+    CYC_CUDA(cudaMemsetAsync(stamp.p, 0, (size_t)n * 4, s));
+    np = hybrid_closure(n, ep.as<uint8_t>(), dc, [&](uint8_t p) {
+      k_color_pull<<<grid, kT, 0, s>>>(n, B.o(), B.c(), hv(B), color.as<uint32_t>(), ep.as<uint8_t>(), p, dc);
       CYC_LAUNCHED();
-      if (gath.n_heavy_chunks) {
-        k_color_chunks<<<cgrid, kT, 0, s>>>(gath.heavy.as<uint4>(), gath.n_heavy_chunks, gath.c(),
-                                            active.as<uint8_t>(), color.as<uint32_t>(), f);
+      if (B.n_heavy_chunks) {
+        k_color_pull_chunks<<<cg, kT, 0, s>>>(B.heavy.as<uint4>(), B.n_heavy_chunks, B.c(), color.as<uint32_t>(),
+                                              ep.as<uint8_t>(), p, dc);
         CYC_LAUNCHED();
       }
-    });
+    }, A, fb, OpColor{color.as<uint32_t>(), stamp.as<uint32_t>()}, s);
     lg.mark("color", np);
-    k_roots<<<grid, kT, 0, s>>>(n, active.as<uint8_t>(), color.as<uint32_t>(), inscc.as<uint8_t>(),
-                                rsize.as<uint32_t>(), rflag.as<uint32_t>());
-    CYC_LAUNCHED();
-    np = until_stable(f, s, [&] {
-      k_bw_color<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), hs, active.as<uint8_t>(),
-                                     color.as<uint32_t>(), inscc.as<uint8_t>(), f);
+    CYC_CUDA(cudaMemsetAsync(inscc.p, 0, words * 4, s));
+    seed_frontier(n, SeedRoots{color.as<uint32_t>()}, fb, inscc.as<uint32_t>(), s);
+    np = hybrid_closure(n, ep.as<uint8_t>(), dc, [&](uint8_t p) {
+      k_same_pull<<<grid, kT, 0, s>>>(n, A.o(), A.c(), hv(A), color.as<uint32_t>(), inscc.as<uint32_t>(),
+                                      ep.as<uint8_t>(), p, dc);
       CYC_LAUNCHED();
-      if (snap.n_heavy_chunks) {
-        k_bw_chunks<<<cgrid, kT, 0, s>>>(snap.heavy.as<uint4>(), snap.n_heavy_chunks, snap.c(),
-                                         active.as<uint8_t>(), color.as<uint32_t>(),
-                                         inscc.as<uint8_t>(), f);
+      if (A.n_heavy_chunks) {
+        k_same_pull_chunks<<<cg, kT, 0, s>>>(A.heavy.as<uint4>(), A.n_heavy_chunks, A.c(), color.as<uint32_t>(),
+                                             inscc.as<uint32_t>(), ep.as<uint8_t>(), p, dc);
         CYC_LAUNCHED();
       }
-    });
-    lg.mark("bw-color", np);
-    k_scc_stats<<<grid, kT, 0, s>>>(n, snap.o(), snap.c(), acc, inscc.as<uint8_t>(),
-                                    color.as<uint32_t>(), rsize.as<uint32_t>(), rflag.as<uint32_t>());
+    }, B, fb, OpSameColor{color.as<uint32_t>(), inscc.as<uint32_t>()}, s);
+    lg.mark("same-color", np);
+    k_clear_roots<<<grid, kT, 0, s>>>(n, color.as<uint32_t>(), inscc.as<uint32_t>(), rsize.as<uint32_t>(),
+                                      rflag.as<uint32_t>());
+    CYC_LAUNCHED();
+    k_scc_stats<<<grid, kT, 0, s>>>(n, A.o(), A.c(), acc, inscc.as<uint32_t>(), color.as<uint32_t>(),
+                                    rsize.as<uint32_t>(), rflag.as<uint32_t>());
     CYC_LAUNCHED();
     uint32_t any = 0;
     CYC_CUDA(cudaMemsetAsync(f, 0, 4, s));
-    k_scc_apply<<<grid, kT, 0, s>>>(n, color.as<uint32_t>(), rsize.as<uint32_t>(),
-                                    rflag.as<uint32_t>(), inscc.as<uint8_t>(), active.as<uint8_t>(),
-                                    keep, f);
+    k_scc_apply<<<grid, kT, 0, s>>>(n, color.as<uint32_t>(), rsize.as<uint32_t>(), rflag.as<uint32_t>(),
+                                    inscc.as<uint32_t>(), active.as<uint8_t>(), keep, f);
     CYC_LAUNCHED();
     CYC_CUDA(cudaMemcpyAsync(&any, f, 4, cudaMemcpyDeviceToHost, s));
     CYC_CUDA(cudaStreamSynchronize(s));
+    lg.mark("apply", round + 1);
     if (!any) break;
   }
 }
