@@ -36,7 +36,7 @@ constexpr uint32_t kBigChunk = 1024;
 struct FrontierBufs {
   uint32_t* q[2] = {nullptr, nullptr};    // capacity cap each
   uint2* big[2] = {nullptr, nullptr};     // {row, chunk} entries, capacity bigcap each
-  uint32_t* cnt = nullptr;                // [0..2] queue lengths, [3..5] big counts, [6] levels
+  uint32_t* cnt = nullptr;  // [0..2] queue lengths, [3..5] big counts, [6] levels, [7] solo exit level
   uint32_t cap = 0;
   uint32_t bigcap = 0;
 };
@@ -56,6 +56,135 @@ __device__ __forceinline__ void frontier_push(bool push, uint32_t w, uint32_t* q
   if (push) q[base + __popc(bal & lanemask_lt())] = w;
 }
 
+// One warp walks the rows of its (up to) 32 vertices, 32 edges per round;
+// rows with d > big_deg are handed to big(u, d) instead. push(ok, w) is
+// called converged once per round.
+template <class Op, class Push, class Big>
+__device__ __forceinline__ void warp_rows(bool has, uint32_t u, const uint32_t* __restrict__ off,
+                                          const uint32_t* __restrict__ col, const Op& op, uint32_t L,
+                                          uint32_t big_deg, Push&& push, Big&& big) {
+  const uint32_t lane = lane_id();
+  const uint32_t tok = has ? op.token(u) : 0u;
+  uint32_t b = 0, d = 0;
+  if (has) {
+    b = off[u];
+    d = off[u + 1] - b;
+    if (d > big_deg) {
+      big(u, d);
+      d = 0;
+    }
+  }
+  const uint32_t incl = warp_incl_scan(d);
+  const uint32_t excl = incl - d;
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  for (uint32_t r = 0; r < total; r += 32u) {
+    const uint32_t e = r + lane;
+    uint32_t owner = 0;
+#pragma unroll
+    for (uint32_t step = 16; step >= 1; step >>= 1) {
+      const uint32_t cand = owner + step;
+      const uint32_t ex = __shfl_sync(kFull, excl, cand & 31u);
+      if (cand < 32u && ex <= e) owner = cand;
+    }
+    const uint32_t ob = __shfl_sync(kFull, b, owner);
+    const uint32_t oe = __shfl_sync(kFull, excl, owner);
+    const uint32_t ot = __shfl_sync(kFull, tok, owner);
+    const uint32_t ou = __shfl_sync(kFull, u, owner);
+    bool ok = false;
+    uint32_t w = 0;
+    if (e < total) {
+      w = col[ob + (e - oe)];
+      ok = op.relax(ou, ot, w, L);
+    }
+    push(ok, w);
+  }
+}
+
+// Solo mode: while levels stay small, CTA 0 runs them alone from shared-memory
+// queues with __syncthreads() between levels (a level then costs its memory
+// round trips, not a grid barrier); the other CTAs wait at the grid barrier.
+// On exit it leaves the global queue and counters as level `L` of the normal
+// mode expects them and publishes L in cnt[7]: queue q[L&1] with cnt[L%3]
+// entries, every other counter zero.
+constexpr uint32_t kSoloCap = 2048;     // shared queue entries per level
+constexpr uint32_t kSoloMaxDeg = 4096;  // a longer row sends the level back to the grid
+constexpr uint32_t kSoloEnter = 512;    // one 32-vertex group per warp of the CTA
+
+template <class Op>
+__device__ void solo_levels(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                            const FrontierBufs& fb, const Op& op, uint32_t L, uint32_t len) {
+  __shared__ uint32_t sq[2][kSoloCap];
+  __shared__ uint32_t scnt[2];
+  __shared__ uint32_t sbig;
+  const uint32_t lane = lane_id();
+  const uint32_t wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  {
+    const uint32_t* qc = (L & 1u) ? fb.q[1] : fb.q[0];
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) sq[0][i] = __ldcg(qc + i);
+  }
+  if (threadIdx.x == 0) {
+    scnt[0] = len;
+    scnt[1] = 0;
+    sbig = 0;
+  }
+  __syncthreads();
+  int cur = 0;
+  for (;;) {
+    const uint32_t n0 = scnt[cur];
+    // a long row in this level: hand the level back to the grid
+    for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) {
+      const uint32_t u = sq[cur][i];
+      if (off[u + 1] - off[u] > kSoloMaxDeg) sbig = 1;
+    }
+    __syncthreads();
+    if (sbig) {
+      uint32_t* qg = (L & 1u) ? fb.q[1] : fb.q[0];
+      for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) qg[i] = sq[cur][i];
+      if (threadIdx.x == 0) {
+        for (int k = 0; k < 6; ++k) fb.cnt[k] = 0;
+        fb.cnt[L % 3u] = n0;
+        fb.cnt[7] = L;
+      }
+      return;
+    }
+    uint32_t* qn_glob = (L & 1u) ? fb.q[0] : fb.q[1];  // overflow target = level L+1's queue
+    uint32_t* sn = sq[cur ^ 1];
+    uint32_t* snc = &scnt[cur ^ 1];
+    auto push = [&](bool ok, uint32_t w) {
+      const uint32_t bal = __ballot_sync(kFull, ok);
+      if (!bal) return;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(snc, (uint32_t)__popc(bal));
+      base = __shfl_sync(kFull, base, 0);
+      if (ok) {
+        const uint32_t idx = base + __popc(bal & lanemask_lt());
+        if (idx < kSoloCap) sn[idx] = w; else qn_glob[idx] = w;
+      }
+    };
+    auto nobig = [](uint32_t, uint32_t) {};
+    for (uint32_t base = wid * 32u; base < n0; base += nwarps * 32u) {
+      const uint32_t i = base + lane;
+      const bool has = i < n0;
+      warp_rows(has, has ? sq[cur][i] : 0u, off, col, op, L, 0xFFFFFFFFu, push, nobig);
+    }
+    __syncthreads();
+    const uint32_t nn = *snc;
+    ++L;
+    if (nn == 0 || nn > kSoloCap) {  // done, or back to the grid with level L
+      for (uint32_t i = threadIdx.x; i < nn && i < kSoloCap; i += blockDim.x) qn_glob[i] = sn[i];
+      if (threadIdx.x == 0) {
+        for (int k = 0; k < 6; ++k) fb.cnt[k] = 0;
+        fb.cnt[L % 3u] = nn;
+        fb.cnt[7] = L;
+      }
+      return;
+    }
+    if (threadIdx.x == 0) scnt[cur] = 0;
+    cur ^= 1;
+    __syncthreads();
+  }
+}
+
 template <class Op>
 __global__ void __launch_bounds__(kFrontierThreads) k_frontier(const uint32_t* __restrict__ off,
                                                                 const uint32_t* __restrict__ col,
@@ -65,63 +194,43 @@ __global__ void __launch_bounds__(kFrontierThreads) k_frontier(const uint32_t* _
   const uint32_t lane = lane_id();
   const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t gw = gtid >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t L = 0;; ++L) {
+  bool solo_ok = true;  // no solo right after leaving it for a long row
+  for (uint32_t L = 0;;) {
+    const uint32_t len = __ldcg(fb.cnt + L % 3u);
+    if (len == 0) {
+      if (gtid == 0) fb.cnt[6] = L;
+      return;
+    }
+    if (len <= kSoloEnter && solo_ok) {
+      if (blockIdx.x == 0) solo_levels(off, col, fb, op, L, len);
+      grid.sync();
+      const uint32_t L2 = __ldcg(fb.cnt + 7);
+      solo_ok = L2 != L;  // solo handed back the level it started with: run it on the grid
+      L = L2;
+      continue;
+    }
+    solo_ok = true;
     const bool odd = L & 1u;
     const uint32_t* __restrict__ qc = odd ? fb.q[1] : fb.q[0];
     uint32_t* qn = odd ? fb.q[0] : fb.q[1];
     uint32_t* ncnt = fb.cnt + (L + 1u) % 3u;
     uint2* bl = odd ? fb.big[1] : fb.big[0];
     uint32_t* bcnt = fb.cnt + 3u + L % 3u;
-    const uint32_t len = __ldcg(fb.cnt + L % 3u);
-    if (len == 0) {
-      if (gtid == 0) fb.cnt[6] = L;
-      return;
-    }
     if (gtid == 0) {
       fb.cnt[(L + 2u) % 3u] = 0;       // read at level L-1, written at level L+1
       fb.cnt[3u + (L + 2u) % 3u] = 0;
     }
     // phase A: rows of the queued vertices, 32 vertices per warp
+    auto push = [&](bool ok, uint32_t w) { frontier_push(ok, w, qn, ncnt); };
+    auto big = [&](uint32_t u, uint32_t d) {
+      const uint32_t nc = (d + kBigChunk - 1u) / kBigChunk;
+      const uint32_t at = atomicAdd(bcnt, nc);
+      for (uint32_t c = 0; c < nc; ++c) bl[at + c] = make_uint2(u, c);
+    };
     for (uint32_t base = gw * 32u; base < len; base += nw * 32u) {
       const uint32_t i = base + lane;
       const bool has = i < len;
-      const uint32_t u = has ? __ldcg(qc + i) : 0u;
-      const uint32_t tok = has ? op.token(u) : 0u;
-      uint32_t b = 0, d = 0;
-      if (has) {
-        b = off[u];
-        d = off[u + 1] - b;
-        if (d > kBigDeg) {
-          const uint32_t nc = (d + kBigChunk - 1u) / kBigChunk;
-          const uint32_t at = atomicAdd(bcnt, nc);
-          for (uint32_t c = 0; c < nc; ++c) bl[at + c] = make_uint2(u, c);
-          d = 0;
-        }
-      }
-      const uint32_t incl = warp_incl_scan(d);
-      const uint32_t excl = incl - d;
-      const uint32_t total = __shfl_sync(kFull, incl, 31);
-      for (uint32_t r = 0; r < total; r += 32u) {
-        const uint32_t e = r + lane;
-        uint32_t owner = 0;
-#pragma unroll
-        for (uint32_t step = 16; step >= 1; step >>= 1) {
-          const uint32_t cand = owner + step;
-          const uint32_t ex = __shfl_sync(kFull, excl, cand & 31u);
-          if (cand < 32u && ex <= e) owner = cand;
-        }
-        const uint32_t ob = __shfl_sync(kFull, b, owner);
-        const uint32_t oe = __shfl_sync(kFull, excl, owner);
-        const uint32_t ot = __shfl_sync(kFull, tok, owner);
-        const uint32_t ou = __shfl_sync(kFull, u, owner);
-        bool push = false;
-        uint32_t w = 0;
-        if (e < total) {
-          w = col[ob + (e - oe)];
-          push = op.relax(ou, ot, w, L);
-        }
-        frontier_push(push, w, qn, ncnt);
-      }
+      warp_rows(has, has ? __ldcg(qc + i) : 0u, off, col, op, L, kBigDeg, push, big);
     }
     grid.sync();
     // phase B: chunks of long rows, one warp per chunk
@@ -136,17 +245,18 @@ __global__ void __launch_bounds__(kFrontierThreads) k_frontier(const uint32_t* _
         const uint32_t end = min(e, b + kBigChunk);
         for (uint32_t i0 = b; i0 < end; i0 += 32u) {
           const uint32_t i = i0 + lane;
-          bool push = false;
+          bool ok = false;
           uint32_t w = 0;
           if (i < end) {
             w = col[i];
-            push = op.relax(u, tok, w, L);
+            ok = op.relax(u, tok, w, L);
           }
-          frontier_push(push, w, qn, ncnt);
+          frontier_push(ok, w, qn, ncnt);
         }
       }
       grid.sync();
     }
+    ++L;
   }
 }
 

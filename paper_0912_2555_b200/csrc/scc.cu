@@ -79,15 +79,26 @@ struct SeedRoots {
 };
 
 // ---- dense kernels
+// Light rows one per lane, rows longer than 64 by the whole warp.
 __global__ void k_count_ascending(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
                                   unsigned long long* cnt) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  unsigned long long c = 0;
-  for (uint32_t v = gw; v < n; v += nw)
-    for (uint32_t i = off[v] + lane; i < off[v + 1]; i += 32u) c += col[i] > v;
-  c = __reduce_add_sync(kFull, (uint32_t)c);
-  if (lane == 0 && c) atomicAdd(cnt, c);
+  const uint32_t lane = lane_id();
+  uint32_t c = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane;
+    const uint32_t b = v < n ? off[v] : 0u, e = v < n ? off[v + 1] : 0u;
+    const bool heavy = e - b > 64u;
+    if (!heavy)
+      for (uint32_t i = b; i < e; ++i) c += col[i] > v;
+    for (uint32_t hb = __ballot_sync(kFull, heavy); hb; hb &= hb - 1u) {
+      const uint32_t l = __ffs(hb) - 1u;
+      const uint32_t hv = v0 + l, hb0 = __shfl_sync(kFull, b, l), he = __shfl_sync(kFull, e, l);
+      for (uint32_t i = hb0 + lane; i < he; i += 32u) c += col[i] > hv;
+    }
+  }
+  c = __reduce_add_sync(kFull, c);
+  if (lane == 0 && c) atomicAdd(cnt, (unsigned long long)c);
 }
 
 __global__ void k_and_bits(uint32_t n, const uint32_t* fw, const uint32_t* bw, uint8_t* active) {
@@ -132,17 +143,24 @@ __device__ bool has_self_loop(const uint32_t* off, const uint32_t* col, uint32_t
   return false;
 }
 
-// per root r (colour r+1): size and {has accepting, has self-loop}
+// per root r (colour r+1): size and {has accepting, has self-loop}; lanes
+// sharing a root (one giant SCC on R-MAT) combine before the atomics
 __global__ void k_scc_stats(uint32_t n, const uint32_t* __restrict__ soff,
                             const uint32_t* __restrict__ scol, const uint64_t* __restrict__ acc,
                             const uint32_t* inscc, const uint32_t* color, uint32_t* rsize,
                             uint32_t* rflag) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    if (!bit(inscc, v)) continue;
-    const uint32_t r = color[v] - 1u;
-    atomicAdd(rsize + r, 1u);
-    const uint32_t f = (accb(acc, v) ? 1u : 0u) | (has_self_loop(soff, scol, v) ? 2u : 0u);
-    if (f) atomicOr(rflag + r, f);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane_id();
+    const bool in = v < n && bit(inscc, v);
+    const uint32_t r = in ? color[v] - 1u : kNone;
+    const uint32_t f = in ? ((accb(acc, v) ? 1u : 0u) | (has_self_loop(soff, scol, v) ? 2u : 0u)) : 0u;
+    const uint32_t peers = __match_any_sync(kFull, r);
+    const uint32_t fo = __reduce_or_sync(peers, f);
+    if (in && (peers & lanemask_lt()) == 0) {  // lowest lane of the group
+      atomicAdd(rsize + r, (uint32_t)__popc(peers));
+      if (fo) atomicOr(rflag + r, fo);
+    }
   }
 }
 
@@ -474,7 +492,7 @@ void scc_keep_mask(const DevCsr& snap_in, const DevCsr& gath_in, const uint64_t*
   // 0. colours flow along A, the relation with mostly ascending edges
   unsigned long long asc = 0;
   CYC_CUDA(cudaMemsetAsync(f, 0, 8, s));
-  k_count_ascending<<<sm_count() * 8, kT, 0, s>>>(n, snap_in.o(), snap_in.c(), (unsigned long long*)f);
+  k_count_ascending<<<grid, kT, 0, s>>>(n, snap_in.o(), snap_in.c(), (unsigned long long*)f);
   CYC_LAUNCHED();
   CYC_CUDA(cudaMemcpyAsync(&asc, f, 8, cudaMemcpyDeviceToHost, s));
   CYC_CUDA(cudaStreamSynchronize(s));
