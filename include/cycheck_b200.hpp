@@ -206,5 +206,39 @@ std::vector<uint32_t> demote(const Engine& e, const std::vector<uint32_t>& value
   return d;
 }
 
+// run_owcty — owcty.hpp:28-31 over the snapshot relation (the reference runs
+// it on a forward snapshot, cycheck_main.cpp:98-106). StatsT is the
+// reference's OwctyStats (outer_iterations, reach_ms, elim_ms, final_size).
+template <class VerdictT, class StatsT, class BitsetT>
+std::pair<VerdictT, StatsT> run_owcty(const Snapshot& s, const BitsetT& accepting) {
+  if (accepting.size() != s.n()) throw DefaultContractError("run_owcty: accepting set size mismatch");
+  int32_t cyc = 0;
+  uint32_t w = 0;
+  cyc_owcty_stats st{};
+  check(cyc_owcty(s.engine().get(), s.get(), accepting.words().data(), &cyc, &w, &st));
+  StatsT stats;
+  stats.outer_iterations = st.outer_iterations;
+  stats.reach_ms = st.reach_ms;
+  stats.elim_ms = st.elim_ms;
+  stats.final_size = st.final_size;
+  return {cyc ? VerdictT::cycle(w) : VerdictT::no_cycle(), stats};
+}
+
+// scc_verdict — oracle.cpp:32-98 on the snapshot relation: the verdict and the
+// accepting vertices of cyclic SCCs (ascending).
+template <class VerdictT>
+VerdictT scc_verdict(const Snapshot& s, std::vector<uint32_t>* cyclic_accepting = nullptr) {
+  int32_t cyc = 0;
+  uint32_t w = 0;
+  uint64_t k = 0;
+  std::vector<uint32_t> buf(cyclic_accepting ? s.n() + 1 : 0);
+  check(cyc_scc_verdict(s.engine().get(), s.get(), &cyc, &w, cyclic_accepting ? buf.data() : nullptr, &k));
+  if (cyclic_accepting) {
+    buf.resize(k);
+    *cyclic_accepting = std::move(buf);
+  }
+  return cyc ? VerdictT::cycle(w) : VerdictT::no_cycle();
+}
+
 }  // namespace b200
 }  // namespace cycheck

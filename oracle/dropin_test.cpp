@@ -11,6 +11,8 @@
 
 #include "cycheck/graph.hpp"
 #include "cycheck/map_engine.hpp"
+#include "cycheck/oracle.hpp"
+#include "cycheck/owcty.hpp"
 #include "../include/cycheck_b200.hpp"
 
 using namespace cycheck;
@@ -58,6 +60,18 @@ int main(int argc, char** argv) {
             ++bad;
           }
         }
+      }
+      // OWCTY and the SCC verdict through the drop-in (owcty.hpp, oracle.hpp)
+      auto [ov, os] = run_owcty(ref, ref.accepting);
+      auto [gov, gos] = b200::run_owcty<Verdict, OwctyStats>(dev, ref.accepting);
+      if (!(gov == ov) || gos.outer_iterations != os.outer_iterations || gos.final_size != os.final_size) {
+        std::printf("trial %d: run_owcty differs\n", t);
+        ++bad;
+      }
+      const Verdict sv = scc_verdict(ref.edge_list(), ref.n, ref.accepting, ~0ull).verdict;
+      if (b200::scc_verdict<Verdict>(dev).cycle_found() != sv.cycle_found()) {
+        std::printf("trial %d: scc_verdict differs\n", t);
+        ++bad;
       }
       SccRestriction rr = restrict_to_accepting_sccs(ref);
       auto [gr, kept] = b200::restrict_to_accepting_sccs(dev);
