@@ -104,6 +104,18 @@ cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, 
 cyc_status cyc_graph_from_csr(cyc_ctx* ctx, const uint64_t* row_offsets, const uint32_t* col_indices,
                               uint32_t n, uint64_t m, const uint64_t* acc_words, int orientation,
                               cyc_graph** out);
+/* Incremental snapshot: the snapshot of the log prefix
+ * (m_prev + m_new edges, n vertices) from `prev` — the snapshot of the prefix
+ * (m_prev, prev n) — and only the new edges new_edges[0 .. 2*m_new) (log
+ * order, host or device). Equal, bit for bit, to cyc_graph_build on the whole
+ * prefix (graph.cpp:63-105), which the explorer's detector does every round
+ * (explore.cpp:71-124). n >= prev's n; acc_words = accepting prefix of n
+ * (NULL: prev's bits, new vertices not accepting). prev must not be
+ * restricted; orientation is prev's. */
+cyc_status cyc_graph_extend(cyc_ctx* ctx, const cyc_graph* prev, const uint32_t* new_edges, uint64_t m_new,
+                            uint32_t n, const uint64_t* acc_words, cyc_graph** out);
+/* Logged-edge prefix length a snapshot was built from (m_prev for extend). */
+cyc_status cyc_graph_log_prefix(const cyc_graph* g, uint64_t* m_log);
 /* restrict_to_accepting_sccs (graph.hpp:103-114, graph.cpp:190-221). */
 cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out);
 void cyc_graph_destroy(cyc_graph* g);

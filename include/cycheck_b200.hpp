@@ -129,6 +129,27 @@ Snapshot build_snapshot(const Engine& e, const EdgeLogT& log, OrientationT orien
   return build_snapshot(e, log, orientation, m, n);
 }
 
+// Incremental snapshot: the snapshot of the prefix (m, n) of
+// the same log `prev` was built from, uploading and sorting only the edges
+// logged since. Same result as build_snapshot(e, log, orientation, m, n) — what
+// the explorer's detector calls every round (explore.cpp:71-124).
+template <class EdgeLogT>
+Snapshot extend_snapshot(const Snapshot& prev, const EdgeLogT& log, uint64_t m, uint32_t n) {
+  uint64_t m_prev = 0;
+  check(cyc_graph_log_prefix(prev.get(), &m_prev));
+  if (m < m_prev) throw DefaultContractError("extend_snapshot: edge prefix shrinks");
+  std::vector<uint32_t> edges(2 * (m - m_prev) + 2);
+  for (uint64_t i = m_prev; i < m; ++i) {
+    auto pr = log.edge(i);
+    edges[2 * (i - m_prev)] = pr.first;
+    edges[2 * (i - m_prev) + 1] = pr.second;
+  }
+  auto acc = log.accepting_prefix(n);
+  cyc_graph* g = nullptr;
+  check(cyc_graph_extend(prev.engine().get(), prev.get(), edges.data(), m - m_prev, n, acc.words().data(), &g));
+  return Snapshot(prev.engine(), g);
+}
+
 // Upload of a host CsrSnapshot (for callers that already built one).
 template <class Csr>
 Snapshot upload(const Engine& e, const Csr& snap) {

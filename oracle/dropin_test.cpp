@@ -6,6 +6,7 @@
 // it: same Verdict, witness and MapStats from cycheck::run_map, the same CSR
 // from build_snapshot, the same restriction. Runs on a GPU box (the binary is
 // prebuilt into oracle/_ref/ and shipped); exits non-zero on any mismatch.
+#include <algorithm>
 #include <cstdio>
 #include <random>
 
@@ -39,6 +40,25 @@ int main(int argc, char** argv) {
         ++bad;
       }
       b200::Snapshot up = b200::upload(gpu, ref);
+      // incremental: snapshot of a prefix (vertex prefix = just enough for
+      // its edges), extended to the whole log
+      {
+        const uint64_t mh = m / 2;
+        uint32_t nh = 0;
+        for (uint64_t i = 0; i < mh; ++i) {
+          auto e = log.edge(i);
+          nh = std::max(nh, std::max(e.first, e.second) + 1);
+        }
+        b200::Snapshot half = b200::build_snapshot(gpu, log, o, mh, nh);
+        b200::Snapshot ext = b200::extend_snapshot(half, log, m, n);
+        CsrSnapshot eb;
+        ext.export_to(eb);
+        if (eb.row_offsets != ref.row_offsets || eb.col_indices != ref.col_indices ||
+            !(eb.accepting == ref.accepting)) {
+          std::printf("trial %d: extend_snapshot differs\n", t);
+          ++bad;
+        }
+      }
       for (bool early : {true, false}) {
         MapOptions opts;
         opts.early_exit = early;

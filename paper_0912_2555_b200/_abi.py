@@ -119,6 +119,8 @@ _SIGS = {
     "cyc_ctx_set_stream": (C.c_int, [_P, _P, C.c_int]),
     "cyc_graph_build": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.POINTER(_P)]),
     "cyc_graph_from_csr": (C.c_int, [_P, _P, _P, C.c_uint32, C.c_uint64, _P, C.c_int, C.POINTER(_P)]),
+    "cyc_graph_extend": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, _P, C.POINTER(_P)]),
+    "cyc_graph_log_prefix": (C.c_int, [_P, _U64P]),
     "cyc_graph_restrict": (C.c_int, [_P, _P, C.POINTER(_P)]),
     "cyc_graph_destroy": (None, [_P]),
     "cyc_graph_info": (C.c_int, [_P, _U32P, _U64P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

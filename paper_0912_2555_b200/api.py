@@ -403,6 +403,37 @@ def build_snapshot(log, orientation: Orientation = Orientation.transposed,
     return CsrSnapshot(h, ctx)
 
 
+def extend_snapshot(prev: CsrSnapshot, log, m: Optional[int] = None, n: Optional[int] = None) -> CsrSnapshot:
+    """Incremental snapshot: the snapshot of the log prefix
+    (m, n) from ``prev`` (the snapshot of a shorter prefix of the same log) and
+    the new edges only. Equal to ``build_snapshot(log, prev.orientation, m, n)``
+    — the explorer's per-round rebuild (explore.cpp:71-124).
+
+    ``log`` is an EdgeLog, or a tuple (n, new_edges[k,2], accepting) holding
+    only the edges after prev's prefix."""
+    ctx = prev.context
+    m_prev = C.c_uint64()
+    check(_abi.lib().cyc_graph_log_prefix(prev.handle, C.byref(m_prev)))
+    if isinstance(log, EdgeLog):
+        mm = log.edge_count() if m is None else int(m)
+        nn = log.vertex_count() if n is None else int(n)
+        if mm > log.edge_count():
+            raise ContractError("build_snapshot: prefix beyond log")
+        if mm < m_prev.value:
+            raise ContractError("extend_snapshot: edge prefix shrinks")
+        new = log.edges(mm)[m_prev.value:]
+        acc = log.accepting_prefix(nn).words()
+    else:
+        nn, new, acc = log
+        new = np.asarray(new, dtype=np.uint32).reshape(-1, 2)
+        acc = as_bitset(acc, int(nn)).words() if acc is not None else None
+    new = np.ascontiguousarray(new)
+    h = C.c_void_p()
+    check(_abi.lib().cyc_graph_extend(ctx.handle, prev.handle, ptr(new), C.c_uint64(len(new)),
+                                      C.c_uint32(int(nn)), ptr(acc), C.byref(h)))
+    return CsrSnapshot(h, ctx)
+
+
 @dataclass
 class SccRestriction:
     """graph.hpp:105-108."""
@@ -689,5 +720,5 @@ __all__ = [
     "as_bitset", "build_snapshot", "check_graph", "default_context", "demote", "fixpoint",
     "init_vector", "launch_count", "propagate_step", "restrict_to_accepting_sccs", "run_map",
     "run_map_detailed", "shard_bounds", "map_trace", "scc_verdict", "OracleVerdict", "OwctyStats",
-    "run_owcty",
+    "run_owcty", "extend_snapshot",
 ]

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/cyc_gen.h"
+#include "extend.cuh"
 #include "gen.cuh"
 #include "map_run.cuh"
 #include "owcty.cuh"
@@ -62,6 +63,7 @@ struct cyc_graph {
   cyc_ctx* ctx = nullptr;
   int orientation = CYC_TRANSPOSED;
   int restricted = 0;
+  uint64_t m_log = 0;  // logged-edge prefix the snapshot was built from (extend needs it)
   cyc::DevCsr snap;  // the snapshot relation (rows as CsrSnapshot), push side
   cyc::DevCsr gath;  // its reverse: the MaxPropagation gather index, pull side
   cyc::DevBuf acc;   // u64 words
@@ -188,6 +190,7 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   const uint32_t* de = stage_in(edges, (size_t)m_log * 2, tmp_edges, s);
   g->ctx = ctx;
   g->orientation = orientation;
+  g->m_log = m_log;
   const int snap_key_dst = orientation == CYC_TRANSPOSED;
   cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>(), ctx->arena);
   cyc::build_csr(de, m_log, n, !snap_key_dst, s, g->gath, err.as<uint32_t>(), ctx->arena);
@@ -365,6 +368,53 @@ cyc_status cyc_graph_from_csr(cyc_ctx* ctx, const uint64_t* row_offsets, const u
     }
     ctx->refs.fetch_add(1);
     *out = g;
+  });
+}
+
+cyc_status cyc_graph_extend(cyc_ctx* ctx, const cyc_graph* prev, const uint32_t* new_edges, uint64_t m_new,
+                            uint32_t n, const uint64_t* acc_words, cyc_graph** out) {
+  return guard([&] {
+    require(ctx && prev && out, CYC_E_CONTRACT, "extend_snapshot: null argument");
+    require(!prev->restricted, CYC_E_CONTRACT, "extend_snapshot: restricted snapshots cannot grow");
+    require(n >= prev->n(), CYC_E_CONTRACT, "extend_snapshot: vertex prefix shrinks");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    auto* g = new cyc_graph;
+    try {
+      cyc_graph delta;
+      build_graph(ctx, new_edges, m_new, n, acc_words, prev->orientation, &delta);
+      cudaStream_t s = ctx->s;
+      g->ctx = ctx;
+      g->orientation = prev->orientation;
+      g->m_log = prev->m_log + m_new;
+      require(g->m_log < 0xFFFFFFFFull, CYC_E_RESOURCE, "edge log prefix must be < 2^32");
+      cyc::merge_csr(prev->snap, delta.snap, n, s, g->snap);
+      cyc::merge_csr(prev->gath, delta.gath, n, s, g->gath);
+      require(g->snap.m == g->gath.m, CYC_E_CUDA, "internal: snapshot/gather edge counts differ");
+      cyc::build_heavy(g->gath, 256, 256, s);
+      cyc::build_heavy(g->snap, 256, 256, s);
+      cyc::build_ell(g->gath, s);
+      if (acc_words) {
+        load_acc(acc_words, n, g->acc, s);
+      } else {  // previous accepting bits, new vertices not accepting
+        const size_t nw = acc_words64(n), pw = acc_words64(prev->n());
+        g->acc.alloc((nw + 1) * 8, s);
+        CYC_CUDA(cudaMemsetAsync(g->acc.p, 0, (nw + 1) * 8, s));
+        if (pw) CYC_CUDA(cudaMemcpyAsync(g->acc.p, prev->acc.p, pw * 8, cudaMemcpyDeviceToDevice, s));
+      }
+      CYC_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    ctx->refs.fetch_add(1);
+    *out = g;
+  });
+}
+
+cyc_status cyc_graph_log_prefix(const cyc_graph* g, uint64_t* m_log) {
+  return guard([&] {
+    require(g && m_log, CYC_E_CONTRACT, "null argument");
+    *m_log = g->m_log;
   });
 }
 

@@ -50,3 +50,12 @@ for mode in modes:
                     q = lambda x: np.median((x[m] - t0[m]) / 1e3)
                     print(f"      Ef in [{lo:.0e},{hi:.0e}): n={m.sum():5d} mean {dur[m].mean():7.2f} us "
                           f"| phase0 {q(p0):6.2f} phase1 {q(p1):6.2f} flags {q(fl):6.2f} end {q(t1):6.2f}")
+    if os.environ.get("TRACE_RAISED"):
+        raised = tr[:, 3]
+        for k, name in ((1, "pull"), (2, "push")):
+            sel = kind == k
+            if sel.any():
+                qs = np.percentile(raised[sel], [5, 25, 50, 75, 95])
+                print(f"   {name} raised per step: p5/25/50/75/95 = {qs.astype(int).tolist()} (n={s.n})")
+        # raised vs step-in-fixpoint for the first few fixpoints
+        print("   step-in-fixpoint raised (first fixpoint):", [int(r) for r in tr[:70, 3]])

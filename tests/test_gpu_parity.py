@@ -457,3 +457,54 @@ def test_device_owcty(eng, R, REF):
     gacc = np.unpackbits(ga.view(np.uint8), bitorder="little")[:gn].astype(bool)
     want = REF.snapshot(gn, ge, gacc, False).run_owcty()
     assert (v.cycle_found(), v.witness, st.outer_iterations, st.final_size) == want
+
+
+def test_extend_snapshot_equals_rebuild(eng, R):
+    """Incremental snapshots: growing a device snapshot round by
+    round, as the explorer's detector does (explore.cpp:71-124), gives exactly
+    the snapshot a full rebuild of the prefix gives (graph.cpp:63-105) — both
+    CSRs, accepting bits — and the same run_map."""
+    rng = np.random.default_rng(1717)
+    for trial in range(6):
+        n_final = int(rng.integers(50, 6000))
+        m_final = int(n_final * rng.choice([2, 4]))
+        e = random_graph(rng, n_final, m_final, hubs=trial % 2)
+        # make the log grow like an explorer: vertex v appears before its edges
+        order = np.argsort(np.maximum(e[:, 0], e[:, 1]), kind="stable")
+        e = np.ascontiguousarray(e[order])
+        acc = rng.random(n_final) < 0.1
+        tr = bool(trial % 3)
+        o = eng.Orientation.transposed if tr else eng.Orientation.forward
+        cuts = sorted(set(int(c) for c in rng.integers(1, len(e), size=4))) + [len(e)]
+        m0 = cuts[0]
+        n0 = int(e[:m0].max()) + 1
+        s = eng.build_snapshot((n0, e[:m0], acc[:n0]), o)
+        prev_m = m0
+        for c in cuts[1:]:
+            n1 = max(int(e[:c].max()) + 1, s.n)
+            s = eng.extend_snapshot(s, (n1, e[prev_m:c], acc[:n1]))
+            full = eng.build_snapshot((n1, e[:c], acc[:n1]), o)
+            assert s.n == full.n and s.m == full.m
+            assert np.array_equal(s.row_offsets, full.row_offsets)
+            assert np.array_equal(s.col_indices, full.col_indices)
+            assert np.array_equal(s.accepting.words(), full.accepting.words())
+            go, gc = s.gather_index()
+            fo, fc = full.gather_index()
+            assert np.array_equal(go, fo) and np.array_equal(gc, fc)
+            prev_m = c
+        v1, st1 = eng.run_map(s, s.accepting)
+        v2, st2 = eng.run_map(full, full.accepting)
+        assert (v1.cycle_found(), v1.witness, st1.kernel_calls) == (v2.cycle_found(), v2.witness, st2.kernel_calls)
+    # EdgeLog form (prefix semantics of the reference API) and contract errors
+    log = eng.EdgeLog()
+    for v in range(5):
+        log.add_vertex(v % 2 == 0)
+    for a, b in [(0, 1), (1, 2), (2, 0), (3, 4)]:
+        log.append_edge(a, b)
+    s = eng.build_snapshot(log, eng.Orientation.transposed, 2, 3)
+    s2 = eng.extend_snapshot(s, log)
+    full = eng.build_snapshot(log, eng.Orientation.transposed)
+    assert s2.row_offsets.tolist() == full.row_offsets.tolist()
+    assert s2.col_indices.tolist() == full.col_indices.tolist()
+    with pytest.raises(eng.ContractError):
+        eng.extend_snapshot(s2, (3, np.zeros((0, 2), np.uint32), [True] * 3))  # vertex prefix shrinks
