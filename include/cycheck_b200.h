@@ -12,6 +12,8 @@
  *   CYC_E_CONTRACT  -> cycheck::ContractError      (precondition broken)
  *   CYC_E_RESOURCE  -> cycheck::ResourceLimitError (capacity / device OOM)
  *   CYC_E_CUDA      -> runtime failure (CUDA / NCCL error)
+ *   CYC_E_PARSE     -> cycheck::ParseError (message = ParseError::what(),
+ *                      code/line/col via cyc_last_parse_error)
  * cyc_last_error() returns the calling thread's last message.
  *
  * Conventions (reference types.hpp:9, map_engine.hpp:16-29, bitset.hpp:12-72):
@@ -34,7 +36,8 @@ typedef enum cyc_status {
   CYC_E_CONTRACT = 1,
   CYC_E_RESOURCE = 2,
   CYC_E_CUDA = 3,
-  CYC_E_INVALID = 4
+  CYC_E_INVALID = 4,
+  CYC_E_PARSE = 5
 } cyc_status;
 
 /* reference types.hpp:12 `enum class Orientation { forward, transposed }` */
@@ -179,6 +182,28 @@ typedef struct cyc_owcty_stats {
 } cyc_owcty_stats;
 cyc_status cyc_owcty(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words, int32_t* cycle,
                      uint32_t* witness, cyc_owcty_stats* stats);
+
+/* ---- explicit-graph ingestion ---------------------------- */
+/* ExplicitGraph (graph.hpp:136-150) on the device. */
+typedef struct cyc_explicit cyc_explicit;
+/* parse_explicit_graph (graph.cpp:259-297) of `len` bytes of text (host or
+ * device): "graph <n>", "accepting <id>...", "edge <src> <dst>" lines, '#'
+ * comments. On malformed input returns CYC_E_PARSE with the reference's
+ * ParseError text ("<line>:<col>: error[syntax|range]: ...") for the same
+ * first offending line. */
+cyc_status cyc_explicit_parse(cyc_ctx* ctx, const char* text, uint64_t len, cyc_explicit** out);
+/* Binary edge list: "CYCGRAPH", u32 version = 1, u32 n, u64 m, u64 accepting
+ * words[ceil(n/64)], u32 edges[2m] (log order) — one file feeds the reference
+ * (oracle/ref_driver.cpp) and the device without text parsing. */
+cyc_status cyc_explicit_load_binary(cyc_ctx* ctx, const void* data, uint64_t len, cyc_explicit** out);
+/* DiagCode (errors.hpp:21-28), line, column of the last CYC_E_PARSE. */
+cyc_status cyc_last_parse_error(int* code, int* line, int* col);
+cyc_status cyc_explicit_info(const cyc_explicit* g, uint32_t* n, uint64_t* n_accepting, uint64_t* m);
+/* accepting ids (file order; ascending for binary input) and edges (2m u32). */
+cyc_status cyc_explicit_export(const cyc_explicit* g, uint32_t* accepting, uint32_t* edges);
+/* fill_log (graph.cpp:305-310) + build_snapshot on the device. */
+cyc_status cyc_explicit_snapshot(cyc_ctx* ctx, const cyc_explicit* g, int orientation, cyc_graph** out);
+void cyc_explicit_destroy(cyc_explicit* g);
 
 /* ---- one-call pipeline: edge log -> verdict ----------------------------- */
 /* cycheck graph / explore final round (cycheck_main.cpp:88-97,

@@ -252,6 +252,10 @@ class Restatement:
         return int(p.n), e, acc
 
 
+class RefParseError(RuntimeError):
+    """cycheck::ParseError raised by the reference; str() = what()."""
+
+
 class Reference:
     """The reference implementation (compiled from /root/reference sources)."""
 
@@ -274,14 +278,48 @@ class Reference:
         L.ref_run_map.argtypes = [_P, _P, C.c_int, C.c_int, _P, _P, _P, _P, C.c_uint64, C.c_int]
         L.ref_scc_verdict.argtypes = [_P, C.POINTER(C.c_int)]
         L.ref_run_owcty.argtypes = [_P, _P, _P]
+        L.ref_explicit_parse.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(_P)]
+        L.ref_explicit_info.argtypes = [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.ref_explicit_info.restype = None
+        L.ref_explicit_export.argtypes = [_P, _P, _P]
+        L.ref_explicit_export.restype = None
+        L.ref_explicit_free.argtypes = [_P]
+        L.ref_explicit_free.restype = None
+        L.ref_explicit_snapshot.argtypes = [_P, C.c_int, C.POINTER(_P)]
         L.ref_time_steps.argtypes = [_P, C.c_int, C.c_uint64, C.c_double, _P, C.POINTER(C.c_uint64)]
         L.ref_time_build.argtypes = [_P, C.c_int, C.POINTER(C.c_double)]
         L.ref_hw_threads.restype = C.c_int
 
     def _ok(self, rc: int) -> None:
         if rc != 0:
-            msg = self.lib.ref_last_error().decode()
-            raise {1: ValueError, 2: MemoryError}.get(rc, RuntimeError)(msg)
+            msg = self.lib.ref_last_error().decode(errors="replace")
+            raise {1: ValueError, 2: MemoryError, 5: RefParseError}.get(rc, RuntimeError)(msg)
+
+    def parse_explicit(self, text: bytes):
+        """parse_explicit_graph (graph.cpp:259-297) -> (n, accepting ids, edges[m,2]);
+        raises RefParseError(ParseError::what()) on malformed text."""
+        h = _P()
+        self._ok(self.lib.ref_explicit_parse(text, len(text), C.byref(h)))
+        try:
+            n, na, m = C.c_uint32(), C.c_uint64(), C.c_uint64()
+            self.lib.ref_explicit_info(h, C.byref(n), C.byref(na), C.byref(m))
+            acc = np.zeros(max(na.value, 1), np.uint32)
+            e = np.zeros((max(m.value, 1), 2), np.uint32)
+            self.lib.ref_explicit_export(h, acc.ctypes.data, e.ctypes.data)
+            return int(n.value), acc[: na.value], e[: m.value]
+        finally:
+            self.lib.ref_explicit_free(h)
+
+    def explicit_snapshot(self, text: bytes, transposed: bool = True) -> "RefSnapshot":
+        """load + fill_log + build_snapshot, all by the reference."""
+        h = _P()
+        self._ok(self.lib.ref_explicit_parse(text, len(text), C.byref(h)))
+        try:
+            sh = _P()
+            self._ok(self.lib.ref_explicit_snapshot(h, int(transposed), C.byref(sh)))
+            return RefSnapshot(self, sh)
+        finally:
+            self.lib.ref_explicit_free(h)
 
     def snapshot(self, n: int, edges, acc, transposed: bool = True) -> "RefSnapshot":
         e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))

@@ -14,10 +14,12 @@
 #include <cstring>
 #include <exception>
 #include <stdexcept>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "cycheck/errors.hpp"
 #include "cycheck/graph.hpp"
 #include "cycheck/map_engine.hpp"
 #include "cycheck/oracle.hpp"
@@ -72,6 +74,7 @@ const char* ref_last_error() { return g_err.c_str(); }
   }                                                \
   catch (const ContractError& e) { return fail(e, 1); } \
   catch (const ResourceLimitError& e) { return fail(e, 2); } \
+  catch (const ParseError& e) { return fail(e, 5); } \
   catch (const std::exception& e) { return fail(e, 3); }
 
 // EdgeLog + build_snapshot (graph.cpp:63-111). edges: 2*m u32 pairs.
@@ -284,6 +287,50 @@ int ref_run_owcty(void* h, const uint64_t* acc, uint64_t* out) {
   out[1] = v.witness ? *v.witness : 0xFFFFFFFFull;
   out[2] = st.outer_iterations;
   out[3] = st.final_size;
+  return 0;
+  REF_CATCH
+}
+
+// parse_explicit_graph (graph.cpp:259-297) of an in-memory text; *out owns the
+// ExplicitGraph. Status 5 = ParseError (message = what()).
+int ref_explicit_parse(const char* text, uint64_t len, void** out) {
+  REF_TRY
+  std::istringstream in(std::string(text, len));
+  *out = new ExplicitGraph(parse_explicit_graph(in));
+  return 0;
+  REF_CATCH
+}
+
+void ref_explicit_info(void* h, uint32_t* n, uint64_t* n_acc, uint64_t* m) {
+  auto* g = static_cast<ExplicitGraph*>(h);
+  *n = g->n;
+  *n_acc = g->accepting.size();
+  *m = g->edges.size();
+}
+
+void ref_explicit_export(void* h, uint32_t* acc, uint32_t* edges) {
+  auto* g = static_cast<ExplicitGraph*>(h);
+  for (size_t i = 0; i < g->accepting.size(); ++i) acc[i] = g->accepting[i];
+  for (size_t i = 0; i < g->edges.size(); ++i) {
+    edges[2 * i] = g->edges[i].first;
+    edges[2 * i + 1] = g->edges[i].second;
+  }
+}
+
+void ref_explicit_free(void* h) { delete static_cast<ExplicitGraph*>(h); }
+
+// fill_log (graph.cpp:305-310) + build_snapshot of a parsed explicit graph.
+int ref_explicit_snapshot(void* h, int transposed, void** out) {
+  REF_TRY
+  auto* g = static_cast<ExplicitGraph*>(h);
+  EdgeLog::Limits lim;
+  lim.max_vertices = g->n > 0 ? g->n : 1;
+  lim.max_edges = g->edges.size() > 0 ? g->edges.size() : 1;
+  EdgeLog log(lim);
+  fill_log(*g, log);
+  auto* s = new Snap;
+  s->snap = build_snapshot(log, transposed ? Orientation::transposed : Orientation::forward);
+  *out = s;
   return 0;
   REF_CATCH
 }

@@ -31,7 +31,16 @@ class CudaError(CycheckError):
     """CUDA runtime failure inside the engine."""
 
 
-_ERRORS = {1: ContractError, 2: ResourceLimitError, 3: CudaError, 4: CycheckError}
+class ParseError(CycheckError):
+    """cycheck::ParseError (reference errors.hpp:32-45): code (DiagCode), line, col;
+    str() is ParseError::what()."""
+
+    def __init__(self, msg: str, code: int = 0, line: int = 0, col: int = 0):
+        super().__init__(msg)
+        self.code, self.line, self.col = code, line, col
+
+
+_ERRORS = {1: ContractError, 2: ResourceLimitError, 3: CudaError, 4: CycheckError, 5: ParseError}
 
 CYC_FORWARD, CYC_TRANSPOSED = 0, 1
 CYC_MODE_AUTO, CYC_MODE_PULL, CYC_MODE_PUSH = 0, 1, 2
@@ -131,6 +140,13 @@ _SIGS = {
     "cyc_demote": (C.c_int, [_P, _P, C.c_uint32, _P, _P, _P, _U64P]),
     "cyc_map_run": (C.c_int, [_P, _P, _P, C.POINTER(MapOptionsC), C.POINTER(MapStatsC), _P, _P, _P,
                               C.c_uint64]),
+    "cyc_explicit_parse": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(_P)]),
+    "cyc_explicit_load_binary": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(_P)]),
+    "cyc_last_parse_error": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "cyc_explicit_info": (C.c_int, [_P, _U32P, _U64P, _U64P]),
+    "cyc_explicit_export": (C.c_int, [_P, _P, _P]),
+    "cyc_explicit_snapshot": (C.c_int, [_P, _P, C.c_int, C.POINTER(_P)]),
+    "cyc_explicit_destroy": (None, [_P]),
     "cyc_check": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.c_int,
                             C.POINTER(MapOptionsC), C.POINTER(MapStatsC), C.POINTER(C.c_double)]),
     "cyc_scc_verdict": (C.c_int, [_P, _P, C.POINTER(C.c_int32), _U32P, _P, _U64P]),
@@ -177,6 +193,10 @@ def lib() -> C.CDLL:
 def check(status: int) -> None:
     if status != 0:
         msg = lib().cyc_last_error().decode(errors="replace")
+        if status == 5:
+            c, ln, col = C.c_int(), C.c_int(), C.c_int()
+            lib().cyc_last_parse_error(C.byref(c), C.byref(ln), C.byref(col))
+            raise ParseError(msg, c.value, ln.value, col.value)
         raise _ERRORS.get(status, CycheckError)(msg)
 
 

@@ -24,7 +24,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 from . import _abi
-from ._abi import ContractError, CudaError, CycheckError, ResourceLimitError, check, ptr
+from ._abi import ContractError, CudaError, CycheckError, ParseError, ResourceLimitError, check, ptr
 
 NIL = 0
 _NONE = 0xFFFFFFFF
@@ -434,6 +434,102 @@ def extend_snapshot(prev: CsrSnapshot, log, m: Optional[int] = None, n: Optional
     return CsrSnapshot(h, ctx)
 
 
+# ------------------------------------------------------- explicit graphs
+@dataclass
+class ExplicitGraph:
+    """ExplicitGraph (graph.hpp:140-144): accepting ids in file order."""
+    n: int
+    accepting: np.ndarray
+    edges: np.ndarray  # [m, 2] (src, dst)
+
+
+class DeviceExplicitGraph:
+    """A parsed explicit graph held on the device (cyc_explicit)."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self._h, self._ctx = handle, ctx
+        n, na, m = C.c_uint32(), C.c_uint64(), C.c_uint64()
+        check(_abi.lib().cyc_explicit_info(handle, C.byref(n), C.byref(na), C.byref(m)))
+        self.n, self.n_accepting, self.m = int(n.value), int(na.value), int(m.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _abi.lib().cyc_explicit_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export(self) -> ExplicitGraph:
+        acc = np.zeros(max(self.n_accepting, 1), np.uint32)
+        e = np.zeros((max(self.m, 1), 2), np.uint32)
+        check(_abi.lib().cyc_explicit_export(self._h, ptr(acc), ptr(e)))
+        return ExplicitGraph(self.n, acc[: self.n_accepting], e[: self.m])
+
+    def snapshot(self, orientation: Orientation = Orientation.transposed) -> CsrSnapshot:
+        """fill_log (graph.cpp:305-310) + build_snapshot, on the device."""
+        h = C.c_void_p()
+        check(_abi.lib().cyc_explicit_snapshot(self._ctx.handle, self._h, int(orientation), C.byref(h)))
+        return CsrSnapshot(h, self._ctx)
+
+
+def parse_explicit_device(text, ctx: Optional[Context] = None) -> DeviceExplicitGraph:
+    """parse_explicit_graph (graph.cpp:259-297) on the device; the graph stays
+    there. Raises ParseError with the reference's message on malformed text."""
+    ctx = ctx or default_context()
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    buf = np.frombuffer(data, dtype=np.uint8) if data else np.zeros(1, np.uint8)
+    h = C.c_void_p()
+    check(_abi.lib().cyc_explicit_parse(ctx.handle, ptr(buf), C.c_uint64(len(data)), C.byref(h)))
+    return DeviceExplicitGraph(h, ctx)
+
+
+def parse_explicit_graph(text, ctx: Optional[Context] = None) -> ExplicitGraph:
+    """parse_explicit_graph (graph.hpp:146) with the parse on the device."""
+    return parse_explicit_device(text, ctx).export()
+
+
+def load_explicit_graph(path: str, ctx: Optional[Context] = None) -> ExplicitGraph:
+    """load_explicit_graph (graph.cpp:299-303)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise ParseError(f"0:0: error[syntax]: cannot open '{path}'", 0, 0, 0) from None
+    return parse_explicit_graph(data, ctx)
+
+
+def write_binary_graph(n: int, edges, accepting, path: Optional[str] = None) -> bytes:
+    """The binary edge list read by cyc_explicit_load_binary: "CYCGRAPH", u32
+    version 1, u32 n, u64 m, u64 accepting words, u32 (src, dst) pairs."""
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+    words = as_bitset(accepting, int(n)).words() if accepting is not None else np.zeros((int(n) + 63) // 64,
+                                                                                          np.uint64)
+    words = np.ascontiguousarray(words[: (int(n) + 63) // 64], dtype=np.uint64)
+    hdr = b"CYCGRAPH" + np.array([1, int(n)], np.uint32).tobytes() + np.array([len(e)], np.uint64).tobytes()
+    data = hdr + words.tobytes() + e.tobytes()
+    if path is not None:
+        with open(path, "wb") as f:
+            f.write(data)
+    return data
+
+
+def load_binary_graph(data_or_path, ctx: Optional[Context] = None) -> DeviceExplicitGraph:
+    ctx = ctx or default_context()
+    if isinstance(data_or_path, str):
+        with open(data_or_path, "rb") as f:
+            data = f.read()
+    else:
+        data = bytes(data_or_path)
+    buf = np.frombuffer(data, dtype=np.uint8)
+    h = C.c_void_p()
+    check(_abi.lib().cyc_explicit_load_binary(ctx.handle, ptr(buf), C.c_uint64(len(data)), C.byref(h)))
+    return DeviceExplicitGraph(h, ctx)
+
+
 @dataclass
 class SccRestriction:
     """graph.hpp:105-108."""
@@ -720,5 +816,7 @@ __all__ = [
     "as_bitset", "build_snapshot", "check_graph", "default_context", "demote", "fixpoint",
     "init_vector", "launch_count", "propagate_step", "restrict_to_accepting_sccs", "run_map",
     "run_map_detailed", "shard_bounds", "map_trace", "scc_verdict", "OracleVerdict", "OwctyStats",
-    "run_owcty", "extend_snapshot",
+    "run_owcty", "extend_snapshot", "ExplicitGraph", "DeviceExplicitGraph", "ParseError",
+    "parse_explicit_graph", "parse_explicit_device", "load_explicit_graph", "write_binary_graph",
+    "load_binary_graph",
 ]

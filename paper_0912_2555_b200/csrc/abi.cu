@@ -15,6 +15,7 @@
 #include "../../include/cyc_gen.h"
 #include "extend.cuh"
 #include "gen.cuh"
+#include "ingest.cuh"
 #include "map_run.cuh"
 #include "owcty.cuh"
 #include "scc.cuh"
@@ -23,6 +24,7 @@ std::atomic<uint64_t> cyc::g_launches{0};
 
 namespace {
 thread_local std::string g_err;
+thread_local int g_parse[3] = {0, 0, 0};  // code, line, col of the last CYC_E_PARSE
 }
 
 [[noreturn]] void cyc::throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
@@ -59,6 +61,11 @@ void ctx_release(cyc_ctx* ctx) {
 }
 }  // namespace
 
+struct cyc_explicit {
+  cyc_ctx* ctx = nullptr;
+  cyc::ExplicitDev g;
+};
+
 struct cyc_graph {
   cyc_ctx* ctx = nullptr;
   int orientation = CYC_TRANSPOSED;
@@ -85,6 +92,14 @@ cyc_status guard(F&& f) {
   } catch (const Error& e) {
     g_err = e.what();
     return e.code;
+  } catch (const cyc::ParseFailure& e) {  // ParseError::what(), errors.cpp:18-22
+    static const char* names[] = {"syntax", "unknown-identifier", "type-mismatch", "duplicate-name",
+                                  "property-restriction", "range"};
+    g_err = std::to_string(e.line) + ":" + std::to_string(e.col) + ": error[" + names[e.code] + "]: " + e.what();
+    g_parse[0] = e.code;
+    g_parse[1] = e.line;
+    g_parse[2] = e.col;
+    return CYC_E_PARSE;
   } catch (const std::bad_alloc&) {
     g_err = "host allocation failed";
     return CYC_E_RESOURCE;
@@ -633,6 +648,125 @@ cyc_status cyc_owcty(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words
       stats->elim_ms = r.elim_ms;
     }
   });
+}
+
+cyc_status cyc_last_parse_error(int* code, int* line, int* col) {
+  if (code) *code = g_parse[0];
+  if (line) *line = g_parse[1];
+  if (col) *col = g_parse[2];
+  return CYC_OK;
+}
+
+cyc_status cyc_explicit_parse(cyc_ctx* ctx, const char* text, uint64_t len, cyc_explicit** out) {
+  return guard([&] {
+    require(ctx && out && (text || !len), CYC_E_CONTRACT, "parse_explicit_graph: null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->s;
+    DevBuf staged;
+    const uint8_t* d = reinterpret_cast<const uint8_t*>(text);
+    if (len && (!is_device_ptr(text) || (reinterpret_cast<uintptr_t>(text) & 15u))) {
+      staged.alloc(len + 16, s);
+      CYC_CUDA(cudaMemcpyAsync(staged.p, text, len, cudaMemcpyDefault, s));
+      d = staged.as<uint8_t>();
+    }
+    auto* e = new cyc_explicit;
+    try {
+      e->ctx = ctx;
+      cyc::parse_explicit_device(d, len, s, e->g);
+      CYC_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    ctx->refs.fetch_add(1);
+    *out = e;
+  });
+}
+
+// Binary layout: "CYCGRAPH", u32 version (1), u32 n, u64 m, u64 accepting
+// words[ceil(n/64)], u32 edges[2m] (src, dst in log order).
+cyc_status cyc_explicit_load_binary(cyc_ctx* ctx, const void* data, uint64_t len, cyc_explicit** out) {
+  return guard([&] {
+    require(ctx && out && data, CYC_E_CONTRACT, "load_binary_graph: null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->s;
+    struct Hdr {
+      char magic[8];
+      uint32_t version, n;
+      uint64_t m;
+    } h;
+    require(len >= sizeof h, CYC_E_CONTRACT, "load_binary_graph: truncated header");
+    CYC_CUDA(cudaMemcpy(&h, data, sizeof h, cudaMemcpyDefault));
+    require(std::memcmp(h.magic, "CYCGRAPH", 8) == 0 && h.version == 1, CYC_E_CONTRACT,
+            "load_binary_graph: not a CYCGRAPH v1 file");
+    const uint64_t nw = ((uint64_t)h.n + 63) / 64;
+    require(len == sizeof h + nw * 8 + h.m * 8, CYC_E_CONTRACT, "load_binary_graph: size does not match header");
+    auto* e = new cyc_explicit;
+    try {
+      e->ctx = ctx;
+      e->g.n = h.n;
+      e->g.m = h.m;
+      e->g.has_words = true;
+      e->g.acc_words.alloc(nw * 8 + 8, s);
+      e->g.edges.alloc(h.m * 8 + 8, s);
+      const char* base = static_cast<const char*>(data) + sizeof h;
+      if (nw) CYC_CUDA(cudaMemcpyAsync(e->g.acc_words.p, base, nw * 8, cudaMemcpyDefault, s));
+      if (h.m) CYC_CUDA(cudaMemcpyAsync(e->g.edges.p, base + nw * 8, h.m * 8, cudaMemcpyDefault, s));
+      cyc::explicit_acc_ids_from_words(e->g, s);
+      CYC_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    ctx->refs.fetch_add(1);
+    *out = e;
+  });
+}
+
+cyc_status cyc_explicit_info(const cyc_explicit* g, uint32_t* n, uint64_t* n_accepting, uint64_t* m) {
+  return guard([&] {
+    require(g, CYC_E_CONTRACT, "null graph");
+    if (n) *n = g->g.n;
+    if (n_accepting) *n_accepting = g->g.n_acc;
+    if (m) *m = g->g.m;
+  });
+}
+
+cyc_status cyc_explicit_export(const cyc_explicit* g, uint32_t* accepting, uint32_t* edges) {
+  return guard([&] {
+    require(g, CYC_E_CONTRACT, "null graph");
+    cudaStream_t s = g->ctx->s;
+    if (accepting && g->g.n_acc) copy_out(accepting, g->g.acc_ids.as<uint32_t>(), g->g.n_acc, s);
+    if (edges && g->g.m) copy_out(edges, g->g.edges.as<uint32_t>(), g->g.m * 2, s);
+    CYC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+cyc_status cyc_explicit_snapshot(cyc_ctx* ctx, const cyc_explicit* eg, int orientation, cyc_graph** out) {
+  return guard([&] {
+    require(ctx && eg && out, CYC_E_CONTRACT, "null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    DevBuf words;
+    cyc::explicit_acc_words(eg->g, ctx->s, words);
+    auto* g = new cyc_graph;
+    try {
+      build_graph(ctx, eg->g.edges.as<uint32_t>(), eg->g.m, eg->g.n, words.as<uint64_t>(), orientation, g);
+      CYC_CUDA(cudaStreamSynchronize(ctx->s));
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    ctx->refs.fetch_add(1);
+    *out = g;
+  });
+}
+
+void cyc_explicit_destroy(cyc_explicit* g) {
+  if (!g) return;
+  cyc_ctx* c = g->ctx;
+  if (c) cudaSetDevice(c->device);
+  delete g;
+  if (c) ctx_release(c);
 }
 
 cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,

@@ -99,6 +99,20 @@ def main():
                               "early": early_rec, "full": full_rec,
                               "final_x_early": fx_e.tolist(), "final_x_full": fx_f.tolist(),
                               "scc_cycle": rs.scc_verdict()})
+    # explicit-graph texts through the reference's parse_explicit_graph
+    import base64
+    sys.path.insert(0, os.path.dirname(HERE))
+    import explicit_cases
+
+    out["explicit"] = []
+    for text in explicit_cases.cases():
+        rec = {"text_b64": base64.b64encode(text).decode()}
+        try:
+            n, acc, e = F.parse_explicit(text)
+            rec["n"], rec["accepting"], rec["edges"] = n, acc.tolist(), e.tolist()
+        except oracle.RefParseError as ex:
+            rec["error"] = str(ex)
+        out["explicit"].append(rec)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)
     np.savez_compressed(os.path.join(HERE, "golden_vectors.npz"), **arrays)

@@ -508,3 +508,75 @@ def test_extend_snapshot_equals_rebuild(eng, R):
     assert s2.col_indices.tolist() == full.col_indices.tolist()
     with pytest.raises(eng.ContractError):
         eng.extend_snapshot(s2, (3, np.zeros((0, 2), np.uint32), [True] * 3))  # vertex prefix shrinks
+
+
+# --------------------------------------------------- explicit-graph ingestion
+def _explicit_same(eng, text, want):
+    """device parse == reference result (dict with n/accepting/edges or error)."""
+    if "error" in want:
+        with pytest.raises(eng.ParseError) as ei:
+            eng.parse_explicit_graph(text)
+        assert str(ei.value) == want["error"]
+        line = int(want["error"].split(":")[0])
+        assert ei.value.line == line and ei.value.col == (0 if line == 0 and "cannot" in want["error"] else 1)
+    else:
+        g = eng.parse_explicit_graph(text)
+        assert (g.n, g.accepting.tolist(), g.edges.tolist()) == (want["n"], want["accepting"], want["edges"])
+
+
+def test_explicit_parse_golden(eng, golden):
+    """parse_explicit_graph on the device reproduces the reference on the
+    committed fixtures: the graph, or the same ParseError text and line."""
+    import base64
+
+    for rec in golden["explicit"]:
+        _explicit_same(eng, base64.b64decode(rec["text_b64"]), rec)
+
+
+def test_explicit_parse_fuzz_and_snapshot(eng, R, REF):
+    import explicit_cases as X
+    import oracle as O
+
+    for text in X.cases(seed=77, count=300):
+        try:
+            n, acc, e = REF.parse_explicit(text)
+            want = {"n": n, "accepting": acc.tolist(), "edges": e.tolist()}
+        except O.RefParseError as ex:
+            want = {"error": str(ex)}
+        _explicit_same(eng, text, want)
+    # a larger file: snapshot through the device parse == reference snapshot
+    rng = np.random.default_rng(5)
+    text, n, acc, edges = X.valid_text(rng, 3000, 20000, 0.05)
+    dg = eng.parse_explicit_device(text)
+    for tr in (True, False):
+        s = dg.snapshot(eng.Orientation.transposed if tr else eng.Orientation.forward)
+        rs = REF.explicit_snapshot(text, tr)
+        c, racc, _ = rs.export()
+        assert np.array_equal(s.row_offsets, c.off) and np.array_equal(s.col_indices, c.col)
+        assert np.array_equal(s.accepting.words()[: len(racc)], racc[: len(s.accepting.words())])
+    # binary round trip feeds the same snapshot
+    g = dg.export()
+    blob = eng.write_binary_graph(g.n, g.edges, eng.Bitset.from_indices(g.n, g.accepting))
+    bg = eng.load_binary_graph(blob)
+    assert (bg.n, bg.m) == (g.n, len(g.edges))
+    b = bg.export()
+    assert np.array_equal(b.edges, g.edges) and b.accepting.tolist() == sorted(set(g.accepting.tolist()))
+    s1, s2 = bg.snapshot(), dg.snapshot()
+    assert np.array_equal(s1.col_indices, s2.col_indices) and np.array_equal(s1.row_offsets, s2.row_offsets)
+    with pytest.raises(eng.ContractError):
+        eng.load_binary_graph(blob[:-4])
+    with pytest.raises(eng.ParseError):
+        eng.load_explicit_graph("/nonexistent/graph.txt")
+
+
+def test_explicit_parse_large(eng, R):
+    """A 2^20-edge file: every id parsed, order kept (device generator log)."""
+    p = eng.preset(1)
+    p.n, p.deg = 1 << 17, 8
+    eng.prepare(p)
+    gn, ge, ga = R.generate(p)
+    acc = np.flatnonzero(np.unpackbits(ga.view(np.uint8), bitorder="little")[:gn])
+    body = "\n".join(f"edge {s} {d}" for s, d in ge.tolist())
+    text = f"graph {gn}\naccepting {' '.join(map(str, acc.tolist()))}\n{body}\n".encode()
+    g = eng.parse_explicit_graph(text)
+    assert g.n == gn and np.array_equal(g.edges, ge) and np.array_equal(g.accepting, acc.astype(np.uint32))

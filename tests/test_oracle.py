@@ -233,6 +233,24 @@ def test_owcty_restatement_vs_reference(R, REF):
     assert R.run_owcty(R.build_snapshot(0, np.zeros((0, 2), np.uint32), False), [])[2] == 0
 
 
+def test_explicit_golden_pinned(REF, golden):
+    # the committed parse_explicit_graph fixtures (graph.cpp:259-297) are what
+    # the compiled reference returns here
+    import base64
+
+    import oracle as O
+
+    for rec in golden["explicit"]:
+        text = base64.b64decode(rec["text_b64"])
+        if "error" in rec:
+            with pytest.raises(O.RefParseError) as ei:
+                REF.parse_explicit(text)
+            assert str(ei.value) == rec["error"]
+        else:
+            n, acc, e = REF.parse_explicit(text)
+            assert (n, acc.tolist(), e.tolist()) == (rec["n"], rec["accepting"], rec["edges"])
+
+
 def test_reference_step_worker_invariance(REF):
     # map_engine.hpp:46-49: bitwise identical for every worker count
     rng = np.random.default_rng(7)
