@@ -580,3 +580,79 @@ def test_explicit_parse_large(eng, R):
     text = f"graph {gn}\naccepting {' '.join(map(str, acc.tolist()))}\n{body}\n".encode()
     g = eng.parse_explicit_graph(text)
     assert g.n == gn and np.array_equal(g.edges, ge) and np.array_equal(g.accepting, acc.astype(np.uint32))
+
+
+# ------------------------------------------- full BASELINE sizes (properties)
+def _device_log(eng, cfg):
+    from paper_0912_2555_b200 import _abi
+
+    p = eng.preset(cfg)
+    ctx = eng.default_context()
+    L, C = _abi.lib(), _abi.C
+    de, da = C.c_void_p(), C.c_void_p()
+    _abi.check(L.cyc_device_alloc(ctx.handle, p.m * 8, C.byref(de)))
+    _abi.check(L.cyc_device_alloc(ctx.handle, ((p.n + 63) // 64) * 8, C.byref(da)))
+    _abi.check(L.cyc_gen_fill(ctx.handle, C.byref(p), de, da))
+    return p, ctx, de, da
+
+
+def _device_snapshot(eng, p, ctx, de, da, orientation):
+    from paper_0912_2555_b200 import _abi
+
+    L, C = _abi.lib(), _abi.C
+    h = C.c_void_p()
+    _abi.check(L.cyc_graph_build(ctx.handle, C.cast(de, C.POINTER(C.c_uint32)), p.m, p.n,
+                                 C.cast(da, C.POINTER(C.c_uint64)), int(orientation), C.byref(h)))
+    return eng.CsrSnapshot(h, ctx)
+
+
+def test_c5_full_size_closed_form(eng):
+    """Config 5 at 2^24: no cycle, one iteration, L*(S/2+2) + S/2 - 1 = 16767
+    steps (the family's closed form, pinned on the CPU by the oracle and the
+    reference); OWCTY and the SCC verdict agree."""
+    from paper_0912_2555_b200 import _abi
+
+    p, ctx, de, da = _device_log(eng, 5)
+    try:
+        s = _device_snapshot(eng, p, ctx, de, da, eng.Orientation.transposed)
+        for mode in MODES:
+            v, st = eng.run_map(s, s.accepting, eng.MapOptions(mode=mode))
+            assert not v.cycle_found()
+            assert (st.iterations, st.kernel_calls) == (1, 64 * 258 + 255), mode
+        assert not eng.run_owcty(s)[0].cycle_found() and not eng.scc_verdict(s).verdict.cycle_found()
+    finally:
+        _abi.lib().cyc_device_free(ctx.handle, de)
+        _abi.lib().cyc_device_free(ctx.handle, da)
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_verdicts_agree(eng, cfg):
+    """Configs 3 (R-MAT 2^26, 2^30 logged edges) and 4 (2^28-state product
+    graph) at full size, where no CPU oracle finishes: MAP (with and without
+    the final-round restriction), OWCTY and the SCC verdict agree; MAP's
+    witness is an accepting vertex of a cyclic SCC; the restricted run maps its
+    witness back to the unrestricted one (the cycle detector's contract)."""
+    from paper_0912_2555_b200 import _abi
+
+    p, ctx, de, da = _device_log(eng, cfg)
+    try:
+        s = _device_snapshot(eng, p, ctx, de, da, eng.Orientation.transposed)
+        ov = eng.scc_verdict(s)
+        cyc_acc = ov.cyclic_accepting
+        assert ov.verdict.cycle_found() and len(cyc_acc) > 0
+        r = eng.restrict_to_accepting_sccs(s)
+        assert np.array_equal(np.intersect1d(r.kept, np.flatnonzero(
+            np.unpackbits(s.accepting.words().view(np.uint8), bitorder="little")[: s.n])), cyc_acc)
+        vr, _ = eng.run_map(r.snapshot, r.snapshot.accepting)
+        w = int(r.kept[vr.witness])
+        assert vr.cycle_found() and w in set(cyc_acc.tolist())
+        if cfg == 3:  # unrestricted MAP on config 4 is MAP's worst case (49 K dense steps)
+            v, _ = eng.run_map(s, s.accepting)
+            assert v.cycle_found() and v.witness in set(cyc_acc.tolist())
+        fwd = _device_snapshot(eng, p, ctx, de, da, eng.Orientation.forward)
+        vo, so = eng.run_owcty(fwd)
+        accb = np.unpackbits(fwd.accepting.words().view(np.uint8), bitorder="little")
+        assert vo.cycle_found() and accb[vo.witness] and so.final_size > 0
+    finally:
+        _abi.lib().cyc_device_free(ctx.handle, de)
+        _abi.lib().cyc_device_free(ctx.handle, da)

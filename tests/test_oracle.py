@@ -251,6 +251,22 @@ def test_explicit_golden_pinned(REF, golden):
             assert (n, acc.tolist(), e.tolist()) == (rec["n"], rec["accepting"], rec["edges"])
 
 
+def test_chain_family_closed_form_oracle(R, REF):
+    # config 5 family: one MAP iteration of exactly L*(S/2+2) + S/2 - 1 steps,
+    # independent of W (derived here on small members, checked against the
+    # reference; pins the full-size GPU test, 64*258 + 255 = 16767)
+    for L, S, W in ((2, 4, 1), (3, 8, 2), (4, 16, 4), (8, 32, 1), (5, 12, 3)):
+        p = R.preset(5)
+        p.L, p.W, p.S = L, W, S
+        R.prepare(p)
+        n, e, a = R.generate(p)
+        r = R.run_map(R.transpose(R.build_snapshot(n, e, True)), a, True)
+        assert (r.iterations, r.kernel_calls, r.cycle) == (1, L * (S // 2 + 2) + S // 2 - 1, False)
+        if L <= 4:
+            rr = REF.snapshot(n, e, a, True).run_map(None, True)
+            assert rr.kernel_calls == r.kernel_calls
+
+
 def test_reference_step_worker_invariance(REF):
     # map_engine.hpp:46-49: bitwise identical for every worker count
     rng = np.random.default_rng(7)
