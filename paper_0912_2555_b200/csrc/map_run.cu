@@ -48,7 +48,7 @@ constexpr int kModePull = 1, kModePush = 2;
 constexpr int kRows = 4;            // rows per lane in a pull step (the ovf test below assumes 4)
 static_assert(kRows == 4, "pull overflow test unrolled for 4 rows");
 constexpr int kBatch = 4;           // frontier vertices per lane in a push step
-constexpr int kHeavyPerLane = 8;    // pull heavy chunk = 256 edges
+constexpr int kHeavyPerLane = kHeavyChunk / 32;  // pull heavy chunk edges per lane
 
 __device__ __forceinline__ bool bit_of(const uint32_t* words, uint32_t v) {
   return (__ldcg(words + (v >> 5)) >> (v & 31u)) & 1u;
@@ -879,7 +879,7 @@ __global__ void k_step_pull(uint32_t n, const uint32_t* __restrict__ goff,
 }
 
 // Sharded dense step over rows [lo, hi). Rows longer than `heavy` start from
-// x[v] here and are finished by k_step_range_chunks (one warp per 256-edge
+// x[v] here and are finished by k_step_range_chunks (one warp per heavy
 // chunk, atomicMax into out) and k_step_range_heavy (their flags).
 __device__ __forceinline__ uint32_t cand_of(uint32_t u, const uint32_t* __restrict__ x,
                                             const uint32_t* __restrict__ accw) {
