@@ -6,7 +6,7 @@
 namespace cyc {
 
 constexpr uint32_t kRowPad = 256;  // row padding of map buffers and the HYB slab
-constexpr uint32_t kHeavyDeg = 256;    // rows longer than this are split into chunks
+constexpr uint32_t kHeavyDeg = 64;     // rows longer than this are split into chunks
 constexpr uint32_t kHeavyChunk = 128;  // edges per heavy chunk (one warp, 4 per lane)
 
 // One CSR on the device. Row offsets are u32 (n+1), columns u32 (m).
