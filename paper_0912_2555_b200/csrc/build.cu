@@ -217,10 +217,8 @@ __global__ void k_sort_small(uint32_t n, const uint32_t* __restrict__ roff,
       ucnt[v] = sort_small_row<16>(seg, d);
     } else if (d <= kWarpRow) {
       wrows[atomicAdd(counts + 2, 1u)] = v;
-    } else if (d <= kMedRow) {
-      med[atomicAdd(counts + 0, 1u)] = v;
     } else {
-      big[atomicAdd(counts + 1, 1u)] = v;
+      med[atomicAdd(counts + 0, 1u)] = v;  // long rows: split sort (sort_long_rows)
     }
   }
 }
@@ -266,27 +264,6 @@ __device__ __forceinline__ void smem_bitonic(uint32_t* s, uint32_t P, int nthrea
   }
 }
 
-__global__ void __launch_bounds__(kMedThreads) k_sort_med(const uint32_t* __restrict__ rows,
-                                                         const uint32_t* __restrict__ counts,
-                                                         const uint32_t* __restrict__ roff,
-                                                         uint32_t* __restrict__ raw,
-                                                         uint32_t* __restrict__ ucnt) {
-  __shared__ uint32_t s[kMedRow];
-  const uint32_t nrows = counts[0];
-  for (uint32_t r = blockIdx.x; r < nrows; r += gridDim.x) {
-    const uint32_t v = rows[r];
-    const uint32_t b = roff[v], d = roff[v + 1] - b;
-    uint32_t P = 1;
-    while (P < d) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += kMedThreads) s[i] = i < d ? raw[b + i] : kNone;
-    __syncthreads();
-    smem_bitonic(s, P, kMedThreads);
-    uint32_t u = block_unique_store<kMedThreads>(s, d, 0, false, raw + b);
-    if (threadIdx.x == 0) ucnt[v] = u;
-    __syncthreads();
-  }
-}
-
 // Hub rows: bitonic network (all-ascending "flip" formulation, so virtual
 // +inf padding beyond d never moves) with every stage whose partner distance
 // is below kBigTile run inside a shared-memory tile.
@@ -320,56 +297,46 @@ __device__ void big_tile_stages(uint32_t* s, uint32_t* g, uint32_t d, uint32_t t
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBigThreads) k_sort_big(const uint32_t* __restrict__ rows,
-                                                         const uint32_t* __restrict__ counts,
-                                                         const uint32_t* __restrict__ roff,
-                                                         uint32_t* __restrict__ raw,
-                                                         uint32_t* __restrict__ ucnt) {
-  __shared__ uint32_t s[kBigTile];
+// Sorts and deduplicates g[0..d) in place with one 1024-thread CTA (bitonic
+// in shared-memory tiles plus global merge stages); returns the unique count.
+__device__ uint32_t cta_sort_unique_global(uint32_t* s, uint32_t* g, uint32_t d) {
   __shared__ uint32_t carry;
-  const uint32_t nrows = counts[1];
-  for (uint32_t r = blockIdx.x; r < nrows; r += gridDim.x) {
-    const uint32_t v = rows[r];
-    const uint32_t b = roff[v], d = roff[v + 1] - b;
-    uint32_t* g = raw + b;
-    uint32_t P = kBigTile;
-    while (P < d) P <<= 1;
-    for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) big_tile_stages(s, g, d, t0, kBigTile, true);
-    for (uint32_t k = kBigTile << 1; k <= P; k <<= 1) {
-      for (uint32_t j = k >> 1; j >= kBigTile; j >>= 1) {
-        const bool flip = j == (k >> 1);
-        for (uint32_t i = threadIdx.x; i < d; i += kBigThreads) {
-          uint32_t p = flip ? (i ^ (k - 1)) : (i ^ j);
-          if (p > i && p < d) {
-            uint32_t x = g[i], y = g[p];
-            if (x > y) {
-              g[i] = y;
-              g[p] = x;
-            }
+  uint32_t P = kBigTile;
+  while (P < d) P <<= 1;
+  for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) big_tile_stages(s, g, d, t0, kBigTile, true);
+  for (uint32_t k = kBigTile << 1; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j >= kBigTile; j >>= 1) {
+      const bool flip = j == (k >> 1);
+      for (uint32_t i = threadIdx.x; i < d; i += kBigThreads) {
+        uint32_t p = flip ? (i ^ (k - 1)) : (i ^ j);
+        if (p > i && p < d) {
+          uint32_t x = g[i], y = g[p];
+          if (x > y) {
+            g[i] = y;
+            g[p] = x;
           }
         }
-        __syncthreads();
       }
-      for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) big_tile_stages(s, g, d, t0, k, false);
+      __syncthreads();
     }
-    // dedup tile by tile (writes never overtake reads: output index <= input index)
-    uint32_t written = 0;
-    if (threadIdx.x == 0) carry = 0;
+    for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) big_tile_stages(s, g, d, t0, k, false);
+  }
+  // dedup tile by tile (writes never overtake reads: output index <= input index)
+  uint32_t written = 0;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) {
+    uint32_t len = min(kBigTile, d - t0);
+    for (uint32_t i = threadIdx.x; i < len; i += kBigThreads) s[i] = g[t0 + i];
     __syncthreads();
-    for (uint32_t t0 = 0; t0 < d; t0 += kBigTile) {
-      uint32_t len = min(kBigTile, d - t0);
-      for (uint32_t i = threadIdx.x; i < len; i += kBigThreads) s[i] = g[t0 + i];
-      __syncthreads();
-      uint32_t prev = carry;
-      __syncthreads();
-      uint32_t u = block_unique_store<kBigThreads>(s, len, prev, t0 > 0, g + written);
-      if (threadIdx.x == 0) carry = s[len - 1];
-      written += u;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) ucnt[v] = written;
+    uint32_t prev = carry;
+    __syncthreads();
+    uint32_t u = block_unique_store<kBigThreads>(s, len, prev, t0 > 0, g + written);
+    if (threadIdx.x == 0) carry = s[len - 1];
+    written += u;
     __syncthreads();
   }
+  return written;
 }
 
 // ------------------------------------------------------------------ compact
@@ -609,6 +576,196 @@ __global__ void k_sort_warp(const uint32_t* __restrict__ rows, const uint32_t* _
   }
 }
 
+// ---------------------------------------------------- long rows: MSD split
+// Rows longer than kWarpRow (R-MAT hubs reach millions of columns) are split
+// by the high bits of (col - row_min) into a power-of-two number of
+// sub-buckets of ~kSubTarget values; each sub-bucket is then sorted and
+// deduplicated by one warp in registers (warp_sort_row), the rare overfull
+// ones by a CTA. Sub-buckets cover disjoint, ordered value ranges, so their
+// concatenation is the sorted unique row. Every pass is spread over all SMs
+// (kSplitChunk-element chunks), where a per-row sort put one hub on one CTA.
+constexpr uint32_t kSubTarget = 256;
+constexpr uint32_t kSplitChunk = 4096;
+constexpr uint32_t kSplitThreads = 1024;
+constexpr uint32_t kSplitBins = 8192;  // shared-memory histogram bins per chunk
+
+__device__ __forceinline__ uint32_t ceil_log2(uint64_t x) {  // smallest b with 2^b >= x
+  return x <= 1 ? 0u : 64u - __clzll(x - 1);
+}
+
+// per long row r: chunk count (SoA: rw[0..n) degrees, rw[n..2n) chunks)
+__global__ void k_split_setup(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cts,
+                              const uint32_t* __restrict__ roff, uint32_t* nch, uint32_t* rmin, uint32_t* rmax) {
+  const uint32_t nr = cts[0];
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
+    const uint32_t v = rows[r];
+    const uint32_t d = roff[v + 1] - roff[v];
+    nch[r] = (d + kSplitChunk - 1) / kSplitChunk;
+    rmin[r] = kNone;
+    rmax[r] = 0;
+  }
+}
+
+__global__ void k_split_desc(const uint32_t* __restrict__ cts, const uint32_t* __restrict__ chbase,
+                             uint2* desc) {
+  const uint32_t nr = cts[0];
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x)
+    for (uint32_t c = chbase[r]; c < chbase[r + 1]; ++c) desc[c] = make_uint2(r, c - chbase[r]);
+}
+
+__global__ void __launch_bounds__(kSplitThreads) k_split_minmax(const uint2* __restrict__ desc, uint32_t nchunks,
+                                                                const uint32_t* __restrict__ rows,
+                                                                const uint32_t* __restrict__ roff,
+                                                                const uint32_t* __restrict__ raw, uint32_t* rmin,
+                                                                uint32_t* rmax) {
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint2 dc = desc[c];
+    const uint32_t v = rows[dc.x];
+    const uint32_t b = roff[v] + dc.y * kSplitChunk, e = min(roff[v + 1], b + kSplitChunk);
+    uint32_t lo = kNone, hi = 0;
+    for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      lo = min(lo, raw[i]);
+      hi = max(hi, raw[i]);
+    }
+    lo = __reduce_min_sync(kFull, lo);
+    hi = __reduce_max_sync(kFull, hi);
+    if ((threadIdx.x & 31u) == 0) {
+      atomicMin(rmin + dc.x, lo);
+      atomicMax(rmax + dc.x, hi);
+    }
+  }
+}
+
+// nsub = next power of two of ceil(d / kSubTarget), capped by the value range
+__global__ void k_split_nsub(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cts,
+                             const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rmin,
+                             const uint32_t* __restrict__ rmax, uint32_t* nsub, uint32_t* shift) {
+  const uint32_t nr = cts[0];
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
+    const uint32_t v = rows[r];
+    const uint32_t d = roff[v + 1] - roff[v];
+    const uint32_t rb = ceil_log2((uint64_t)(rmax[r] - rmin[r]) + 1);  // value-range bits
+    uint32_t sb = ceil_log2((d + kSubTarget - 1) / kSubTarget);
+    if (sb > rb) sb = rb;
+    nsub[r] = 1u << sb;
+    shift[r] = rb - sb;
+  }
+}
+
+template <bool SCATTER>
+__global__ void __launch_bounds__(kSplitThreads) k_split_bins(const uint2* __restrict__ desc, uint32_t nchunks,
+                                                              const uint32_t* __restrict__ rows,
+                                                              const uint32_t* __restrict__ roff,
+                                                              const uint32_t* __restrict__ raw,
+                                                              const uint32_t* __restrict__ rmin,
+                                                              const uint32_t* __restrict__ shift,
+                                                              const uint32_t* __restrict__ nsub,
+                                                              const uint32_t* __restrict__ subbase,
+                                                              uint32_t* cnt_or_cur, uint32_t* tmp) {
+  __shared__ uint32_t h[kSplitBins];
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint2 dc = desc[c];
+    const uint32_t r = dc.x, v = rows[r];
+    const uint32_t b = roff[v] + dc.y * kSplitChunk, e = min(roff[v + 1], b + kSplitChunk);
+    const uint32_t lo = rmin[r], sh = shift[r], ns = nsub[r], sb = subbase[r];
+    if (ns > kSplitBins) {  // very long rows: few elements per bin, global atomics
+      for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const uint32_t x = raw[i];
+        const uint32_t bin = (x - lo) >> sh;
+        if (SCATTER) tmp[atomicAdd(cnt_or_cur + sb + bin, 1u)] = x;
+        else atomicAdd(cnt_or_cur + sb + bin, 1u);
+      }
+      continue;
+    }
+    for (uint32_t k = threadIdx.x; k < ns; k += blockDim.x) h[k] = 0;
+    __syncthreads();
+    for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[(raw[i] - lo) >> sh], 1u);
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < ns; k += blockDim.x) {
+      const uint32_t x = h[k];
+      if (SCATTER) h[k] = x ? atomicAdd(cnt_or_cur + sb + k, x) : 0u;  // reserve: h becomes the base
+      else if (x) atomicAdd(cnt_or_cur + sb + k, x);
+    }
+    __syncthreads();
+    if (SCATTER) {
+      for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const uint32_t x = raw[i];
+        tmp[atomicAdd(&h[(x - lo) >> sh], 1u)] = x;
+      }
+    }
+    __syncthreads();  // h is reused by the next chunk
+  }
+}
+
+// one warp per sub-bucket: sort + dedup in place; overfull ones are listed
+__global__ void k_split_sort(uint32_t S, const uint32_t* __restrict__ soff, uint32_t* tmp, uint32_t* usub,
+                             uint32_t* over, uint32_t* nover) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t sI = gw; sI < S; sI += nw) {
+    const uint32_t b = soff[sI], d = soff[sI + 1] - b;
+    uint32_t u;
+    if (d <= 1) u = d;
+    else if (d <= 64) u = warp_sort_row<2>(tmp + b, d);
+    else if (d <= 128) u = warp_sort_row<4>(tmp + b, d);
+    else if (d <= 256) u = warp_sort_row<8>(tmp + b, d);
+    else if (d <= kWarpRow) u = warp_sort_row<16>(tmp + b, d);
+    else {
+      if ((threadIdx.x & 31u) == 0) over[atomicAdd(nover, 1u)] = sI;
+      continue;
+    }
+    if ((threadIdx.x & 31u) == 0) usub[sI] = u;
+  }
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_split_sort_over(const uint32_t* __restrict__ over,
+                                                                 const uint32_t* __restrict__ nover,
+                                                                 const uint32_t* __restrict__ soff, uint32_t* tmp,
+                                                                 uint32_t* usub) {
+  __shared__ uint32_t s[kBigTile];
+  const uint32_t no = *nover;
+  for (uint32_t k = blockIdx.x; k < no; k += gridDim.x) {
+    const uint32_t sI = over[k];
+    const uint32_t b = soff[sI], d = soff[sI + 1] - b;
+    uint32_t u;
+    if (d <= kBigTile) {
+      uint32_t P = 1;
+      while (P < d) P <<= 1;
+      for (uint32_t i = threadIdx.x; i < P; i += kBigThreads) s[i] = i < d ? tmp[b + i] : kNone;
+      __syncthreads();
+      smem_bitonic(s, P, kBigThreads);
+      u = block_unique_store<kBigThreads>(s, d, 0, false, tmp + b);
+    } else {
+      u = cta_sort_unique_global(s, tmp + b, d);
+    }
+    if (threadIdx.x == 0) usub[sI] = u;
+    __syncthreads();
+  }
+}
+
+// one warp per sub-bucket: unique values to their place in the row
+__global__ void k_split_write(uint32_t S, uint32_t nr, const uint32_t* __restrict__ rows,
+                              const uint32_t* __restrict__ roff, const uint32_t* __restrict__ subbase,
+                              const uint32_t* __restrict__ soff, const uint32_t* __restrict__ uoff,
+                              const uint32_t* __restrict__ tmp, uint32_t* raw, uint32_t* ucnt) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t sI = gw; sI < S; sI += nw) {
+    uint32_t lo = 0, hi = nr;  // row r: subbase[r] <= sI < subbase[r+1]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (subbase[mid] <= sI) lo = mid; else hi = mid;
+    }
+    const uint32_t v = rows[lo];
+    const uint32_t first = uoff[subbase[lo]];
+    const uint32_t u = uoff[sI + 1] - uoff[sI];
+    uint32_t* dst = raw + roff[v] + (uoff[sI] - first);
+    const uint32_t* src = tmp + soff[sI];
+    for (uint32_t i = lane; i < u; i += 32u) dst[i] = src[i];
+    if (sI == subbase[lo] && lane == 0) ucnt[v] = uoff[subbase[lo + 1]] - first;
+  }
+}
+
+
 // per K in {1,2,4,8}: rows longer than K and the edges beyond K
 __global__ void k_ell_hist(uint32_t n, const uint32_t* __restrict__ off,
                            unsigned long long* __restrict__ out /* [8] */) {
@@ -804,6 +961,66 @@ struct PhaseTimer {
   }
 };
 
+// Long rows (list `rows`, count cts[0]): the MSD split sort above.
+static void sort_long_rows(const uint32_t* rows, const uint32_t* cts, const uint32_t* roff, uint32_t* raw,
+                           uint32_t* ucnt, cudaStream_t s, BuildArena& ar) {
+  uint32_t nr = 0;
+  CYC_CUDA(cudaMemcpyAsync(&nr, cts, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  if (!nr) return;
+  DevBuf& scratch = ar.scratch;
+  // per-row arrays: nch, chbase, rmin, rmax, nsub, shift, subbase, (misc)
+  uint32_t* rw = ar.get<uint32_t>(ar.sp_row, ((size_t)nr + 2) * 4 * 8, s);
+  const size_t R = (size_t)nr + 2;
+  uint32_t *nch = rw, *chbase = rw + R, *rmin = rw + 2 * R, *rmax = rw + 3 * R, *nsub = rw + 4 * R,
+           *shift = rw + 5 * R, *subbase = rw + 6 * R, *misc = rw + 7 * R;
+  const uint32_t g = grid_for(nr, 256, 8);
+  k_split_setup<<<g, 256, 0, s>>>(rows, cts, roff, nch, rmin, rmax);
+  CYC_LAUNCHED();
+  exclusive_scan(nch, chbase, nr, nullptr, s, scratch);
+  uint32_t hdr[2] = {0, 0};  // chunks, elements
+  CYC_CUDA(cudaMemcpyAsync(&hdr[0], chbase + nr, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  const uint32_t C = hdr[0];
+  uint2* desc = ar.get<uint2>(ar.sp_desc, ((size_t)C + 1) * 8, s);
+  k_split_desc<<<g, 256, 0, s>>>(cts, chbase, desc);
+  CYC_LAUNCHED();
+  const uint32_t gc = std::min<uint32_t>(C, sm_count() * 2);
+  k_split_minmax<<<gc, kSplitThreads, 0, s>>>(desc, C, rows, roff, raw, rmin, rmax);
+  CYC_LAUNCHED();
+  k_split_nsub<<<g, 256, 0, s>>>(rows, cts, roff, rmin, rmax, nsub, shift);
+  CYC_LAUNCHED();
+  exclusive_scan(nsub, subbase, nr, nullptr, s, scratch);
+  uint32_t S = 0;
+  CYC_CUDA(cudaMemcpyAsync(&S, subbase + nr, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  // per-sub arrays: cnt/cursor, soff, usub, uoff, over list
+  uint32_t* sw = ar.get<uint32_t>(ar.sp_sub, ((size_t)S + 2) * 4 * 5, s);
+  const size_t SS = (size_t)S + 2;
+  uint32_t *cnt = sw, *soff = sw + SS, *usub = sw + 2 * SS, *uoff = sw + 3 * SS, *over = sw + 4 * SS;
+  CYC_CUDA(cudaMemsetAsync(cnt, 0, SS * 4, s));
+  CYC_CUDA(cudaMemsetAsync(misc, 0, 8, s));
+  k_split_bins<false><<<gc, kSplitThreads, 0, s>>>(desc, C, rows, roff, raw, rmin, shift, nsub, subbase, cnt,
+                                                   nullptr);
+  CYC_LAUNCHED();
+  exclusive_scan(cnt, soff, S, nullptr, s, scratch);
+  uint32_t E = 0;
+  CYC_CUDA(cudaMemcpyAsync(&E, soff + S, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaMemcpyAsync(cnt, soff, (size_t)S * 4, cudaMemcpyDeviceToDevice, s));  // cursors
+  CYC_CUDA(cudaStreamSynchronize(s));
+  uint32_t* tmp = ar.get<uint32_t>(ar.sp_tmp, ((size_t)E + 1) * 4, s);
+  k_split_bins<true><<<gc, kSplitThreads, 0, s>>>(desc, C, rows, roff, raw, rmin, shift, nsub, subbase, cnt, tmp);
+  CYC_LAUNCHED();
+  k_split_sort<<<grid_for((uint64_t)S * 32, 256, 8), 256, 0, s>>>(S, soff, tmp, usub, over, misc);
+  CYC_LAUNCHED();
+  k_split_sort_over<<<sm_count(), kBigThreads, 0, s>>>(over, misc, soff, tmp, usub);
+  CYC_LAUNCHED();
+  exclusive_scan(usub, uoff, S, nullptr, s, scratch);
+  k_split_write<<<grid_for((uint64_t)S * 32, 256, 8), 256, 0, s>>>(S, nr, rows, roff, subbase, soff, uoff, tmp,
+                                                                   raw, ucnt);
+  CYC_LAUNCHED();
+}
+
 void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
                DevCsr& out, uint32_t* d_err, BuildArena& ar) {
   PhaseTimer pt(s);
@@ -832,12 +1049,7 @@ void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst,
     k_sort_warp<<<sm_count() * 8, 256, 0, s>>>(wrows, cts, roff.as<uint32_t>(), raw.as<uint32_t>(),
                                                ucnt.as<uint32_t>());
     CYC_LAUNCHED();
-    k_sort_med<<<sm_count() * 8, kMedThreads, 0, s>>>(med, cts, roff.as<uint32_t>(),
-                                                       raw.as<uint32_t>(), ucnt.as<uint32_t>());
-    CYC_LAUNCHED();
-    k_sort_big<<<sm_count(), kBigThreads, 0, s>>>(big, cts, roff.as<uint32_t>(), raw.as<uint32_t>(),
-                                                  ucnt.as<uint32_t>());
-    CYC_LAUNCHED();
+    sort_long_rows(med, cts, roff.as<uint32_t>(), raw.as<uint32_t>(), ucnt.as<uint32_t>(), s, ar);
   }
   pt.mark("row_sort");
   exclusive_scan(ucnt.as<uint32_t>(), out.off.as<uint32_t>(), n, nullptr, s, scratch);
