@@ -340,15 +340,38 @@ __device__ uint32_t cta_sort_unique_global(uint32_t* s, uint32_t* g, uint32_t d)
 }
 
 // ------------------------------------------------------------------ compact
-__global__ void k_compact_small(uint32_t n, const uint32_t* __restrict__ roff,
-                                const uint32_t* __restrict__ off,
-                                const uint32_t* __restrict__ raw, uint32_t* __restrict__ col) {
+// Rows of raw degree <= kWarpRow: one warp per 32 consecutive rows walks the
+// concatenation of their unique prefixes 32 values per round, so the writes
+// (a contiguous range of col) and the reads are coalesced.
+__global__ void k_compact_rows(uint32_t n, const uint32_t* __restrict__ roff, const uint32_t* __restrict__ off,
+                               const uint32_t* __restrict__ raw, uint32_t* __restrict__ col) {
+  const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-    uint32_t b = roff[v], d = roff[v + 1] - b;
-    if (d > kSmallRow) continue;
-    uint32_t o = off[v], u = off[v + 1] - o;
-    for (uint32_t i = 0; i < u; ++i) col[o + i] = raw[b + i];
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane;
+    uint32_t src = 0, dst = 0, u = 0;
+    if (v < n && roff[v + 1] - roff[v] <= kWarpRow) {  // longer rows: k_compact_list
+      src = roff[v];
+      dst = off[v];
+      u = off[v + 1] - dst;
+    }
+    const uint32_t incl = warp_incl_scan(u);
+    const uint32_t excl = incl - u;
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    for (uint32_t r = 0; r < total; r += 32u) {
+      const uint32_t e = r + lane;
+      uint32_t owner = 0;
+#pragma unroll
+      for (uint32_t step = 16; step >= 1; step >>= 1) {
+        const uint32_t cand = owner + step;
+        const uint32_t ex = __shfl_sync(kFull, excl, cand & 31u);
+        if (cand < 32u && ex <= e) owner = cand;
+      }
+      const uint32_t os = __shfl_sync(kFull, src, owner);
+      const uint32_t od = __shfl_sync(kFull, dst, owner);
+      const uint32_t oe = __shfl_sync(kFull, excl, owner);
+      if (e < total) col[od + (e - oe)] = raw[os + (e - oe)];
+    }
   }
 }
 
@@ -417,34 +440,72 @@ __global__ void __launch_bounds__(kPartThreads) k_bucket_hist(const uint2* __res
     if (h[b]) atomicAdd(bcnt + b, h[b]);
 }
 
-__global__ void __launch_bounds__(kPartThreads) k_bucket_scatter(const uint2* __restrict__ edges, uint64_t m,
-                                                                 uint32_t n, int key_dst, uint32_t sh,
-                                                                 uint32_t nb, uint64_t per_block,
-                                                                 uint32_t* __restrict__ bcur,
-                                                                 unsigned long long* __restrict__ tmp) {
-  extern __shared__ uint32_t h[];  // [0, nb): counts then cursors, [nb, 2nb): bases
-  uint32_t* base = h + nb;
-  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  const uint64_t lo = blockIdx.x * per_block, hi = min(m, lo + per_block);
-  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const uint2 e = edges[i];
-    if (e.x < n && e.y < n) atomicAdd(&h[(key_dst ? e.y : e.x) >> sh], 1u);
+// Two-pass partition: pass 1 to super-buckets of 2^kSuperLog buckets, pass
+// 2 from super-bucket order to bucket order. A single high-radix pass wrote
+// to nb x blocks interleaved streams (4096 x 296 on config 3): L2 lines were
+// evicted half-written, costing ~3x the payload in DRAM traffic. Each block
+// works on kSubChunk-element sub-chunks (histogram, one reservation per bin,
+// scatter) so the second read of a sub-chunk hits L2 and every bin receives a
+// contiguous run.
+constexpr uint32_t kSuperLog = 6;
+constexpr uint32_t kSubChunk = 16384;
+
+template <bool FROM_EDGES>
+__global__ void __launch_bounds__(kPartThreads) k_part(const void* __restrict__ in, uint64_t m, uint32_t n,
+                                                       int key_dst, uint32_t shift, uint32_t nbins,
+                                                       uint32_t* __restrict__ cursor,
+                                                       unsigned long long* __restrict__ out) {
+  // each thread keeps its kPer elements of the sub-chunk in registers between
+  // the histogram and the scatter (16 independent loads in flight, one read)
+  constexpr uint32_t kPer = kSubChunk / kPartThreads;
+  extern __shared__ uint32_t h[];
+  const uint64_t nsub = (m + kSubChunk - 1) / kSubChunk;
+  for (uint64_t c = blockIdx.x; c < nsub; c += gridDim.x) {
+    const uint64_t lo = c * kSubChunk, hi = min(m, lo + kSubChunk);
+    // pass 2 input is in super-bucket order: only the bins of the super-buckets
+    // between the sub-chunk's first and last element can occur
+    uint32_t b0 = 0, b1 = nbins;
+    if (!FROM_EDGES) {
+      const unsigned long long* t = reinterpret_cast<const unsigned long long*>(in);
+      b0 = (((uint32_t)(t[lo] >> 32) >> shift) >> kSuperLog) << kSuperLog;
+      b1 = min(nbins, ((((uint32_t)(t[hi - 1] >> 32) >> shift) >> kSuperLog) + 1) << kSuperLog);
+    }
+    for (uint32_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) h[b - b0] = 0;
+    unsigned long long v[kPer];
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint64_t i = lo + k * kPartThreads + threadIdx.x;
+      v[k] = ~0ull;  // invalid / past the end
+      if (i < hi) {
+        if (FROM_EDGES) {
+          const uint2 e = reinterpret_cast<const uint2*>(in)[i];
+          const uint32_t row = key_dst ? e.y : e.x, other = key_dst ? e.x : e.y;
+          if (e.x < n && e.y < n) v[k] = ((unsigned long long)row << 32) | other;
+        } else {
+          v[k] = reinterpret_cast<const unsigned long long*>(in)[i];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k)
+      if (v[k] != ~0ull) atomicAdd(&h[((uint32_t)(v[k] >> 32) >> shift) - b0], 1u);
+    __syncthreads();
+    for (uint32_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+      const uint32_t x = h[b - b0];
+      h[b - b0] = x ? atomicAdd(cursor + b, x) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k)
+      if (v[k] != ~0ull) out[atomicAdd(&h[((uint32_t)(v[k] >> 32) >> shift) - b0], 1u)] = v[k];
+    __syncthreads();
   }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
-    base[b] = h[b] ? atomicAdd(bcur + b, h[b]) : 0u;
-    h[b] = 0;
-  }
-  __syncthreads();
-  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const uint2 e = edges[i];
-    if (e.x >= n || e.y >= n) continue;
-    const uint32_t row = key_dst ? e.y : e.x, other = key_dst ? e.x : e.y;
-    const uint32_t b = row >> sh;
-    const uint32_t pos = base[b] + atomicAdd(&h[b], 1u);
-    tmp[pos] = ((unsigned long long)row << 32) | other;
-  }
+}
+
+__global__ void k_super_cursors(const uint32_t* __restrict__ bbase, uint32_t nb, uint32_t ns, uint32_t* cur) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x)
+    cur[s] = bbase[min(nb, s << kSuperLog)];
 }
 
 __global__ void __launch_bounds__(kPartThreads) k_bucket_rows(const unsigned long long* __restrict__ tmp,
@@ -897,7 +958,8 @@ static void count_sort_rows(const uint2* e2, uint64_t m_log, uint32_t n, int key
     static bool attr = false;
     if (!attr) {
       CYC_CUDA(cudaFuncSetAttribute(k_bucket_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-      CYC_CUDA(cudaFuncSetAttribute(k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+      CYC_CUDA(cudaFuncSetAttribute(k_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      CYC_CUDA(cudaFuncSetAttribute(k_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       CYC_CUDA(cudaFuncSetAttribute(k_bucket_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       attr = true;
     }
@@ -912,9 +974,19 @@ static void count_sort_rows(const uint2* e2, uint64_t m_log, uint32_t n, int key
                                                        bcnt, d_err);
     CYC_LAUNCHED();
     exclusive_scan(bcnt, bbase, nb, nullptr, s, scratch);
+    // pass 1: log -> super-bucket order (tmp2); pass 2: -> bucket order (tmp)
+    const uint32_t ns = (nb + (1u << kSuperLog) - 1) >> kSuperLog;
+    unsigned long long* tmp2 = ar.get<unsigned long long>(ar.tmp2, m_log * 8, s);
+    k_super_cursors<<<grid_for(ns, 256, 4), 256, 0, s>>>(bbase, nb, ns, bcur);
+    CYC_LAUNCHED();
+    const uint32_t pblocks = (uint32_t)std::min<uint64_t>((uint64_t)sm_count() * 2, (m_log + kSubChunk - 1) / kSubChunk);
+    k_part<true><<<pblocks, kPartThreads, ns * 4, s>>>(e2, m_log, n, key_dst, sh + kSuperLog, ns, bcur, tmp2);
+    CYC_LAUNCHED();
     CYC_CUDA(cudaMemcpyAsync(bcur, bbase, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
-    k_bucket_scatter<<<blocks, kPartThreads, nb * 8, s>>>(e2, m_log, n, key_dst, sh, nb, per_block,
-                                                          bcur, tmp);
+    uint32_t m_ok = 0;  // valid logged edges (invalid ones were counted nowhere)
+    CYC_CUDA(cudaMemcpyAsync(&m_ok, bbase + nb, 4, cudaMemcpyDeviceToHost, s));
+    CYC_CUDA(cudaStreamSynchronize(s));
+    k_part<false><<<pblocks, kPartThreads, nb * 4, s>>>(tmp2, m_ok, n, key_dst, sh, nb, bcur, tmp);
     CYC_LAUNCHED();
     k_bucket_rows<<<std::min<uint32_t>(nb, sm_count() * 2), kPartThreads, (1u << sh) * 4, s>>>(
         tmp, bbase, n, sh, nb, roff, raw);
@@ -1059,16 +1131,12 @@ void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst,
   out.m = m;
   out.col.alloc((m ? m : 1) * 4ull, s);
   if (n) {
-    k_compact_small<<<grid_for(n, 256, 16), 256, 0, s>>>(n, roff.as<uint32_t>(), out.off.as<uint32_t>(),
-                                                         raw.as<uint32_t>(), out.col.as<uint32_t>());
+    k_compact_rows<<<grid_for(n, 256, 16), 256, 0, s>>>(n, roff.as<uint32_t>(), out.off.as<uint32_t>(),
+                                                        raw.as<uint32_t>(), out.col.as<uint32_t>());
     CYC_LAUNCHED();
-    for (int li = 0; li < 3; ++li) {
-      const uint32_t* lst = li == 0 ? med : li == 1 ? big : wrows;
-      k_compact_list<<<sm_count() * 4, 256, 0, s>>>(lst, cts + li, roff.as<uint32_t>(),
-                                                    out.off.as<uint32_t>(), raw.as<uint32_t>(),
-                                                    out.col.as<uint32_t>());
-      CYC_LAUNCHED();
-    }
+    k_compact_list<<<sm_count() * 4, 256, 0, s>>>(med, cts, roff.as<uint32_t>(), out.off.as<uint32_t>(),
+                                                  raw.as<uint32_t>(), out.col.as<uint32_t>());
+    CYC_LAUNCHED();
   }
   pt.mark("compact");
 }

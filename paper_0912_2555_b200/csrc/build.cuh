@@ -31,7 +31,7 @@ struct DevCsr {
 // Grow-only build temporaries owned by a context and reused by every build
 // (pool allocations of several GB per build cost up to ~1 s of mapping).
 struct BuildArena {
-  DevBuf tmp, raw, roff, ucnt, lists, counts, bcnt, bbase, bcur, scratch;
+  DevBuf tmp, tmp2, raw, roff, ucnt, lists, counts, bcnt, bbase, bcur, scratch;
   DevBuf sp_row, sp_sub, sp_desc, sp_tmp;  // long-row split sort
   template <class T>
   T* get(DevBuf& b, size_t bytes, cudaStream_t s) {
