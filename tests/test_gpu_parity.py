@@ -656,3 +656,27 @@ def test_full_size_verdicts_agree(eng, cfg):
     finally:
         _abi.lib().cyc_device_free(ctx.handle, de)
         _abi.lib().cyc_device_free(ctx.handle, da)
+
+
+def test_build_long_rows_edge_cases(eng, R):
+    """K1's long-row split sort (rows > 512): heavy duplication (one value
+    range collapsing into an overfull sub-bucket, CTA and global fallbacks),
+    narrow consecutive column ranges, and wide random ranges, in both CSRs."""
+    rng = np.random.default_rng(31)
+    n = 50000
+    parts = [rng.integers(0, n, size=(60000, 2))]
+    parts.append(np.stack([np.full(9000, 7), rng.integers(0, 3, size=9000)], 1))        # 9000 dups of 3 values
+    parts.append(np.stack([np.full(6000, 11), np.full(6000, 12)], 1))                    # one value x 6000
+    parts.append(np.stack([np.full(5000, 13), 20000 + np.arange(5000) % 2500], 1))       # narrow range, 2 copies
+    parts.append(np.stack([np.full(70000, 17), rng.integers(0, n, size=70000)], 1))      # wide hub
+    parts.append(np.stack([rng.integers(0, n, size=20000), np.full(20000, 19)], 1))      # hub in the other CSR
+    e = np.concatenate(parts).astype(np.uint32)
+    e = e[rng.permutation(len(e))]
+    acc = rng.random(n) < 0.05
+    for tr in (True, False):
+        s = snap_of(eng, n, e, acc, tr)
+        g = R.build_snapshot(n, e, tr)
+        assert np.array_equal(s.row_offsets, g.off) and np.array_equal(s.col_indices, g.col)
+        off, col = s.gather_index()
+        gt = R.transpose(g)
+        assert np.array_equal(off, gt.off) and np.array_equal(col, gt.col)
