@@ -216,7 +216,7 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   CYC_CUDA(cudaStreamSynchronize(s));
   require(herr == 0, CYC_E_CONTRACT, "build_snapshot: edge endpoint >= n (not interned)");
   require(g->snap.m == g->gath.m, CYC_E_CUDA, "internal: snapshot/gather edge counts differ");
-  cyc::build_heavy(g->gath, cyc::kHeavyDeg, cyc::kHeavyChunk, s);
+  cyc::build_heavy(g->gath, cyc::kHeavyDeg, cyc::kHeavyChunk, s, cyc::pull_col_blocks(g->gath.n));
   cyc::build_heavy(g->snap, cyc::kHeavyDeg, cyc::kHeavyChunk, s);
   cyc::build_ell(g->gath, s);
   load_acc(acc_words, n, g->acc, s);
@@ -405,7 +405,7 @@ cyc_status cyc_graph_extend(cyc_ctx* ctx, const cyc_graph* prev, const uint32_t*
       cyc::merge_csr(prev->snap, delta.snap, n, s, g->snap);
       cyc::merge_csr(prev->gath, delta.gath, n, s, g->gath);
       require(g->snap.m == g->gath.m, CYC_E_CUDA, "internal: snapshot/gather edge counts differ");
-      cyc::build_heavy(g->gath, cyc::kHeavyDeg, cyc::kHeavyChunk, s);
+      cyc::build_heavy(g->gath, cyc::kHeavyDeg, cyc::kHeavyChunk, s, cyc::pull_col_blocks(g->gath.n));
       cyc::build_heavy(g->snap, cyc::kHeavyDeg, cyc::kHeavyChunk, s);
       cyc::build_ell(g->gath, s);
       if (acc_words) {
@@ -444,7 +444,7 @@ cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out
       g->restricted = 1;
       cyc::restrict_graph(in->snap, in->gath, in->acc.as<uint64_t>(), ctx->s, g->snap, g->gath,
                           g->acc, g->kept);
-      cyc::build_heavy(g->gath, cyc::kHeavyDeg, cyc::kHeavyChunk, ctx->s);
+      cyc::build_heavy(g->gath, cyc::kHeavyDeg, cyc::kHeavyChunk, ctx->s, cyc::pull_col_blocks(g->gath.n));
       cyc::build_heavy(g->snap, cyc::kHeavyDeg, cyc::kHeavyChunk, ctx->s);
       cyc::build_ell(g->gath, ctx->s);
     } catch (...) {
@@ -788,7 +788,7 @@ cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32
       restricted.restricted = 1;
       cyc::restrict_graph(base.snap, base.gath, base.acc.as<uint64_t>(), ctx->s, restricted.snap,
                           restricted.gath, restricted.acc, restricted.kept);
-      cyc::build_heavy(restricted.gath, cyc::kHeavyDeg, cyc::kHeavyChunk, ctx->s);
+      cyc::build_heavy(restricted.gath, cyc::kHeavyDeg, cyc::kHeavyChunk, ctx->s, cyc::pull_col_blocks(restricted.gath.n));
       cyc::build_heavy(restricted.snap, cyc::kHeavyDeg, cyc::kHeavyChunk, ctx->s);
       cyc::build_ell(restricted.gath, ctx->s);
       run_on = &restricted;

@@ -14,6 +14,7 @@
 // Row offsets are u32 (snapshot edges < 2^32; checked by the caller).
 #include <algorithm>
 #include <chrono>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
@@ -397,6 +398,49 @@ __global__ void k_heavy_chunks(uint32_t n, const uint32_t* __restrict__ off, uin
     for (uint32_t c = 0; c < nc; ++c) {
       uint32_t cb = b + c * chunk;
       out[base + c] = make_uint4(v, cb, min(e, cb + chunk), 0u);
+    }
+  }
+}
+
+// Heavy rows split at column-block boundaries (cols are sorted, so each
+// block's part of a row is one range), chunks grouped by column block: the
+// pull pass walks the list in order, so at any time all warps gather from one
+// L2-sized slice of the map vector (config 3: 268 MB vector, 126 MB L2).
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* p, uint32_t len, uint32_t x) {
+  uint32_t lo = 0, hi = len;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_heavy_blocks(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                               uint32_t heavy, uint32_t chunk, uint32_t ncb, uint32_t width,
+                               uint32_t* __restrict__ bcount, uint32_t* __restrict__ bcur, uint4* __restrict__ out) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const uint32_t b = off[v], e = off[v + 1];
+    if (e - b <= heavy) continue;
+    uint32_t lo = 0;
+    for (uint32_t j = 0; j < ncb; ++j) {
+      const uint64_t bound = (uint64_t)(j + 1) * width;
+      const uint32_t hi = j + 1 == ncb || bound > 0xFFFFFFFFull
+                              ? e - b
+                              : lo + lower_bound_u32(col + b + lo, e - b - lo, (uint32_t)bound);
+      const uint32_t nc = (hi - lo + chunk - 1) / chunk;
+      if (nc) {
+        if (!out) {
+          atomicAdd(bcount + j, nc);
+        } else {
+          const uint32_t base = atomicAdd(bcur + j, nc);
+          for (uint32_t c = 0; c < nc; ++c) {
+            const uint32_t cb = b + lo + c * chunk;
+            out[base + c] = make_uint4(v, cb, min(b + hi, cb + chunk), 0u);
+          }
+        }
+      }
+      lo = hi;
     }
   }
 }
@@ -1141,15 +1185,36 @@ void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst,
   pt.mark("compact");
 }
 
-void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s) {
-  uint64_t cap = g.m / chunk + g.m / (heavy ? heavy : 1) + 2;
+void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s, uint32_t col_blocks) {
+  const uint32_t ncb = col_blocks ? col_blocks : 1;
+  uint64_t cap = g.m / chunk + (g.m / (heavy ? heavy : 1) + 1) * ncb + 2;
   g.heavy.alloc(cap * sizeof(uint4), s);
   DevBuf cnt(8, s);
   CYC_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
-  if (g.n) {
+  if (g.n && ncb == 1) {
     k_heavy_chunks<<<grid_for(g.n, 256, 16), 256, 0, s>>>(g.n, g.off.as<uint32_t>(), heavy, chunk,
                                                           g.heavy.as<uint4>(), cnt.as<uint32_t>());
     CYC_LAUNCHED();
+  } else if (g.n) {
+    const uint32_t width = (uint32_t)(((uint64_t)g.n + ncb - 1) / ncb);
+    DevBuf bc((size_t)(2 * ncb + 2) * 4, s);
+    CYC_CUDA(cudaMemsetAsync(bc.p, 0, (size_t)(2 * ncb + 2) * 4, s));
+    uint32_t* bcount = bc.as<uint32_t>();
+    uint32_t* bcur = bcount + ncb + 1;
+    k_heavy_blocks<<<grid_for(g.n, 256, 16), 256, 0, s>>>(g.n, g.o(), g.c(), heavy, chunk, ncb, width, bcount,
+                                                          nullptr, nullptr);
+    CYC_LAUNCHED();
+    std::vector<uint32_t> hc(ncb), hb(ncb + 1, 0);
+    CYC_CUDA(cudaMemcpyAsync(hc.data(), bcount, ncb * 4, cudaMemcpyDeviceToHost, s));
+    CYC_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t j = 0; j < ncb; ++j) hb[j + 1] = hb[j] + hc[j];
+    CYC_CUDA(cudaMemcpyAsync(bcur, hb.data(), ncb * 4, cudaMemcpyHostToDevice, s));
+    CYC_CUDA(cudaMemcpyAsync(cnt.p, &hb[ncb], 4, cudaMemcpyHostToDevice, s));
+    k_heavy_blocks<<<grid_for(g.n, 256, 16), 256, 0, s>>>(g.n, g.o(), g.c(), heavy, chunk, ncb, width, nullptr,
+                                                          bcur, g.heavy.as<uint4>());
+    CYC_LAUNCHED();
+  }
+  if (g.n) {
     k_max_degree<<<grid_for(g.n, 256, 8), 256, 0, s>>>(g.n, g.off.as<uint32_t>(),
                                                        cnt.as<uint32_t>() + 1);
     CYC_LAUNCHED();
@@ -1160,6 +1225,14 @@ void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s) {
   g.n_heavy_chunks = h[0];
   g.max_degree = h[1];
   g.heavy_deg = heavy;
+}
+
+uint32_t pull_col_blocks(uint32_t n) {
+  // keep each column block's slice of the map vector (4 B per vertex) within
+  // ~48 MB of the 126 MB L2, leaving room for the streamed CSR data
+  const uint64_t bytes = (uint64_t)n * 4;
+  const uint64_t budget = 48ull << 20;
+  return bytes <= 2 * budget ? 1u : (uint32_t)((bytes + budget - 1) / budget);
 }
 
 }  // namespace cyc

@@ -46,7 +46,11 @@ void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* tot
                     cudaStream_t s, DevBuf& scratch);
 void build_csr(const uint32_t* d_edges, uint64_t m_log, uint32_t n, int key_dst, cudaStream_t s,
                DevCsr& out, uint32_t* d_err, BuildArena& ar);
-void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s);
+// col_blocks > 1: chunks split at column-block boundaries and grouped by block
+// (pull gathers stay within an L2-sized slice of the map vector).
+void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s, uint32_t col_blocks = 1);
+// Column blocks for the pull side of an n-vertex graph (1 when the map fits L2).
+uint32_t pull_col_blocks(uint32_t n);
 // Chooses ell_k in {1,2,4,8} minimising per-step pull bytes and builds the slab.
 void build_ell(DevCsr& g, cudaStream_t s);
 

@@ -49,6 +49,7 @@ constexpr int kRows = 4;            // rows per lane in a pull step (the ovf tes
 static_assert(kRows == 4, "pull overflow test unrolled for 4 rows");
 constexpr int kBatch = 4;           // frontier vertices per lane in a push step
 constexpr int kHeavyPerLane = kHeavyChunk / 32;  // pull heavy chunk edges per lane
+constexpr int kHeavyBatch = 4;                     // heavy chunks in flight per warp
 
 __device__ __forceinline__ bool bit_of(const uint32_t* words, uint32_t v) {
   return (__ldcg(words + (v >> 5)) >> (v & 31u)) & 1u;
@@ -415,34 +416,58 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
-  // heavy rows first (they are the long poles): one warp per chunk of at
-  // most 32*kHeavyPerLane edges, every lane issuing all its loads at once;
-  // combined with atomicMax into Q (Q holds x_{k-2}, never larger)
-  for (uint32_t c = nw - 1u - gw; c < a.n_heavy; c += nw) {  // tail warps do fewer light rows
-    const uint4 ch = a.heavy[c];
-    const uint32_t v = ch.x;
-    uint32_t u[kHeavyPerLane];
+  // heavy rows first (they are the long poles): a warp takes kHeavyBatch
+  // chunks of at most 32*kHeavyPerLane edges at once, every lane issuing all
+  // its loads together; lane k finalises chunk k (own value prefetched) with
+  // an atomicMax into Q (Q holds x_{k-2}, never larger)
+  for (uint32_t c0 = nw - 1u - gw; c0 < a.n_heavy; c0 += nw * kHeavyBatch) {  // tail warps do fewer light rows
+    uint4 ch[kHeavyBatch];
 #pragma unroll
-    for (int r = 0; r < kHeavyPerLane; ++r) {
-      const uint32_t i = ch.y + lane + 32u * r;
-      u[r] = i < ch.z ? __ldg(a.gcol + i) : kNone;
+    for (int k = 0; k < kHeavyBatch; ++k) {
+      const uint32_t c = c0 + (uint32_t)k * nw;
+      ch[k] = c < a.n_heavy ? a.heavy[c] : make_uint4(0u, 0u, 0u, 0u);
     }
-    uint32_t best = 0;
+    uint32_t own = 0;
 #pragma unroll
-    for (int r = 0; r < kHeavyPerLane; ++r)
-      if (u[r] != kNone) best = max(best, cand_of(__ldca(P + u[r]), u[r]));
-    best = __reduce_max_sync(kFull, best);
-    if (lane == 0) {
-      const uint32_t own = __ldca(P + v);
-      best = max(best, own & kCode);
-      atomicMax(Q + v, (own & kFlag) | best);
-      if (best > (own & kCode)) {
+    for (int k = 0; k < kHeavyBatch; ++k)
+      if (lane == (uint32_t)k && ch[k].z > ch[k].y) own = __ldca(P + ch[k].x);
+    uint32_t u[kHeavyBatch][kHeavyPerLane];
+#pragma unroll
+    for (int k = 0; k < kHeavyBatch; ++k)
+#pragma unroll
+      for (int r = 0; r < kHeavyPerLane; ++r) {
+        const uint32_t i = ch[k].y + lane + 32u * r;
+        u[k][r] = i < ch[k].z ? __ldg(a.gcol + i) : kNone;
+      }
+    uint32_t best[kHeavyBatch];
+#pragma unroll
+    for (int k = 0; k < kHeavyBatch; ++k) {
+      best[k] = 0;
+#pragma unroll
+      for (int r = 0; r < kHeavyPerLane; ++r)
+        if (u[k][r] != kNone) best[k] = max(best[k], cand_of(__ldca(P + u[k][r]), u[k][r]));
+    }
+#pragma unroll
+    for (int k = 0; k < kHeavyBatch; ++k) best[k] = __reduce_max_sync(kFull, best[k]);
+    uint32_t mine = 0, v = 0;
+    bool live = false;
+#pragma unroll
+    for (int k = 0; k < kHeavyBatch; ++k)
+      if (lane == (uint32_t)k) {
+        mine = best[k];
+        v = ch[k].x;
+        live = ch[k].z > ch[k].y;
+      }
+    if (live) {
+      mine = max(mine, own & kCode);
+      atomicMax(Q + v, (own & kFlag) | mine);
+      if (mine > (own & kCode)) {
         ++acc.raised;
         if (mark(fb, sh, v)) {
           ++acc.first;
           if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
         }
-        if ((own & kFlag) && best == v + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
+        if ((own & kFlag) && mine == v + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
       }
     }
   }
