@@ -198,8 +198,11 @@ __device__ void step_flags(const RunArgs& a, const StepAcc& acc, SlotCtl* sl, Bl
 }
 
 // Sets bit v of the frontier bitmap (and its summary bit); true iff new.
-__device__ __forceinline__ bool mark(uint32_t* fb, BlockSh* sh, uint32_t v) {
+__device__ __forceinline__ bool mark(uint32_t* fb, BlockSh* sh, uint32_t v, bool precheck = false) {
   const uint32_t w = v >> 5, bit = 1u << (v & 31u);
+  // hub rows / large frontiers raise one vertex many times: a read first
+  // avoids contended atomics (skipped on latency-bound small frontiers)
+  if (precheck && (__ldcg(fb + w) & bit)) return false;
   const uint32_t old = atomicOr(fb + w, bit);
   if (old == 0u) note_word(sh, w);
   return !(old & bit);
@@ -275,6 +278,7 @@ struct PushCtx {
   unsigned int* nchunk;
   uint32_t* Cn;
   unsigned int* ccnt;
+  bool contend;  // large frontier: check Pn before atomics (hub targets)
 };
 
 // Batched Jacobi push of val[r] into tgt[r], as predicated stages (read the
@@ -289,13 +293,16 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
 #pragma unroll
   for (int r = 0; r < R; ++r) old[r] = tgt[r] != kNone ? __ldca(c.Pc + tgt[r]) : kCode;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    go[r] = tgt[r] != kNone && val[r] > (old[r] & kCode);
-    if (go[r]) atomicMax(c.Pn + tgt[r], (old[r] & kFlag) | val[r]);
-  }
+  for (int r = 0; r < R; ++r) go[r] = tgt[r] != kNone && val[r] > (old[r] & kCode);
+  uint32_t cur[R];  // hub targets: many sources raise the same word, skip settled atomics
+#pragma unroll
+  for (int r = 0; r < R; ++r) cur[r] = go[r] && c.contend ? __ldcg(c.Pn + tgt[r]) : 0u;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (go[r] && ((old[r] & kFlag) | val[r]) > cur[r]) atomicMax(c.Pn + tgt[r], (old[r] & kFlag) | val[r]);
   bool first[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) first[r] = go[r] && mark(c.fb, c.sh, tgt[r]);
+  for (int r = 0; r < R; ++r) first[r] = go[r] && mark(c.fb, c.sh, tgt[r], c.contend);
   uint32_t bw[R], b[R], e[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {  // one round trip for the big bit and the degree
@@ -460,10 +467,12 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
       }
     if (live) {
       mine = max(mine, own & kCode);
-      atomicMax(Q + v, (own & kFlag) | mine);
+      // chunks of one hub row run on neighbouring warps: skip the atomic when
+      // another chunk already raised Q[v] at least as far
+      if (((own & kFlag) | mine) > __ldcg(Q + v)) atomicMax(Q + v, (own & kFlag) | mine);
       if (mine > (own & kCode)) {
         ++acc.raised;
-        if (mark(fb, sh, v)) {
+        if (mark(fb, sh, v, true)) {
           ++acc.first;
           if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
         }
@@ -496,6 +505,9 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   c.nchunk = &sl->nchunk;
   c.Cn = a.C[g & 1u];
   c.ccnt = &sl->cand_cnt;
+  // previous step's frontier edges: small frontiers are latency-bound (one
+  // more round trip costs), large ones meet hub targets (atomics contend)
+  c.contend = __ldca(&pl->fedges) > (1ull << 20);
   uint32_t* fp = a.FB[(g - 1u) & 1u];
   const uint32_t* wlp = a.WL[(g - 1u) & 1u];
   const uint4* bp = a.BC[(g - 1u) & 1u];
