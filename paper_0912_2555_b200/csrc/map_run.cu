@@ -411,6 +411,72 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
   }
 }
 
+// Heavy rows of a pull step (the long poles): a warp takes B chunks of at
+// most 32*kHeavyPerLane edges at once, every lane issuing all its loads
+// together; lane k finalises chunk k (own value prefetched) with an atomicMax
+// into Q (Q holds x_{k-2}, never larger).
+template <int B, bool PRE>
+__device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __restrict__ P,
+                                           uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh, uint4* bc,
+                                           SlotCtl* sl, uint32_t* Cn, StepAcc& acc) {
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t c0 = nw - 1u - gw; c0 < a.n_heavy; c0 += nw * B) {  // tail warps do fewer light rows
+    uint4 ch[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const uint32_t c = c0 + (uint32_t)k * nw;
+      ch[k] = c < a.n_heavy ? a.heavy[c] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    uint32_t own = 0;
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      if (lane == (uint32_t)k && ch[k].z > ch[k].y) own = __ldca(P + ch[k].x);
+    uint32_t u[B][kHeavyPerLane];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int r = 0; r < kHeavyPerLane; ++r) {
+        const uint32_t i = ch[k].y + lane + 32u * r;
+        u[k][r] = i < ch[k].z ? __ldg(a.gcol + i) : kNone;
+      }
+    uint32_t best[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      best[k] = 0;
+#pragma unroll
+      for (int r = 0; r < kHeavyPerLane; ++r)
+        if (u[k][r] != kNone) best[k] = max(best[k], cand_of(__ldca(P + u[k][r]), u[k][r]));
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) best[k] = __reduce_max_sync(kFull, best[k]);
+    uint32_t mine = 0, v = 0;
+    bool live = false;
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      if (lane == (uint32_t)k) {
+        mine = best[k];
+        v = ch[k].x;
+        live = ch[k].z > ch[k].y;
+      }
+    if (live) {
+      mine = max(mine, own & kCode);
+      // chunks of one hub row run on neighbouring warps: skip the atomic when
+      // another chunk already raised Q[v] at least as far
+      if (!PRE || ((own & kFlag) | mine) > __ldcg(Q + v)) atomicMax(Q + v, (own & kFlag) | mine);
+      if (mine > (own & kCode)) {
+        ++acc.raised;
+        if (mark(fb, sh, v, PRE)) {
+          ++acc.first;
+          if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
+        }
+        if ((own & kFlag) && mine == v + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
+      }
+    }
+  }
+}
+
 __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, unsigned long long tk) {
   const uint32_t* __restrict__ P = a.P[cur];
   uint32_t* __restrict__ Q = a.P[cur ^ 1];
@@ -423,63 +489,11 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
-  // heavy rows first (they are the long poles): a warp takes kHeavyBatch
-  // chunks of at most 32*kHeavyPerLane edges at once, every lane issuing all
-  // its loads together; lane k finalises chunk k (own value prefetched) with
-  // an atomicMax into Q (Q holds x_{k-2}, never larger)
-  for (uint32_t c0 = nw - 1u - gw; c0 < a.n_heavy; c0 += nw * kHeavyBatch) {  // tail warps do fewer light rows
-    uint4 ch[kHeavyBatch];
-#pragma unroll
-    for (int k = 0; k < kHeavyBatch; ++k) {
-      const uint32_t c = c0 + (uint32_t)k * nw;
-      ch[k] = c < a.n_heavy ? a.heavy[c] : make_uint4(0u, 0u, 0u, 0u);
-    }
-    uint32_t own = 0;
-#pragma unroll
-    for (int k = 0; k < kHeavyBatch; ++k)
-      if (lane == (uint32_t)k && ch[k].z > ch[k].y) own = __ldca(P + ch[k].x);
-    uint32_t u[kHeavyBatch][kHeavyPerLane];
-#pragma unroll
-    for (int k = 0; k < kHeavyBatch; ++k)
-#pragma unroll
-      for (int r = 0; r < kHeavyPerLane; ++r) {
-        const uint32_t i = ch[k].y + lane + 32u * r;
-        u[k][r] = i < ch[k].z ? __ldg(a.gcol + i) : kNone;
-      }
-    uint32_t best[kHeavyBatch];
-#pragma unroll
-    for (int k = 0; k < kHeavyBatch; ++k) {
-      best[k] = 0;
-#pragma unroll
-      for (int r = 0; r < kHeavyPerLane; ++r)
-        if (u[k][r] != kNone) best[k] = max(best[k], cand_of(__ldca(P + u[k][r]), u[k][r]));
-    }
-#pragma unroll
-    for (int k = 0; k < kHeavyBatch; ++k) best[k] = __reduce_max_sync(kFull, best[k]);
-    uint32_t mine = 0, v = 0;
-    bool live = false;
-#pragma unroll
-    for (int k = 0; k < kHeavyBatch; ++k)
-      if (lane == (uint32_t)k) {
-        mine = best[k];
-        v = ch[k].x;
-        live = ch[k].z > ch[k].y;
-      }
-    if (live) {
-      mine = max(mine, own & kCode);
-      // chunks of one hub row run on neighbouring warps: skip the atomic when
-      // another chunk already raised Q[v] at least as far
-      if (((own & kFlag) | mine) > __ldcg(Q + v)) atomicMax(Q + v, (own & kFlag) | mine);
-      if (mine > (own & kCode)) {
-        ++acc.raised;
-        if (mark(fb, sh, v, true)) {
-          ++acc.first;
-          if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
-        }
-        if ((own & kFlag) && mine == v + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
-      }
-    }
-  }
+  // many chunks per warp (R-MAT hubs): four in flight, and reads before the
+  // contended atomics; few (config 2's connectors): one per warp, spread over
+  // more warps, no extra round trip
+  if (a.n_heavy > 4u * nw) pull_heavy<kHeavyBatch, true>(a, P, Q, fb, sh, bc, sl, Cn, acc);
+  else pull_heavy<1, false>(a, P, Q, fb, sh, bc, sl, Cn, acc);
   phase_mark(a, tk, 0);
   switch (a.ell_k) {
     case 1: pull_light<1, 8>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
