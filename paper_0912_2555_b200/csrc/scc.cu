@@ -344,35 +344,50 @@ __global__ void k_list_from_flags(uint32_t n, const uint32_t* flags, const uint3
     if (flags[v]) out[pos[v]] = v;
 }
 
-// ---- compaction of the kept subgraph
-__global__ void k_keep32(uint32_t n, const uint8_t* keep, uint32_t* k32) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    k32[v] = keep[v];
+// ---- compaction of the kept subgraph. The kept set is a bitmap (n/8 bytes)
+// with a per-word exclusive popcount prefix, both L2-resident even at 2^26+
+// vertices: keep tests and new ids (prefix + popc) of the random column reads
+// hit L2 instead of n-byte / 4n-byte arrays in HBM.
+__global__ void k_keep_bits(uint32_t n, const uint8_t* keep, uint32_t* kb, uint32_t* pc) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane_id();
+    const uint32_t w = __ballot_sync(kFull, v < n && keep[v]);
+    if (lane_id() == 0) {
+      kb[v0 >> 5] = w;
+      pc[v0 >> 5] = __popc(w);
+    }
+  }
 }
 
-__global__ void k_kept_list(uint32_t n, const uint8_t* keep, const uint32_t* newid, uint32_t* kept) {
+__device__ __forceinline__ bool kbit(const uint32_t* kb, uint32_t v) { return (kb[v >> 5] >> (v & 31u)) & 1u; }
+__device__ __forceinline__ uint32_t knew(const uint32_t* kb, const uint32_t* wp, uint32_t v) {
+  return wp[v >> 5] + __popc(kb[v >> 5] & ((1u << (v & 31u)) - 1u));
+}
+
+__global__ void k_kept_list(uint32_t n, const uint32_t* kb, const uint32_t* wp, uint32_t* kept) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    if (keep[v]) kept[newid[v]] = v;
+    if (kbit(kb, v)) kept[knew(kb, wp, v)] = v;
 }
 
 // One warp per kept row (rows of R-MAT hubs are long): count, then an
 // order-preserving ballot compaction of the kept columns.
 __global__ void k_filter_count(uint32_t k, const uint32_t* kept, const uint32_t* __restrict__ off,
-                               const uint32_t* __restrict__ col, const uint8_t* keep, uint32_t* cnt) {
+                               const uint32_t* __restrict__ col, const uint32_t* kb, uint32_t* cnt) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t a = gw; a < k; a += nw) {
     const uint32_t v = kept[a];
     uint32_t c = 0;
-    for (uint32_t i = off[v] + lane; i < off[v + 1]; i += 32u) c += keep[col[i]];
+    for (uint32_t i = off[v] + lane; i < off[v + 1]; i += 32u) c += kbit(kb, col[i]);
     c = __reduce_add_sync(kFull, c);
     if (lane == 0) cnt[a] = c;
   }
 }
 
 __global__ void k_filter_fill(uint32_t k, const uint32_t* kept, const uint32_t* __restrict__ off,
-                              const uint32_t* __restrict__ col, const uint8_t* keep,
-                              const uint32_t* newid, const uint32_t* noff, uint32_t* ncol) {
+                              const uint32_t* __restrict__ col, const uint32_t* kb, const uint32_t* wp,
+                              const uint32_t* noff, uint32_t* ncol) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t a = gw; a < k; a += nw) {
@@ -382,9 +397,9 @@ __global__ void k_filter_fill(uint32_t k, const uint32_t* kept, const uint32_t* 
     for (uint32_t i0 = b; i0 < e; i0 += 32u) {
       const uint32_t i = i0 + lane;
       const uint32_t w = i < e ? col[i] : 0u;
-      const bool in = i < e && keep[w];
+      const bool in = i < e && kbit(kb, w);
       const uint32_t bal = __ballot_sync(kFull, in);
-      if (in) ncol[o + __popc(bal & lanemask_lt())] = newid[w];
+      if (in) ncol[o + __popc(bal & lanemask_lt())] = knew(kb, wp, w);
       o += __popc(bal);
     }
   }
@@ -456,13 +471,13 @@ int hybrid_closure(uint32_t n, uint8_t* ep, unsigned long long* dcnt, Dense&& de
   }
 }
 
-void filter_csr(const DevCsr& in, const uint8_t* keep, const uint32_t* newid, const uint32_t* kept,
+void filter_csr(const DevCsr& in, const uint32_t* kb, const uint32_t* wp, const uint32_t* kept,
                 uint32_t k, cudaStream_t s, DevCsr& out) {
   out.n = k;
   out.off.alloc(((size_t)k + 1) * 4, s);
   DevBuf cnt(((size_t)k + 1) * 4, s), scratch;
   if (k) {
-    k_filter_count<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), keep, cnt.as<uint32_t>());
+    k_filter_count<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), kb, cnt.as<uint32_t>());
     CYC_LAUNCHED();
   }
   exclusive_scan(cnt.as<uint32_t>(), out.off.as<uint32_t>(), k, nullptr, s, scratch);
@@ -472,8 +487,8 @@ void filter_csr(const DevCsr& in, const uint8_t* keep, const uint32_t* newid, co
   out.m = m;
   out.col.alloc(((size_t)m + 1) * 4, s);
   if (k) {
-    k_filter_fill<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), keep, newid,
-                                                out.off.as<uint32_t>(), out.col.as<uint32_t>());
+    k_filter_fill<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), kb, wp, out.off.as<uint32_t>(),
+                                                out.col.as<uint32_t>());
     CYC_LAUNCHED();
   }
 }
@@ -608,24 +623,27 @@ uint32_t scc_cyclic_accepting(const DevCsr& snap, const DevCsr& gath, const uint
 void restrict_graph(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc, cudaStream_t s,
                     DevCsr& out_snap, DevCsr& out_gath, DevBuf& out_acc, DevBuf& out_kept) {
   const uint32_t n = snap.n;
-  DevBuf keep((size_t)n + 1, s), k32(((size_t)n + 1) * 4, s), newid(((size_t)n + 2) * 4, s), scratch;
+  const size_t nwd = (size_t)n / 32 + 2;
+  DevBuf keep((size_t)n + 1, s), kb(nwd * 4, s), pc(nwd * 4, s), wp((nwd + 1) * 4, s), scratch;
   scc_keep_mask(snap, gath, acc, s, keep.as<uint8_t>());
+  CYC_CUDA(cudaMemsetAsync(kb.p, 0, nwd * 4, s));
+  CYC_CUDA(cudaMemsetAsync(pc.p, 0, nwd * 4, s));
   if (n) {
-    k_keep32<<<grid_for(n, kT, 8), kT, 0, s>>>(n, keep.as<uint8_t>(), k32.as<uint32_t>());
+    k_keep_bits<<<grid_for(n, kT, 8), kT, 0, s>>>(n, keep.as<uint8_t>(), kb.as<uint32_t>(), pc.as<uint32_t>());
     CYC_LAUNCHED();
   }
-  exclusive_scan(k32.as<uint32_t>(), newid.as<uint32_t>(), n, nullptr, s, scratch);
+  const uint32_t nw = (uint32_t)((n + 31) / 32);
+  exclusive_scan(pc.as<uint32_t>(), wp.as<uint32_t>(), nw, nullptr, s, scratch);
   uint32_t k = 0;
-  CYC_CUDA(cudaMemcpyAsync(&k, newid.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaMemcpyAsync(&k, wp.as<uint32_t>() + nw, 4, cudaMemcpyDeviceToHost, s));
   CYC_CUDA(cudaStreamSynchronize(s));
   out_kept.alloc(((size_t)k + 1) * 4, s);
   if (n) {
-    k_kept_list<<<grid_for(n, kT, 8), kT, 0, s>>>(n, keep.as<uint8_t>(), newid.as<uint32_t>(),
-                                                  out_kept.as<uint32_t>());
+    k_kept_list<<<grid_for(n, kT, 8), kT, 0, s>>>(n, kb.as<uint32_t>(), wp.as<uint32_t>(), out_kept.as<uint32_t>());
     CYC_LAUNCHED();
   }
-  filter_csr(snap, keep.as<uint8_t>(), newid.as<uint32_t>(), out_kept.as<uint32_t>(), k, s, out_snap);
-  filter_csr(gath, keep.as<uint8_t>(), newid.as<uint32_t>(), out_kept.as<uint32_t>(), k, s, out_gath);
+  filter_csr(snap, kb.as<uint32_t>(), wp.as<uint32_t>(), out_kept.as<uint32_t>(), k, s, out_snap);
+  filter_csr(gath, kb.as<uint32_t>(), wp.as<uint32_t>(), out_kept.as<uint32_t>(), k, s, out_gath);
   const size_t words = ((size_t)k + 63) / 64;
   out_acc.alloc((words + 1) * 8, s);
   CYC_CUDA(cudaMemsetAsync(out_acc.p, 0, (words + 1) * 8, s));
