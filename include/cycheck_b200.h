@@ -229,8 +229,10 @@ cyc_status cyc_memcpy(cyc_ctx* ctx, void* dst, const void* src, size_t bytes);
 cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes);
 
 /* ---- multi-GPU row sharding (one process per GPU) ------------------------ */
-/* Device-side state of one sharded fixpoint (int64[4], device memory):
- * [0] done, [1] steps taken, [2] witness (UINT32_MAX = none), [3] early_exit.
+/* Device-side state of one sharded fixpoint (int64[8], device memory):
+ * [0] done, [1] steps taken, [2] witness (UINT32_MAX = none), [3] early_exit,
+ * [4] blocked by a sparse step that overflowed, [5] largest per-rank change
+ * count seen, [6..7] that step's reduced record (for its dense completion).
  * Every rank holds an identical copy; all updates happen on the device from
  * all-reduced records, so ranks stay in lockstep without host syncs. */
 /* One Jacobi step (MaxPropagation::step) restricted to rows [lo, hi) of the
@@ -249,6 +251,17 @@ cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_
  * no change (map_engine.cpp:94-121). Asynchronous. */
 cyc_status cyc_shard_post(cyc_ctx* ctx, const int64_t* rec, int64_t* state, const uint32_t* x_pad,
                           const uint32_t* bounds, int world, uint32_t maxrows, uint32_t* x);
+/* Sparse (changed-only) exchange: after cyc_shard_step, the
+ * rank's changed rows (out[v-lo] != x[v]) as (v, value) pairs into sp
+ * (uint2[cap+1], sp[0] = {count, 0}); after an all-gather of every rank's sp
+ * (sp_all = world x (cap+1) uint2) and the MAX all-reduce of rec,
+ * cyc_shard_post_sparse applies all changes and advances state, or — if some
+ * rank changed more than cap rows — blocks the rest of the batch (state[4])
+ * so the host completes that step with the dense exchange. */
+cyc_status cyc_shard_collect(cyc_ctx* ctx, uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out,
+                             uint32_t cap, uint32_t* sp, const int64_t* state);
+cyc_status cyc_shard_post_sparse(cyc_ctx* ctx, const int64_t* rec, int64_t* state, const uint32_t* sp_all,
+                                 int world, uint32_t cap, uint32_t* x);
 /* used-bitmap demotion on a full replicated vector, entirely on device:
  * remaining = F \ D (words, device), counts[0] = |D|, counts[1] = |F'|
  * (device u64[2]); asynchronous. */

@@ -938,6 +938,24 @@ cyc_status cyc_shard_post(cyc_ctx* ctx, const int64_t* rec, int64_t* state, cons
   });
 }
 
+cyc_status cyc_shard_collect(cyc_ctx* ctx, uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out,
+                             uint32_t cap, uint32_t* sp, const int64_t* state) {
+  return guard([&] {
+    require(ctx && x && sp && state && (out || hi <= lo), CYC_E_CONTRACT, "shard_collect: null argument");
+    cyc::launch_shard_collect(lo, hi, x, out, cap, reinterpret_cast<uint2*>(sp),
+                              reinterpret_cast<const long long*>(state), ctx->s);
+  });
+}
+
+cyc_status cyc_shard_post_sparse(cyc_ctx* ctx, const int64_t* rec, int64_t* state, const uint32_t* sp_all,
+                                 int world, uint32_t cap, uint32_t* x) {
+  return guard([&] {
+    require(ctx && rec && state && sp_all && x && world >= 1, CYC_E_CONTRACT, "shard_post_sparse: bad argument");
+    cyc::launch_shard_post_sparse(reinterpret_cast<const long long*>(rec), reinterpret_cast<long long*>(state),
+                                  reinterpret_cast<const uint2*>(sp_all), world, cap, x, ctx->s);
+  });
+}
+
 cyc_status cyc_shard_demote(cyc_ctx* ctx, const uint32_t* x, uint32_t n, const uint64_t* acc_words,
                             uint64_t* remaining, uint64_t* counts) {
   return guard([&] {

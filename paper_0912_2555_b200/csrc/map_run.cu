@@ -949,7 +949,7 @@ __global__ void k_step_range(uint32_t lo, uint32_t hi, uint32_t heavy, const uin
                              const uint32_t* __restrict__ gcol, const uint32_t* __restrict__ x,
                              const uint32_t* __restrict__ accw, uint32_t* __restrict__ out,
                              unsigned long long* __restrict__ rec, const long long* __restrict__ state) {
-  if (state && state[0]) return;  // fixpoint already decided on every rank
+  if (state && (state[0] | state[4])) return;  // decided, or a sparse step awaits its dense completion
   const uint32_t stride = gridDim.x * blockDim.x;
   bool ch = false;
   uint32_t wit = kNone;
@@ -978,7 +978,7 @@ __global__ void k_step_range_ell(uint32_t lo, uint32_t hi, uint32_t n, uint32_t 
                                  const uint32_t* __restrict__ x, const uint32_t* __restrict__ accw,
                                  uint32_t* __restrict__ out, unsigned long long* __restrict__ rec,
                                  const long long* __restrict__ state) {
-  if (state && state[0]) return;
+  if (state && (state[0] | state[4])) return;
   const uint32_t stride = gridDim.x * blockDim.x;
   bool ch = false;
   uint32_t wit = kNone;
@@ -1010,7 +1010,7 @@ __global__ void k_step_range_chunks(const uint4* __restrict__ chunks, uint32_t n
                                     const uint32_t* __restrict__ gcol, const uint32_t* __restrict__ x,
                                     const uint32_t* __restrict__ accw, uint32_t* __restrict__ out,
                                     const long long* __restrict__ state) {
-  if (state && state[0]) return;
+  if (state && (state[0] | state[4])) return;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t k = gw; k < nch; k += nw) {
@@ -1027,7 +1027,7 @@ __global__ void k_step_range_heavy(const uint4* __restrict__ chunks, uint32_t nc
                                    const uint32_t* __restrict__ goff, const uint32_t* __restrict__ x,
                                    const uint32_t* __restrict__ accw, const uint32_t* __restrict__ out,
                                    unsigned long long* __restrict__ rec, const long long* __restrict__ state) {
-  if (state && state[0]) return;
+  if (state && (state[0] | state[4])) return;
   bool chg = false;
   uint32_t wit = kNone;
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nch; k += gridDim.x * blockDim.x) {
@@ -1057,6 +1057,65 @@ __global__ void k_shard_post(const long long* __restrict__ rec, long long* state
     if ((state[3] && wit != kNone) || !rec[0]) {
       state[0] = 1;
       state[2] = wit;
+    }
+  }
+}
+
+// Sparse exchange: this rank's changed rows as (v, value) after the step;
+// sp[0] = {count, 0}, entries sp[1..cap]; a count above cap marks overflow.
+__global__ void k_shard_collect(uint32_t lo, uint32_t hi, const uint32_t* __restrict__ x,
+                                const uint32_t* __restrict__ out, uint32_t cap, uint2* sp,
+                                const long long* __restrict__ state) {
+  if (state[0] | state[4]) return;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = lo + ((blockIdx.x * blockDim.x + threadIdx.x) & ~31u); v0 < hi; v0 += stride) {
+    const uint32_t v = v0 + lane_id();
+    const bool ch = v < hi && out[v - lo] != x[v];
+    const uint32_t bal = __ballot_sync(kFull, ch);
+    if (!bal) continue;
+    uint32_t base = 0;
+    if (lane_id() == 0) base = atomicAdd(&sp[0].x, (uint32_t)__popc(bal));
+    base = __shfl_sync(kFull, base, 0);
+    const uint32_t idx = base + __popc(bal & lanemask_lt());
+    if (ch && idx < cap) sp[1 + idx] = make_uint2(v, out[v - lo]);
+  }
+}
+
+// After the all-gather of every rank's sparse buffer (sp_all: world x (cap+1))
+// and the MAX all-reduce of rec: apply all changes (idempotent) and advance
+// the state, unless some rank overflowed — then block the batch (state[4])
+// and keep rec in state[6..7] for the host's dense completion of this step.
+__global__ void k_shard_post_sparse(const long long* __restrict__ rec, long long* state,
+                                    const uint2* __restrict__ sp_all, int world, uint32_t cap,
+                                    uint32_t* __restrict__ x) {
+  uint32_t maxc = 0;
+  for (int r = 0; r < world; ++r) maxc = max(maxc, sp_all[(size_t)r * (cap + 1)].x);
+  const bool over = maxc > cap;
+  if (!over) {
+    const uint64_t total = (uint64_t)world * cap;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+      const uint32_t r = (uint32_t)(e / cap), i = (uint32_t)(e % cap);
+      const uint2* b = sp_all + (size_t)r * (cap + 1);
+      if (i < b[0].x) {
+        const uint2 t = b[1 + i];
+        x[t.x] = t.y;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !(state[0] | state[4])) {
+    state[5] = max(state[5], (long long)maxc);
+    if (over) {
+      state[4] = 1;
+      state[6] = rec[0];
+      state[7] = rec[1];
+    } else {
+      const uint32_t wit = kNone - (uint32_t)rec[1];
+      state[1] += 1;
+      if ((state[3] && wit != kNone) || !rec[0]) {
+        state[0] = 1;
+        state[2] = wit;
+      }
     }
   }
 }
@@ -1276,6 +1335,21 @@ void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint3
                                                              accw, out, r, state);
     CYC_LAUNCHED();
   }
+}
+
+void launch_shard_collect(uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out, uint32_t cap,
+                          uint2* sp, const long long* state, cudaStream_t s) {
+  CYC_CUDA(cudaMemsetAsync(sp, 0, 8, s));
+  if (hi <= lo) return;
+  k_shard_collect<<<grid_for(hi - lo, 256, 8), 256, 0, s>>>(lo, hi, x, out, cap, sp, state);
+  CYC_LAUNCHED();
+}
+
+void launch_shard_post_sparse(const long long* rec, long long* state, const uint2* sp_all, int world,
+                              uint32_t cap, uint32_t* x, cudaStream_t s) {
+  k_shard_post_sparse<<<grid_for((uint64_t)world * cap + 1, 256, 8), 256, 0, s>>>(rec, state, sp_all, world,
+                                                                                  cap, x);
+  CYC_LAUNCHED();
 }
 
 void launch_shard_post(const long long* rec, long long* state, const uint32_t* x_pad,

@@ -106,6 +106,12 @@ void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* acc
 void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint32_t* x,
                        const uint32_t* accw, uint32_t* out, long long* rec, const long long* state,
                        cudaStream_t s);
+// Sparse exchange: changed rows of [lo, hi) into sp (sp[0] = count) and the
+// post step applying every rank's changes (or flagging overflow).
+void launch_shard_collect(uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out, uint32_t cap,
+                          uint2* sp, const long long* state, cudaStream_t s);
+void launch_shard_post_sparse(const long long* rec, long long* state, const uint2* sp_all, int world,
+                              uint32_t cap, uint32_t* x, cudaStream_t s);
 // Unpads the gathered slices into x and advances the sharded fixpoint state.
 void launch_shard_post(const long long* rec, long long* state, const uint32_t* x_pad,
                        const uint32_t* bounds, int world, uint32_t maxrows, uint32_t* x, cudaStream_t s);

@@ -95,6 +95,14 @@ class CudaShardBackend:
                                              _abi.ptr(x_pad), _abi.ptr(self.bounds), world, maxrows,
                                              _abi.ptr(x)))
 
+    def collect(self, lo: int, hi: int, x, out, cap: int, sp, state):
+        _abi.check(_abi.lib().cyc_shard_collect(self.snap.context.handle, lo, hi, _abi.ptr(x), _abi.ptr(out),
+                                                cap, _abi.ptr(sp), _abi.ptr(state)))
+
+    def post_sparse(self, rec, state, sp_all, world: int, cap: int, x):
+        _abi.check(_abi.lib().cyc_shard_post_sparse(self.snap.context.handle, _abi.ptr(rec), _abi.ptr(state),
+                                                    _abi.ptr(sp_all), world, cap, _abi.ptr(x)))
+
     def demote(self, x, acc):
         rem = self.torch.zeros_like(acc)
         _abi.check(_abi.lib().cyc_shard_demote(self.snap.context.handle, _abi.ptr(x), self.n,
@@ -135,9 +143,15 @@ class _StepGraphs:
 
 
 class _Runner:
-    """Persistent buffers (and captured step graphs) of one rank's shard."""
+    """Persistent buffers (and captured step graphs) of one rank's shard.
 
-    def __init__(self, backend, dist, rank, world, bounds, group, graphs):
+    Two exchange modes per step: dense (all-gather of the padded row slices)
+    and sparse (all-gather of each rank's changed (v, value) pairs, at most
+    `cap` per rank). A sparse step whose change count overflows
+    `cap` on any rank blocks the rest of its batch on the device; the host
+    then completes that one step densely and stays dense for the fixpoint."""
+
+    def __init__(self, backend, dist, rank, world, bounds, group, graphs, cap=None):
         torch = backend.torch
         self.be, self.dist, self.group = backend, dist, group
         self.world = world
@@ -148,28 +162,50 @@ class _Runner:
         self.send = backend.zeros(self.maxrows)
         self.x_pad = backend.zeros(world * self.maxrows)
         self.rec = backend.zeros(2, torch.int64)
-        self.state = backend.zeros(4, torch.int64)
+        self.state = backend.zeros(8, torch.int64)
         self.acc = backend.zeros((backend.n + 63) // 64, torch.int64)
-        self.graphs = _StepGraphs(backend, self.one_step) if graphs else None
+        self.cap = int(cap) if cap is not None else max(4096, self.maxrows // 32)
+        self.sp = backend.zeros(2 * (self.cap + 1))                 # uint2[cap+1] as int32 pairs
+        self.sp_all = backend.zeros(world * 2 * (self.cap + 1))
+        self.graphs = ({"dense": _StepGraphs(backend, self.one_dense),
+                        "sparse": _StepGraphs(backend, self.one_sparse)} if graphs else None)
 
-    def one_step(self):
+    def one_dense(self):
         be, d = self.be, self.dist
         be.step(self.x, self.acc, self.lo, self.hi, self.send, self.rec, self.state)
         d.all_gather_into_tensor(self.x_pad, self.send[: self.maxrows], group=self.group)
         d.all_reduce(self.rec, op=d.ReduceOp.MAX, group=self.group)
         be.post(self.rec, self.state, self.x_pad, self.world, self.maxrows, self.x)
 
-    def steps(self, k: int):
+    def one_sparse(self):
+        be, d = self.be, self.dist
+        be.step(self.x, self.acc, self.lo, self.hi, self.send, self.rec, self.state)
+        be.collect(self.lo, self.hi, self.x, self.send, self.cap, self.sp, self.state)
+        d.all_gather_into_tensor(self.sp_all, self.sp, group=self.group)
+        d.all_reduce(self.rec, op=d.ReduceOp.MAX, group=self.group)
+        be.post_sparse(self.rec, self.state, self.sp_all, self.world, self.cap, self.x)
+
+    def complete_dense(self):
+        """Dense exchange of the step a sparse batch could not apply."""
+        d = self.dist
+        self.state[4] = 0
+        self.rec.copy_(self.state[6:8])
+        d.all_gather_into_tensor(self.x_pad, self.send[: self.maxrows], group=self.group)
+        self.be.post(self.rec, self.state, self.x_pad, self.world, self.maxrows, self.x)
+
+    def steps(self, k: int, mode: str):
         if self.graphs is not None:
-            self.graphs.run(k)
+            self.graphs[mode].run(k)
         else:
+            one = self.one_sparse if mode == "sparse" else self.one_dense
             for _ in range(k):
-                self.one_step()
+                one()
 
 
 def run_map_sharded(backend, dist, rank: int, world: int, bounds, acc_words: np.ndarray,
                     early_exit: bool = True, group=None, max_batch: int = 64,
-                    graphs: Optional[bool] = None) -> ShardedResult:
+                    graphs: Optional[bool] = None, exchange: str = "auto",
+                    sparse_cap: Optional[int] = None) -> ShardedResult:
     """run_map (map_engine.cpp:139-162) with rows sharded over `world` ranks.
 
     Steps are enqueued in batches; the first batch of a fixpoint is the
@@ -177,14 +213,19 @@ def run_map_sharded(backend, dist, rank: int, world: int, bounds, acc_words: np.
     ones double up to `max_batch`. The host reads the device state once per
     batch. With `graphs` (default: the backend's choice) every batch is a
     replay of captured CUDA graphs, so a step costs no host launches; the
-    buffers and graphs persist on the backend across calls."""
+    buffers and graphs persist on the backend across calls.
+
+    exchange: "dense", "sparse" or "auto" (sparse until a step changes more
+    than the sparse capacity on some rank; that step is completed densely and
+    the run stays dense from then on — config 2 overflows at its first step,
+    config 5's chain never does)."""
     n = backend.n
     bounds = [int(b) for b in bounds]
     use_graphs = getattr(backend, "graphs", False) if graphs is None else graphs
-    key = (tuple(bounds), rank, world, id(group), bool(use_graphs))
+    key = (tuple(bounds), rank, world, id(group), bool(use_graphs), sparse_cap)
     cache = backend.__dict__.setdefault("_runners", {})
     if key not in cache:
-        cache[key] = _Runner(backend, dist, rank, world, bounds, group, use_graphs)
+        cache[key] = _Runner(backend, dist, rank, world, bounds, group, use_graphs, sparse_cap)
     rn = cache[key]
     words = np.ascontiguousarray(acc_words, dtype=np.uint64)
     rn.acc.copy_(backend.acc_tensor(words))
@@ -193,15 +234,27 @@ def run_map_sharded(backend, dist, rank: int, world: int, bounds, acc_words: np.
     verdict = Verdict.no_cycle()
     fsize = int(np.bitwise_count(words).sum())
     guess = 4
+    ex = stats.device["exchange"] = {"dense_batches": 0, "sparse_batches": 0, "dense_completions": 0}
+    sparse_ok = exchange != "dense"
     while fsize > 0:  # front.any()
         x.zero_()
         state.zero_()
         state[2] = _NONE
         state[3] = int(early_exit)
+        mode = "sparse" if sparse_ok else "dense"
         batch = max(guess, 1)
         while True:
-            rn.steps(batch)
-            done, steps, witness, _ = (int(v) for v in state.cpu())
+            rn.steps(batch, mode)
+            ex[mode + "_batches"] += 1
+            st = [int(v) for v in state.cpu()]
+            if st[4]:  # a sparse step overflowed: complete it densely
+                rn.complete_dense()
+                ex["dense_completions"] += 1
+                if exchange == "auto":
+                    mode = "dense"
+                    sparse_ok = False
+                st = [int(v) for v in state.cpu()]
+            done, steps, witness = st[0], st[1], st[2]
             if done:
                 break
             batch = min(max(batch * 2, 4), max_batch)

@@ -57,8 +57,11 @@ def test_cuda_shard_backend_matches_run_map(eng, R, nccl):
         be = sharded.CudaShardBackend(snap, torch.device("cuda", 0))
         off, _ = snap.gather_index()
         for early in (True, False):
-            # eager launches and captured CUDA-graph batches give the same run
-            res = sharded.run_map_sharded(be, nccl, 0, 1, [0, n], words, early, graphs=bool(t % 2))
+            # eager launches and captured CUDA-graph batches, dense / sparse
+            # (capacity 7: overflow and dense completion) / auto exchange
+            exchange, cap = [("auto", None), ("sparse", 7), ("dense", None), ("auto", 3)][(2 * t + early) % 4]
+            res = sharded.run_map_sharded(be, nccl, 0, 1, [0, n], words, early, graphs=bool(t % 2),
+                                          exchange=exchange, sparse_cap=cap)
             ref = R.run_map(R.transpose(R.build_snapshot(n, e, True)), words, early)
             got = (res.verdict.cycle_found(), res.verdict.witness, res.stats.iterations,
                    res.stats.kernel_calls, res.stats.demoted_total)

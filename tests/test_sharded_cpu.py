@@ -36,7 +36,7 @@ class HostShardBackend:
 
     def step(self, x, acc, lo, hi, out, rec, state=None):
         rec.zero_()
-        if state is not None and int(state[0]):
+        if state is not None and (int(state[0]) or int(state[4])):
             return
         xv = x.numpy().view(np.uint32)[: self.n]
         words = acc.numpy().view(np.uint64)
@@ -59,6 +59,40 @@ class HostShardBackend:
             if (int(state[3]) and wit != self.NONE) or not int(rec[0]):
                 state[0] = 1
                 state[2] = wit
+
+    def collect(self, lo, hi, x, out, cap, sp, state):
+        sp.zero_()
+        if int(state[0]) or int(state[4]):
+            return
+        xv = x.numpy()[lo:hi]
+        ov = out.numpy()[: hi - lo]
+        idx = np.flatnonzero(ov != xv)
+        sp[0] = len(idx)
+        k = min(len(idx), cap)
+        pairs = np.stack([idx[:k] + lo, ov[idx[:k]].astype(np.int64)], 1).astype(np.int64)
+        sp[2: 2 + 2 * k] = torch.from_numpy(pairs.reshape(-1).astype(np.int32))
+
+    def post_sparse(self, rec, state, sp_all, world, cap, x):
+        a = sp_all.numpy().reshape(world, cap + 1, 2)
+        counts = a[:, 0, 0].astype(np.int64) & 0xFFFFFFFF
+        over = counts.max() > cap
+        if not over:
+            for r in range(world):
+                c = int(counts[r])
+                if c:
+                    x[torch.from_numpy(a[r, 1:1 + c, 0].astype(np.int64))] = torch.from_numpy(a[r, 1:1 + c, 1].copy())
+        if not (int(state[0]) or int(state[4])):
+            state[5] = max(int(state[5]), int(counts.max()))
+            if over:
+                state[4] = 1
+                state[6] = rec[0]
+                state[7] = rec[1]
+            else:
+                wit = self.NONE - int(rec[1])
+                state[1] += 1
+                if (int(state[3]) and wit != self.NONE) or not int(rec[0]):
+                    state[0] = 1
+                    state[2] = wit
 
     def demote(self, x, acc):
         rem, dem = self.R.demote(x.numpy().view(np.uint32)[: self.n], acc.numpy().view(np.uint64))
@@ -83,11 +117,14 @@ def _worker(rank, world, port, cases, q):
 
     R = oracle.Restatement()
     out = []
-    for n, edges, accw, early in cases:
+    for t, (n, edges, accw, early) in enumerate(cases):
         gat = R.transpose(R.build_snapshot(n, edges, True))
         bounds = sharded.shard_bounds(gat.off, world)
         be = HostShardBackend(R, gat, n)
-        res = sharded.run_map_sharded(be, dist, rank, world, bounds, accw, early)
+        # dense, sparse with overflow fallbacks (tiny capacity) and auto
+        exchange, cap = [("dense", None), ("sparse", 3), ("auto", None), ("auto", 1)][t % 4]
+        res = sharded.run_map_sharded(be, dist, rank, world, bounds, accw, early, exchange=exchange,
+                                      sparse_cap=cap)
         out.append((res.verdict.cycle_found(), res.verdict.witness, res.stats.iterations,
                     res.stats.kernel_calls, res.stats.demoted_total,
                     res.final_values.numpy().view(np.uint32).copy()))
