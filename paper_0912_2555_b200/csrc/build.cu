@@ -1229,9 +1229,11 @@ void build_heavy(DevCsr& g, uint32_t heavy, uint32_t chunk, cudaStream_t s, uint
 
 uint32_t pull_col_blocks(uint32_t n) {
   // keep each column block's slice of the map vector (4 B per vertex) within
-  // ~48 MB of the 126 MB L2, leaving room for the streamed CSR data
+  // ~96 MB of the 126 MB L2 (measured on config 3: 3 blocks 69 ms per 8
+  // steps, 6 blocks 77, 12 blocks 145, none 97 — more blocks cut rows into
+  // more, shorter chunks)
   const uint64_t bytes = (uint64_t)n * 4;
-  const uint64_t budget = 48ull << 20;
+  const uint64_t budget = 96ull << 20;
   return bytes <= 2 * budget ? 1u : (uint32_t)((bytes + budget - 1) / budget);
 }
 
