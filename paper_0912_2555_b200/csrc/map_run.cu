@@ -422,11 +422,13 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t c0 = nw - 1u - gw; c0 < a.n_heavy; c0 += nw * B) {  // tail warps do fewer light rows
+  // a warp takes B consecutive chunks (often of one hub row: their results
+  // merge before a single finalisation); tail warps do fewer light rows
+  for (uint32_t c0 = (nw - 1u - gw) * B; c0 < a.n_heavy; c0 += nw * B) {
     uint4 ch[B];
 #pragma unroll
     for (int k = 0; k < B; ++k) {
-      const uint32_t c = c0 + (uint32_t)k * nw;
+      const uint32_t c = c0 + (uint32_t)k;
       ch[k] = c < a.n_heavy ? a.heavy[c] : make_uint4(0u, 0u, 0u, 0u);
     }
     uint32_t own = 0;
@@ -456,9 +458,12 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
 #pragma unroll
     for (int k = 0; k < B; ++k)
       if (lane == (uint32_t)k) {
-        mine = best[k];
         v = ch[k].x;
-        live = ch[k].z > ch[k].y;
+        // first chunk of its row within the group finalises the merged max
+        live = ch[k].z > ch[k].y && (k == 0 || ch[k - 1].x != v || ch[k - 1].z <= ch[k - 1].y);
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (ch[j].x == v && ch[j].z > ch[j].y) mine = max(mine, best[j]);
       }
     if (live) {
       mine = max(mine, own & kCode);
