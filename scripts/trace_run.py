@@ -59,3 +59,8 @@ for mode in modes:
                 print(f"   {name} raised per step: p5/25/50/75/95 = {qs.astype(int).tolist()} (n={s.n})")
         # raised vs step-in-fixpoint for the first few fixpoints
         print("   step-in-fixpoint raised (first fixpoint):", [int(r) for r in tr[:70, 3]])
+    if os.environ.get("TRACE_GAPS"):
+        t_start, t_end = tr[:, 4].astype(np.float64), tr[:, 8].astype(np.float64)
+        gap = (t_start[1:] - t_end[:-1]) / 1e3
+        per = (t_start[1:] - t_start[:-1]) / 1e3
+        print(f"   step period p50 {np.median(per):.2f} us, gap end->next start p50 {np.median(gap):.2f} us")
