@@ -385,10 +385,16 @@ def run_b200_sharded(args, rank, world, local):
     snap = eng.build_snapshot((n, e, eng.Bitset.from_words(a, n)), ctx=ctx)
     off, _ = snap.gather_index()
     bounds = sharded.plan(off, world)
-    be = sharded.CudaShardBackend(snap, device)
     words = snap.accepting.words().copy()
+    if args.fused:  # exchange fused into the step kernel over peer memory
+        fs = sharded.FusedShard(snap, dist, rank, world, bounds)
+        run = lambda: fs.run(words, True)  # noqa: E731
+    else:
+        be = sharded.CudaShardBackend(snap, device)
+        run = lambda: sharded.run_map_sharded(be, dist, rank, world, bounds, words, True,  # noqa: E731
+                                              exchange=args.exchange)
     for _ in range(args.warmup):
-        sharded.run_map_sharded(be, dist, rank, world, bounds, words, True)
+        run()
     times = []
     for _ in range(args.steps):
         _abi.check(_abi.lib().cyc_flush_l2(ctx.handle, L2_FLUSH_BYTES))
@@ -397,7 +403,7 @@ def run_b200_sharded(args, rank, world, local):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
-        res = sharded.run_map_sharded(be, dist, rank, world, bounds, words, True)
+        res = run()
         t1.record()
         torch.cuda.synchronize(device)
         times.append(t0.elapsed_time(t1))
@@ -411,7 +417,9 @@ def run_b200_sharded(args, rank, world, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded include/cyc_gen.h)",
             "config": {"workload": f"config{args.config}", "n": n, "m": m,
-                       "parallelism": f"rowshard{world}", "exchange": "nccl allgather + allreduce per step"},
+                       "parallelism": f"rowshard{world}",
+                       "exchange": ("fused: peer-memory stores in the step kernel + system-scope barrier"
+                                    if args.fused else f"nccl ({args.exchange}): allgather + allreduce per step")},
             "verdict": {"cycle_found": res.verdict.cycle_found(), "iterations": res.stats.iterations,
                         "kernel_calls": res.stats.kernel_calls}}))
     dist.destroy_process_group()
@@ -434,6 +442,10 @@ def main():
     ap.add_argument("--n-override", type=int, default=0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="with --sharded: exchange fused into the step kernel (peer memory) instead of NCCL")
+    ap.add_argument("--exchange", default="dense", choices=["dense", "sparse", "auto"],
+                    help="with --sharded (NCCL): dense slices, changed-only pairs, or auto")
     ap.add_argument("--sharded", action="store_true",
                     help="N>1: row-shard one graph over the ranks (NCCL exchange per step) "
                          "instead of independent replicas")

@@ -267,6 +267,21 @@ cyc_status cyc_shard_post_sparse(cyc_ctx* ctx, const int64_t* rec, int64_t* stat
  * (device u64[2]); asynchronous. */
 cyc_status cyc_shard_demote(cyc_ctx* ctx, const uint32_t* x, uint32_t n, const uint64_t* acc_words,
                             uint64_t* remaining, uint64_t* counts);
+/* Fused exchange: one persistent kernel per rank runs the whole
+ * run_map for rows [lo, hi) and stores every new row value straight into all
+ * ranks' replicated vectors over peer memory (CUDA IPC / NVLink) as it is
+ * computed; a system-scope barrier per step replaces the collectives.
+ * open: allocates the rank's shared block, writes its 64-byte IPC handle;
+ * connect: all ranks' handles in rank order (world x 64 bytes); run: every
+ * rank calls it with the same accepting words and early_exit; stats and the
+ * final vector (n codes, nullable) equal run_map's. */
+typedef struct cyc_fused cyc_fused;
+cyc_status cyc_fused_open(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi, int rank, int world,
+                          cyc_fused** out, void* handle_out);
+cyc_status cyc_fused_connect(cyc_fused* f, const void* handles);
+cyc_status cyc_fused_run(cyc_fused* f, const uint64_t* acc_words, int early_exit, cyc_map_stats* st,
+                         uint32_t* final_values);
+void cyc_fused_close(cyc_fused* f);
 /* Edge-balanced contiguous row ranges, the reference's worker partition rule
  * (map_engine.cpp:35-43): bounds[r] for r in [0, parts], computed on the
  * host from gather row offsets (n+1 u64). */

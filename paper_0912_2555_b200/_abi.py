@@ -167,6 +167,10 @@ _SIGS = {
     "cyc_shard_collect": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, C.c_uint32, _P, _P]),
     "cyc_shard_post_sparse": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_uint32, _P]),
     "cyc_shard_demote": (C.c_int, [_P, _P, C.c_uint32, _P, _P, _P]),
+    "cyc_fused_open": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(_P), _P]),
+    "cyc_fused_connect": (C.c_int, [_P, _P]),
+    "cyc_fused_run": (C.c_int, [_P, _P, C.c_int, C.POINTER(MapStatsC), _P]),
+    "cyc_fused_close": (None, [_P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -14,6 +14,7 @@
 
 #include "../../include/cyc_gen.h"
 #include "extend.cuh"
+#include "fused.cuh"
 #include "gen.cuh"
 #include "ingest.cuh"
 #include "map_run.cuh"
@@ -60,6 +61,12 @@ void ctx_release(cyc_ctx* ctx) {
   delete ctx;
 }
 }  // namespace
+
+struct cyc_fused {
+  cyc_ctx* ctx = nullptr;
+  const cyc_graph* g = nullptr;
+  cyc::FusedShard sh;
+};
 
 struct cyc_explicit {
   cyc_ctx* ctx = nullptr;
@@ -954,6 +961,60 @@ cyc_status cyc_shard_post_sparse(cyc_ctx* ctx, const int64_t* rec, int64_t* stat
     cyc::launch_shard_post_sparse(reinterpret_cast<const long long*>(rec), reinterpret_cast<long long*>(state),
                                   reinterpret_cast<const uint2*>(sp_all), world, cap, x, ctx->s);
   });
+}
+
+cyc_status cyc_fused_open(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi, int rank, int world,
+                          cyc_fused** out, void* handle_out) {
+  return guard([&] {
+    require(ctx && g && out && handle_out, CYC_E_CONTRACT, "fused_open: null argument");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    auto* f = new cyc_fused;
+    try {
+      f->ctx = ctx;
+      f->g = g;
+      f->sh.open(g->gath, lo, hi, rank, world, handle_out);
+    } catch (...) {
+      delete f;
+      throw;
+    }
+    ctx->refs.fetch_add(1);
+    *out = f;
+  });
+}
+
+cyc_status cyc_fused_connect(cyc_fused* f, const void* handles) {
+  return guard([&] {
+    require(f && handles, CYC_E_CONTRACT, "fused_connect: null argument");
+    CYC_CUDA(cudaSetDevice(f->ctx->device));
+    f->sh.connect(handles);
+  });
+}
+
+cyc_status cyc_fused_run(cyc_fused* f, const uint64_t* acc_words, int early_exit, cyc_map_stats* st,
+                         uint32_t* final_values) {
+  return guard([&] {
+    require(f && acc_words, CYC_E_CONTRACT, "fused_run: null argument");
+    CYC_CUDA(cudaSetDevice(f->ctx->device));
+    unsigned long long res[6];
+    f->sh.run(acc_words, early_exit, f->ctx->s, res);
+    if (st) {
+      std::memset(st, 0, sizeof *st);
+      st->cycle_found = (int32_t)res[0];
+      st->witness = (uint32_t)res[1];
+      st->iterations = res[2];
+      st->kernel_calls = res[3];
+      st->demoted_total = res[4];
+    }
+    if (final_values) f->sh.final_vector(final_values, f->ctx->s);
+  });
+}
+
+void cyc_fused_close(cyc_fused* f) {
+  if (!f) return;
+  cyc_ctx* c = f->ctx;
+  cudaSetDevice(c->device);
+  delete f;
+  ctx_release(c);
 }
 
 cyc_status cyc_shard_demote(cyc_ctx* ctx, const uint32_t* x, uint32_t n, const uint64_t* acc_words,

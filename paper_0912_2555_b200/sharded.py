@@ -271,3 +271,57 @@ def run_map_sharded(backend, dist, rank: int, world: int, bounds, acc_words: np.
         if dcount == 0:
             break
     return ShardedResult(verdict, stats, x[:n].clone() if n else x[:0].clone())
+
+
+def exchange_handles(dist, handle: bytes, world: int, group=None) -> bytes:
+    """Every rank's 64-byte IPC handle, concatenated in rank order."""
+    got = [None] * world
+    dist.all_gather_object(got, bytes(handle), group=group)
+    assert all(isinstance(h, bytes) and len(h) == len(handle) for h in got)
+    return b"".join(got)
+
+
+class FusedShard:
+    """Row-sharded run_map with the exchange fused into the step kernel
+    (cyc_fused_*): every rank's persistent kernel stores its new row values
+    straight into all ranks' replicated vectors over peer memory and meets the
+    others at a system-scope barrier per step — no collective per step. The
+    NCCL protocol above (run_map_sharded) is the baseline. Handles travel once
+    over torch.distributed; every rank must call run() with the same inputs."""
+
+    def __init__(self, snap: CsrSnapshot, dist, rank: int, world: int, bounds, group=None):
+        lib = _abi.lib()
+        bounds = [int(b) for b in bounds]
+        self.snap, self.n = snap, snap.n
+        self.h = C.c_void_p()
+        handle = (C.c_char * 64)()
+        _abi.check(lib.cyc_fused_open(snap.context.handle, snap.handle, bounds[rank], bounds[rank + 1], rank,
+                                      world, C.byref(self.h), handle))
+        blob = exchange_handles(dist, bytes(handle), world, group)
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        _abi.check(lib.cyc_fused_connect(self.h, buf))
+        if world > 1:
+            dist.barrier(group=group)  # every rank connected before anyone runs
+
+    def run(self, acc_words: np.ndarray, early_exit: bool = True) -> ShardedResult:
+        words = np.ascontiguousarray(acc_words, dtype=np.uint64)
+        st = _abi.MapStatsC()
+        fx = np.zeros(max(self.n, 1), np.uint32)
+        _abi.check(_abi.lib().cyc_fused_run(self.h, _abi.ptr(words), int(early_exit), C.byref(st), _abi.ptr(fx)))
+        stats = MapStats()
+        stats.iterations, stats.kernel_calls, stats.demoted_total = st.iterations, st.kernel_calls, st.demoted_total
+        if st.cycle_found:
+            stats.cycle_witness = st.witness
+        v = Verdict.cycle(st.witness) if st.cycle_found else Verdict.no_cycle()
+        return ShardedResult(v, stats, fx[: self.n])
+
+    def close(self):
+        if getattr(self, "h", None):
+            _abi.lib().cyc_fused_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -91,3 +91,37 @@ def test_cuda_shard_backend_matches_run_map(eng, R, nccl):
         be.step(x, accd, 0, n, o, rec, done)
         assert bool((o == -1).all())
         be.release()
+
+
+def test_fused_shard_matches_run_map(eng, R, nccl):
+    """The fused peer-memory exchange path (cyc_fused_*), world 1: the
+    persistent kernel with system-scope barriers and IPC-exported buffers
+    reproduces run_map (verdict, witness, MapStats, final vector)."""
+    from paper_0912_2555_b200 import sharded
+
+    rng = np.random.default_rng(77)
+    p = eng.preset(2)
+    p.L, p.W, p.S = 8, 64, 8
+    eng.prepare(p)
+    gn, ge, ga = R.generate(p)
+    s = eng.build_snapshot((gn, ge, eng.Bitset.from_words(ga, gn)))
+    f = sharded.FusedShard(s, nccl, 0, 1, [0, gn])
+    res = f.run(ga, True)
+    assert (res.stats.iterations, res.stats.kernel_calls, res.stats.demoted_total) == (9, 81, 8)
+    f.close()
+    for t in range(4):
+        n = int(rng.integers(500, 20000))
+        e = rng.integers(0, n, size=(n * 3, 2)).astype(np.uint32)
+        acc = rng.random(n) < [0.01, 0.2][t % 2]
+        snap = eng.build_snapshot((n, e, acc))
+        words = snap.accepting.words().copy()
+        f = sharded.FusedShard(snap, nccl, 0, 1, [0, n])
+        for early in (True, False):
+            for rep in range(2):  # barrier counters carry over between runs
+                res = f.run(words, early)
+                ref = R.run_map(R.transpose(R.build_snapshot(n, e, True)), words, early)
+                got = (res.verdict.cycle_found(), res.verdict.witness, res.stats.iterations,
+                       res.stats.kernel_calls, res.stats.demoted_total)
+                assert got == (ref.cycle, ref.witness, ref.iterations, ref.kernel_calls, ref.demoted_total)
+                assert np.array_equal(res.final_values, ref.final_x)
+        f.close()

@@ -173,3 +173,34 @@ def test_sharded_protocol_matches_single_device(world):
         ref = R.run_map(R.transpose(R.build_snapshot(n, e, True)), w, early)
         assert g[:5] == (ref.cycle, ref.witness, ref.iterations, ref.kernel_calls, ref.demoted_total)
         assert np.array_equal(g[5], ref.final_x)
+
+
+def _handles_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_0912_2555_b200 import sharded
+
+    mine = bytes([rank]) * 64
+    blob = sharded.exchange_handles(dist, mine, world)
+    if rank == 0:
+        q.put(blob)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_handle_exchange(world):
+    """The fused path's host protocol: every rank ends up with all ranks'
+    IPC handles in rank order (cyc_fused_connect's input)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handles_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    blob = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert blob == b"".join(bytes([r]) * 64 for r in range(world))
