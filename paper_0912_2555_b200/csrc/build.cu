@@ -999,14 +999,14 @@ static void count_sort_rows(const uint2* e2, uint64_t m_log, uint32_t n, int key
   if (n <= (1u << 28) && m_log > 0) {
     const uint32_t sh = kBucketLog;
     const uint32_t nb = (uint32_t)(((uint64_t)n + (1u << sh) - 1) >> sh);
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // thread-safe one-time init
       CYC_CUDA(cudaFuncSetAttribute(k_bucket_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       CYC_CUDA(cudaFuncSetAttribute(k_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       CYC_CUDA(cudaFuncSetAttribute(k_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       CYC_CUDA(cudaFuncSetAttribute(k_bucket_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-      attr = true;
-    }
+      return true;
+    }();
+    (void)attr;
     uint32_t* bcnt = ar.get<uint32_t>(ar.bcnt, ((size_t)nb + 1) * 4, s);
     uint32_t* bbase = ar.get<uint32_t>(ar.bbase, ((size_t)nb + 2) * 4, s);
     uint32_t* bcur = ar.get<uint32_t>(ar.bcur, ((size_t)nb + 1) * 4, s);

@@ -1273,12 +1273,11 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
     a.trace_cap = trace_cap;
   }
 
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
+  static const int blocks_per_sm = [] {  // thread-safe one-time init
     int b = 0;
     CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_map_run, kRunThreads, 0));
-    blocks_per_sm = b > 0 ? b : 1;
-  }
+    return b > 0 ? b : 1;
+  }();
   dim3 grid((unsigned)(sm_count() * blocks_per_sm)), block(kRunThreads);
   void* args[] = {&a};
   CYC_CUDA(cudaEventRecord(e0, s));
