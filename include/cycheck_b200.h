@@ -56,7 +56,7 @@ typedef struct cyc_map_options {
   int32_t mode;            /* CYC_MODE_* (default AUTO) */
   uint64_t max_iterations; /* 0 = run to verdict (run_map); 1 = one fixpoint */
   uint64_t max_steps;      /* 0 = unbounded; else stop the first fixpoint after k steps */
-  uint32_t push_alpha;     /* push when frontier edges * alpha < m (0 = default) */
+  uint32_t push_alpha;     /* push when frontier edges * alpha < m (0 = default 16) */
   uint32_t trace_cap;      /* > 0: record up to this many steps (cyc_map_trace) */
 } cyc_map_options;
 
