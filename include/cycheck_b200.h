@@ -239,11 +239,13 @@ cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes);
  * gather index: out[v - lo] for v in the range, from the full replicated
  * vector x (n codes, device) and accepting words (device). rec (device
  * int64[2]) receives {changed, UINT32_MAX - min self-witness} (MAX-reducible;
- * 0 = no witness). A no-op when state[0] (done) is set. Asynchronous on the
- * context's stream (no host sync), for use between collectives. */
+ * 0 = no witness). A no-op when state[0] (done) or state[4] (blocked) is
+ * set, and with first_only (sparse protocol) after the fixpoint's first step,
+ * which cyc_shard_push then takes. Asynchronous on the context's stream (no
+ * host sync), for use between collectives. */
 cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi,
                           const uint32_t* x, const uint64_t* acc_words, uint32_t* out,
-                          int64_t* rec, const int64_t* state);
+                          int64_t* rec, const int64_t* state, int first_only);
 /* After the all-gather of the padded slices (x_pad: world * maxrows codes)
  * and the MAX all-reduce of rec: x[bounds[r] + i] = x_pad[r*maxrows + i]
  * (bounds: device u32[world+1]) and, unless done, state advances: steps++,
@@ -259,7 +261,18 @@ cyc_status cyc_shard_post(cyc_ctx* ctx, const int64_t* rec, int64_t* state, cons
  * rank changed more than cap rows — blocks the rest of the batch (state[4])
  * so the host completes that step with the dense exchange. */
 cyc_status cyc_shard_collect(cyc_ctx* ctx, uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out,
-                             uint32_t cap, uint32_t* sp, const int64_t* state);
+                             uint32_t cap, uint32_t* sp, const int64_t* state, int list_mode,
+                             const uint32_t* rlist, const uint32_t* rcnt, uint32_t* rbits,
+                             const uint64_t* acc_words, int64_t* rec);
+/* Frontier (push) step of the sparse protocol, steps after the first: from
+ * every rank's changes of the previous step (sp_all, already applied to x),
+ * raise this rank's targets in out (= x's slice) along the snapshot rows;
+ * raised rows go to rlist (local indices, count rcnt, dedup bitmap rbits of
+ * (hi-lo)/32+1 words, all device memory) for cyc_shard_collect(list_mode=1),
+ * which also produces the step record. Early-exit runs only. */
+cyc_status cyc_shard_push(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi, const uint32_t* sp_all,
+                          int world, uint32_t cap, const uint64_t* acc_words, uint32_t* out, uint32_t* rbits,
+                          uint32_t* rlist, uint32_t* rcnt, const int64_t* state);
 cyc_status cyc_shard_post_sparse(cyc_ctx* ctx, const int64_t* rec, int64_t* state, const uint32_t* sp_all,
                                  int world, uint32_t cap, uint32_t* x);
 /* used-bitmap demotion on a full replicated vector, entirely on device:

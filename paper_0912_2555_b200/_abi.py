@@ -162,9 +162,12 @@ _SIGS = {
     "cyc_flush_l2": (C.c_int, [_P, C.c_size_t]),
     "cyc_shard_bounds": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
     "cyc_map_trace": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
-    "cyc_shard_step": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, _P, _P, _P, _P, _P]),
+    "cyc_shard_step": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, _P, _P, _P, _P, _P, C.c_int]),
     "cyc_shard_post": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_uint32, _P]),
-    "cyc_shard_collect": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, C.c_uint32, _P, _P]),
+    "cyc_shard_collect": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, C.c_uint32, _P, _P, C.c_int, _P, _P,
+                                    _P, _P, _P]),
+    "cyc_shard_push": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, _P, C.c_int, C.c_uint32, _P, _P, _P, _P, _P,
+                                 _P]),
     "cyc_shard_post_sparse": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_uint32, _P]),
     "cyc_shard_demote": (C.c_int, [_P, _P, C.c_uint32, _P, _P, _P]),
     "cyc_fused_open": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(_P), _P]),

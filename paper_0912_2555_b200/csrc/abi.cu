@@ -921,7 +921,7 @@ cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes) {
 
 cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi,
                           const uint32_t* x, const uint64_t* acc_words, uint32_t* out, int64_t* rec,
-                          const int64_t* state) {
+                          const int64_t* state, int first_only) {
   return guard([&] {
     require(ctx && g && x && acc_words && rec && (out || hi <= lo), CYC_E_CONTRACT,
             "shard_step: null argument");
@@ -929,9 +929,10 @@ cyc_status cyc_shard_step(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_
     require(is_device_ptr(x) && is_device_ptr(acc_words) && is_device_ptr(rec) &&
                 (!state || is_device_ptr(state)),
             CYC_E_CONTRACT, "shard_step: vectors must be device memory");
+    require(!first_only || state, CYC_E_CONTRACT, "shard_step: first_only needs the state");
     cyc::launch_step_range(g->gath, lo, hi, x, reinterpret_cast<const uint32_t*>(acc_words), out,
                            reinterpret_cast<long long*>(rec), reinterpret_cast<const long long*>(state),
-                           ctx->s);
+                           first_only, ctx->s);
   });
 }
 
@@ -946,11 +947,30 @@ cyc_status cyc_shard_post(cyc_ctx* ctx, const int64_t* rec, int64_t* state, cons
 }
 
 cyc_status cyc_shard_collect(cyc_ctx* ctx, uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out,
-                             uint32_t cap, uint32_t* sp, const int64_t* state) {
+                             uint32_t cap, uint32_t* sp, const int64_t* state, int list_mode,
+                             const uint32_t* rlist, const uint32_t* rcnt, uint32_t* rbits,
+                             const uint64_t* acc_words, int64_t* rec) {
   return guard([&] {
     require(ctx && x && sp && state && (out || hi <= lo), CYC_E_CONTRACT, "shard_collect: null argument");
+    require(!list_mode || (rlist && rcnt && rbits && acc_words && rec), CYC_E_CONTRACT,
+            "shard_collect: list mode needs the raised list and the record");
     cyc::launch_shard_collect(lo, hi, x, out, cap, reinterpret_cast<uint2*>(sp),
-                              reinterpret_cast<const long long*>(state), ctx->s);
+                              reinterpret_cast<const long long*>(state), list_mode, rlist, rcnt, rbits,
+                              reinterpret_cast<const uint32_t*>(acc_words), reinterpret_cast<long long*>(rec),
+                              ctx->s);
+  });
+}
+
+cyc_status cyc_shard_push(cyc_ctx* ctx, const cyc_graph* g, uint32_t lo, uint32_t hi, const uint32_t* sp_all,
+                          int world, uint32_t cap, const uint64_t* acc_words, uint32_t* out, uint32_t* rbits,
+                          uint32_t* rlist, uint32_t* rcnt, const int64_t* state) {
+  return guard([&] {
+    require(ctx && g && sp_all && acc_words && out && rbits && rlist && rcnt && state && world >= 1,
+            CYC_E_CONTRACT, "shard_push: null argument");
+    require(lo <= hi && hi <= g->n(), CYC_E_CONTRACT, "shard_push: bad row range");
+    cyc::launch_shard_push(reinterpret_cast<const uint2*>(sp_all), world, cap, g->snap, lo, hi,
+                           reinterpret_cast<const uint32_t*>(acc_words), out, rbits, rlist, rcnt,
+                           reinterpret_cast<const long long*>(state), ctx->s);
   });
 }
 

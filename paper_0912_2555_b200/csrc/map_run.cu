@@ -944,6 +944,12 @@ __device__ __forceinline__ uint32_t cand_of(uint32_t u, const uint32_t* __restri
   return c;
 }
 
+// Range (pull) kernels skip when the fixpoint is decided, a sparse step is
+// blocked, or (first_only: the sparse protocol) a push step takes this step.
+__device__ __forceinline__ bool range_skip(const long long* st, int first_only) {
+  return st && (st[0] | st[4] | (first_only ? st[1] : 0));
+}
+
 __device__ __forceinline__ void shard_flags(bool ch, uint32_t wit, unsigned long long* rec) {
   wit = __reduce_min_sync(__activemask(), wit);
   if (__any_sync(__activemask(), ch) && lane_id() == 0) atomicMax(rec, 1ull);
@@ -953,8 +959,9 @@ __device__ __forceinline__ void shard_flags(bool ch, uint32_t wit, unsigned long
 __global__ void k_step_range(uint32_t lo, uint32_t hi, uint32_t heavy, const uint32_t* __restrict__ goff,
                              const uint32_t* __restrict__ gcol, const uint32_t* __restrict__ x,
                              const uint32_t* __restrict__ accw, uint32_t* __restrict__ out,
-                             unsigned long long* __restrict__ rec, const long long* __restrict__ state) {
-  if (state && (state[0] | state[4])) return;  // decided, or a sparse step awaits its dense completion
+                             unsigned long long* __restrict__ rec, const long long* __restrict__ state,
+                             int first_only) {
+  if (range_skip(state, first_only)) return;  // decided, blocked, or a push step follows
   const uint32_t stride = gridDim.x * blockDim.x;
   bool ch = false;
   uint32_t wit = kNone;
@@ -982,8 +989,8 @@ __global__ void k_step_range_ell(uint32_t lo, uint32_t hi, uint32_t n, uint32_t 
                                  const uint32_t* __restrict__ goff, const uint32_t* __restrict__ gcol,
                                  const uint32_t* __restrict__ x, const uint32_t* __restrict__ accw,
                                  uint32_t* __restrict__ out, unsigned long long* __restrict__ rec,
-                                 const long long* __restrict__ state) {
-  if (state && (state[0] | state[4])) return;
+                                 const long long* __restrict__ state, int first_only) {
+  if (range_skip(state, first_only)) return;
   const uint32_t stride = gridDim.x * blockDim.x;
   bool ch = false;
   uint32_t wit = kNone;
@@ -1014,8 +1021,8 @@ __global__ void k_step_range_ell(uint32_t lo, uint32_t hi, uint32_t n, uint32_t 
 __global__ void k_step_range_chunks(const uint4* __restrict__ chunks, uint32_t nch, uint32_t lo, uint32_t hi,
                                     const uint32_t* __restrict__ gcol, const uint32_t* __restrict__ x,
                                     const uint32_t* __restrict__ accw, uint32_t* __restrict__ out,
-                                    const long long* __restrict__ state) {
-  if (state && (state[0] | state[4])) return;
+                                    const long long* __restrict__ state, int first_only) {
+  if (range_skip(state, first_only)) return;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t k = gw; k < nch; k += nw) {
@@ -1031,8 +1038,9 @@ __global__ void k_step_range_chunks(const uint4* __restrict__ chunks, uint32_t n
 __global__ void k_step_range_heavy(const uint4* __restrict__ chunks, uint32_t nch, uint32_t lo, uint32_t hi,
                                    const uint32_t* __restrict__ goff, const uint32_t* __restrict__ x,
                                    const uint32_t* __restrict__ accw, const uint32_t* __restrict__ out,
-                                   unsigned long long* __restrict__ rec, const long long* __restrict__ state) {
-  if (state && (state[0] | state[4])) return;
+                                   unsigned long long* __restrict__ rec, const long long* __restrict__ state,
+                                   int first_only) {
+  if (range_skip(state, first_only)) return;
   bool chg = false;
   uint32_t wit = kNone;
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nch; k += gridDim.x * blockDim.x) {
@@ -1068,11 +1076,42 @@ __global__ void k_shard_post(const long long* __restrict__ rec, long long* state
 
 // Sparse exchange: this rank's changed rows as (v, value) after the step;
 // sp[0] = {count, 0}, entries sp[1..cap]; a count above cap marks overflow.
+// After a pull step (or list_mode off) the slice is scanned; after a push step
+// the raised list is read (and its bits cleared), and the step record comes
+// from it: changed = any raised, witness = min raised t with t accepting and
+// out[t] = t + 1 (early exit only: a self-valued row that is not raised now
+// would have stopped the fixpoint at an earlier step).
 __global__ void k_shard_collect(uint32_t lo, uint32_t hi, const uint32_t* __restrict__ x,
                                 const uint32_t* __restrict__ out, uint32_t cap, uint2* sp,
-                                const long long* __restrict__ state) {
+                                const long long* __restrict__ state, int list_mode,
+                                const uint32_t* __restrict__ rlist, const uint32_t* __restrict__ rcnt,
+                                uint32_t* rbits, const uint32_t* __restrict__ accw, unsigned long long* rec) {
   if (state[0] | state[4]) return;
   const uint32_t stride = gridDim.x * blockDim.x;
+  if (list_mode && state[1] != 0) {
+    const uint32_t k = *rcnt;
+    bool chg = false;
+    uint32_t wit = kNone;
+    for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; i0 < k; i0 += stride) {
+      const uint32_t i = i0 + lane_id();
+      const bool in = i < k;
+      const uint32_t t = in ? rlist[i] : 0u;  // local row index
+      const uint32_t v = lo + t, val = in ? out[t] : 0u;
+      if (in) {
+        atomicAnd(rbits + (t >> 5), ~(1u << (t & 31u)));
+        chg = true;
+        if (val == v + 1u && ((accw[v >> 5] >> (v & 31u)) & 1u)) wit = min(wit, v);
+      }
+      const uint32_t bal = __ballot_sync(kFull, in);
+      uint32_t base = 0;
+      if (lane_id() == 0) base = atomicAdd(&sp[0].x, (uint32_t)__popc(bal));
+      base = __shfl_sync(kFull, base, 0);
+      const uint32_t idx = base + __popc(bal & lanemask_lt());
+      if (in && idx < cap) sp[1 + idx] = make_uint2(v, val);
+    }
+    shard_flags(chg, wit, rec);
+    return;
+  }
   for (uint32_t v0 = lo + ((blockIdx.x * blockDim.x + threadIdx.x) & ~31u); v0 < hi; v0 += stride) {
     const uint32_t v = v0 + lane_id();
     const bool ch = v < hi && out[v - lo] != x[v];
@@ -1083,6 +1122,46 @@ __global__ void k_shard_collect(uint32_t lo, uint32_t hi, const uint32_t* __rest
     base = __shfl_sync(kFull, base, 0);
     const uint32_t idx = base + __popc(bal & lanemask_lt());
     if (ch && idx < cap) sp[1 + idx] = make_uint2(v, out[v - lo]);
+  }
+}
+
+// Sparse protocol, steps after the first: push from every rank's changes of
+// the previous step (sp_all, applied to x already) along the snapshot rows,
+// restricted to this rank's targets [lo, hi) (rows are sorted: two binary
+// searches per source). out holds x's slice; raised targets are listed once.
+__device__ __forceinline__ uint32_t lbound(const uint32_t* p, uint32_t len, uint32_t x) {
+  uint32_t lo = 0, hi = len;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_shard_push(const uint2* __restrict__ sp_all, int world, uint32_t cap,
+                             const uint32_t* __restrict__ soff, const uint32_t* __restrict__ scol, uint32_t lo,
+                             uint32_t hi, const uint32_t* __restrict__ accw, uint32_t* out, uint32_t* rbits,
+                             uint32_t* rlist, uint32_t* rcnt, const long long* __restrict__ state) {
+  if (state[0] | state[4] | (state[1] == 0)) return;
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t total = (uint64_t)world * cap;
+  for (uint64_t e = gw; e < total; e += nw) {
+    const uint32_t r = (uint32_t)(e / cap), i = (uint32_t)(e % cap);
+    const uint2* b = sp_all + (size_t)r * (cap + 1);
+    if (i >= b[0].x) continue;
+    const uint2 pr = b[1 + i];
+    const uint32_t u = pr.x;
+    const uint32_t cu = ((accw[u >> 5] >> (u & 31u)) & 1u) ? max(pr.y, u + 1u) : pr.y;
+    const uint32_t rb = soff[u], re = soff[u + 1];
+    const uint32_t s0 = rb + lbound(scol + rb, re - rb, lo), s1 = rb + lbound(scol + rb, re - rb, hi);
+    for (uint32_t k = s0 + lane; k < s1; k += 32u) {
+      const uint32_t t = scol[k] - lo;
+      if (cu > out[t] && atomicMax(out + t, cu) < cu) {
+        const uint32_t m = 1u << (t & 31u);
+        if (!(atomicOr(rbits + (t >> 5), m) & m)) rlist[atomicAdd(rcnt, 1u)] = t;
+      }
+    }
   }
 }
 
@@ -1313,7 +1392,7 @@ void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* acc
 
 void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint32_t* x,
                        const uint32_t* accw, uint32_t* out, long long* rec, const long long* state,
-                       cudaStream_t s) {
+                       int first_only, cudaStream_t s) {
   CYC_CUDA(cudaMemsetAsync(rec, 0, 16, s));
   if (hi <= lo) return;
   auto* r = reinterpret_cast<unsigned long long*>(rec);
@@ -1323,29 +1402,42 @@ void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint3
   const uint32_t* ell = gath.ell.as<uint32_t>();
   const uint32_t* ovf = gath.ovf.as<uint32_t>();
   switch (gath.ell_k) {
-    case 1: k_step_range_ell<1><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
-    case 2: k_step_range_ell<2><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
-    case 4: k_step_range_ell<4><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
-    case 8: k_step_range_ell<8><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state); break;
-    default: k_step_range<<<g, 256, 0, s>>>(lo, hi, heavy, gath.o(), gath.c(), x, accw, out, r, state); break;
+    case 1: k_step_range_ell<1><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state, first_only); break;
+    case 2: k_step_range_ell<2><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state, first_only); break;
+    case 4: k_step_range_ell<4><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state, first_only); break;
+    case 8: k_step_range_ell<8><<<g, 256, 0, s>>>(lo, hi, n, np, heavy, ell, ovf, gath.o(), gath.c(), x, accw, out, r, state, first_only); break;
+    default: k_step_range<<<g, 256, 0, s>>>(lo, hi, heavy, gath.o(), gath.c(), x, accw, out, r, state, first_only); break;
   }
   CYC_LAUNCHED();
   if (gath.n_heavy_chunks) {
     const uint32_t nch = gath.n_heavy_chunks;
     k_step_range_chunks<<<grid_for((uint64_t)nch * 32, 256, 8), 256, 0, s>>>(
-        gath.heavy.as<uint4>(), nch, lo, hi, gath.c(), x, accw, out, state);
+        gath.heavy.as<uint4>(), nch, lo, hi, gath.c(), x, accw, out, state, first_only);
     CYC_LAUNCHED();
     k_step_range_heavy<<<grid_for(nch, 256, 4), 256, 0, s>>>(gath.heavy.as<uint4>(), nch, lo, hi, gath.o(), x,
-                                                             accw, out, r, state);
+                                                             accw, out, r, state, first_only);
     CYC_LAUNCHED();
   }
 }
 
 void launch_shard_collect(uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out, uint32_t cap,
-                          uint2* sp, const long long* state, cudaStream_t s) {
+                          uint2* sp, const long long* state, int list_mode, const uint32_t* rlist,
+                          const uint32_t* rcnt, uint32_t* rbits, const uint32_t* accw, long long* rec,
+                          cudaStream_t s) {
   CYC_CUDA(cudaMemsetAsync(sp, 0, 8, s));
   if (hi <= lo) return;
-  k_shard_collect<<<grid_for(hi - lo, 256, 8), 256, 0, s>>>(lo, hi, x, out, cap, sp, state);
+  k_shard_collect<<<grid_for(hi - lo, 256, 8), 256, 0, s>>>(lo, hi, x, out, cap, sp, state, list_mode, rlist, rcnt,
+                                                            rbits, accw,
+                                                            reinterpret_cast<unsigned long long*>(rec));
+  CYC_LAUNCHED();
+}
+
+void launch_shard_push(const uint2* sp_all, int world, uint32_t cap, const DevCsr& snap, uint32_t lo, uint32_t hi,
+                       const uint32_t* accw, uint32_t* out, uint32_t* rbits, uint32_t* rlist, uint32_t* rcnt,
+                       const long long* state, cudaStream_t s) {
+  CYC_CUDA(cudaMemsetAsync(rcnt, 0, 4, s));
+  k_shard_push<<<grid_for((uint64_t)world * cap * 32 + 32, 256, 8), 256, 0, s>>>(
+      sp_all, world, cap, snap.o(), snap.c(), lo, hi, accw, out, rbits, rlist, rcnt, state);
   CYC_LAUNCHED();
 }
 

@@ -105,11 +105,16 @@ void launch_step_pull(const DevCsr& gath, const uint32_t* x, const uint32_t* acc
 // UINT32_MAX - min witness} as int64 (MAX-reducible); no-op when state[0].
 void launch_step_range(const DevCsr& gath, uint32_t lo, uint32_t hi, const uint32_t* x,
                        const uint32_t* accw, uint32_t* out, long long* rec, const long long* state,
-                       cudaStream_t s);
+                       int first_only, cudaStream_t s);
 // Sparse exchange: changed rows of [lo, hi) into sp (sp[0] = count) and the
 // post step applying every rank's changes (or flagging overflow).
 void launch_shard_collect(uint32_t lo, uint32_t hi, const uint32_t* x, const uint32_t* out, uint32_t cap,
-                          uint2* sp, const long long* state, cudaStream_t s);
+                          uint2* sp, const long long* state, int list_mode, const uint32_t* rlist,
+                          const uint32_t* rcnt, uint32_t* rbits, const uint32_t* accw, long long* rec,
+                          cudaStream_t s);
+void launch_shard_push(const uint2* sp_all, int world, uint32_t cap, const DevCsr& snap, uint32_t lo, uint32_t hi,
+                       const uint32_t* accw, uint32_t* out, uint32_t* rbits, uint32_t* rlist, uint32_t* rcnt,
+                       const long long* state, cudaStream_t s);
 void launch_shard_post_sparse(const long long* rec, long long* state, const uint2* sp_all, int world,
                               uint32_t cap, uint32_t* x, cudaStream_t s);
 // Unpads the gathered slices into x and advances the sharded fixpoint state.

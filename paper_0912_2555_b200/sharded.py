@@ -85,19 +85,28 @@ class CudaShardBackend:
     def prepare(self, bounds):
         self.bounds = self.torch.tensor(np.asarray(bounds, np.int64).astype(np.int32), device=self.device)
 
-    def step(self, x, acc, lo: int, hi: int, out, rec, state=None):
+    def step(self, x, acc, lo: int, hi: int, out, rec, state=None, first_only: bool = False):
         _abi.check(_abi.lib().cyc_shard_step(self.snap.context.handle, self.snap.handle, lo, hi,
                                              _abi.ptr(x), _abi.ptr(acc), _abi.ptr(out), _abi.ptr(rec),
-                                             None if state is None else _abi.ptr(state)))
+                                             None if state is None else _abi.ptr(state), int(first_only)))
+
+    def push(self, sp_all, world: int, cap: int, acc, lo: int, hi: int, out, rbits, rlist, rcnt, state):
+        _abi.check(_abi.lib().cyc_shard_push(self.snap.context.handle, self.snap.handle, lo, hi, _abi.ptr(sp_all),
+                                             world, cap, _abi.ptr(acc), _abi.ptr(out), _abi.ptr(rbits),
+                                             _abi.ptr(rlist), _abi.ptr(rcnt), _abi.ptr(state)))
 
     def post(self, rec, state, x_pad, world: int, maxrows: int, x):
         _abi.check(_abi.lib().cyc_shard_post(self.snap.context.handle, _abi.ptr(rec), _abi.ptr(state),
                                              _abi.ptr(x_pad), _abi.ptr(self.bounds), world, maxrows,
                                              _abi.ptr(x)))
 
-    def collect(self, lo: int, hi: int, x, out, cap: int, sp, state):
+    def collect(self, lo: int, hi: int, x, out, cap: int, sp, state, lists=None):
+        """lists = (rlist, rcnt, rbits, acc, rec): list mode after push steps."""
+        rl, rc, rb, acc, rec = lists if lists is not None else (None,) * 5
         _abi.check(_abi.lib().cyc_shard_collect(self.snap.context.handle, lo, hi, _abi.ptr(x), _abi.ptr(out),
-                                                cap, _abi.ptr(sp), _abi.ptr(state)))
+                                                cap, _abi.ptr(sp), _abi.ptr(state), int(lists is not None),
+                                                _abi.ptr(rl), _abi.ptr(rc), _abi.ptr(rb), _abi.ptr(acc),
+                                                _abi.ptr(rec)))
 
     def post_sparse(self, rec, state, sp_all, world: int, cap: int, x):
         _abi.check(_abi.lib().cyc_shard_post_sparse(self.snap.context.handle, _abi.ptr(rec), _abi.ptr(state),
@@ -167,6 +176,10 @@ class _Runner:
         self.cap = int(cap) if cap is not None else max(4096, self.maxrows // 32)
         self.sp = backend.zeros(2 * (self.cap + 1))                 # uint2[cap+1] as int32 pairs
         self.sp_all = backend.zeros(world * 2 * (self.cap + 1))
+        rows = self.hi - self.lo
+        self.rbits = backend.zeros(rows // 32 + 2)                  # raised-row dedup bitmap
+        self.rlist = backend.zeros(rows + 1)                        # raised local rows
+        self.rcnt = backend.zeros(1)
         self.graphs = ({"dense": _StepGraphs(backend, self.one_dense),
                         "sparse": _StepGraphs(backend, self.one_sparse)} if graphs else None)
 
@@ -178,17 +191,25 @@ class _Runner:
         be.post(self.rec, self.state, self.x_pad, self.world, self.maxrows, self.x)
 
     def one_sparse(self):
+        """Pull at the fixpoint's first step, then frontier pushes from the
+        previous step's gathered changes; changed-only exchange."""
         be, d = self.be, self.dist
-        be.step(self.x, self.acc, self.lo, self.hi, self.send, self.rec, self.state)
-        be.collect(self.lo, self.hi, self.x, self.send, self.cap, self.sp, self.state)
+        be.step(self.x, self.acc, self.lo, self.hi, self.send, self.rec, self.state, first_only=True)
+        be.push(self.sp_all, self.world, self.cap, self.acc, self.lo, self.hi, self.send, self.rbits, self.rlist,
+                self.rcnt, self.state)
+        be.collect(self.lo, self.hi, self.x, self.send, self.cap, self.sp, self.state,
+                   (self.rlist, self.rcnt, self.rbits, self.acc, self.rec))
         d.all_gather_into_tensor(self.sp_all, self.sp, group=self.group)
         d.all_reduce(self.rec, op=d.ReduceOp.MAX, group=self.group)
         be.post_sparse(self.rec, self.state, self.sp_all, self.world, self.cap, self.x)
 
     def complete_dense(self):
-        """Dense exchange of the step a sparse batch could not apply."""
+        """Dense exchange of the step a sparse batch could not apply (the
+        fixpoint then continues dense: the partial change lists cannot seed a
+        push step)."""
         d = self.dist
         self.state[4] = 0
+        self.rbits.zero_()
         self.rec.copy_(self.state[6:8])
         d.all_gather_into_tensor(self.x_pad, self.send[: self.maxrows], group=self.group)
         self.be.post(self.rec, self.state, self.x_pad, self.world, self.maxrows, self.x)
@@ -235,9 +256,10 @@ def run_map_sharded(backend, dist, rank: int, world: int, bounds, acc_words: np.
     fsize = int(np.bitwise_count(words).sum())
     guess = 4
     ex = stats.device["exchange"] = {"dense_batches": 0, "sparse_batches": 0, "dense_completions": 0}
-    sparse_ok = exchange != "dense"
+    sparse_ok = exchange != "dense" and early_exit
     while fsize > 0:  # front.any()
         x.zero_()
+        rn.rbits.zero_()
         state.zero_()
         state[2] = _NONE
         state[3] = int(early_exit)
@@ -250,8 +272,8 @@ def run_map_sharded(backend, dist, rank: int, world: int, bounds, acc_words: np.
             if st[4]:  # a sparse step overflowed: complete it densely
                 rn.complete_dense()
                 ex["dense_completions"] += 1
+                mode = "dense"
                 if exchange == "auto":
-                    mode = "dense"
                     sparse_ok = False
                 st = [int(v) for v in state.cpu()]
             done, steps, witness = st[0], st[1], st[2]

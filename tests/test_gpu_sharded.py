@@ -59,7 +59,7 @@ def test_cuda_shard_backend_matches_run_map(eng, R, nccl):
         for early in (True, False):
             # eager launches and captured CUDA-graph batches, dense / sparse
             # (capacity 7: overflow and dense completion) / auto exchange
-            exchange, cap = [("auto", None), ("sparse", 7), ("dense", None), ("auto", 3)][(2 * t + early) % 4]
+            exchange, cap = [("auto", None), ("sparse", None), ("dense", None), ("sparse", 7)][(2 * t + early) % 4]
             res = sharded.run_map_sharded(be, nccl, 0, 1, [0, n], words, early, graphs=bool(t % 2),
                                           exchange=exchange, sparse_cap=cap)
             ref = R.run_map(R.transpose(R.build_snapshot(n, e, True)), words, early)

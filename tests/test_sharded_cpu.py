@@ -18,12 +18,14 @@ class HostShardBackend:
 
     NONE = 0xFFFFFFFF
 
-    def __init__(self, R, gather, n):
+    def __init__(self, R, gather, n, snap=None):
         self.torch = torch
         self.R = R
         self.gather = gather
+        self.snap = snap if snap is not None else R.transpose(gather)  # push side rows
         self.n = n
         self.bounds = None
+        self.raised = []
 
     def zeros(self, k, dtype=None):
         return torch.zeros(max(k, 1), dtype=dtype or torch.int32)
@@ -34,9 +36,9 @@ class HostShardBackend:
     def prepare(self, bounds):
         self.bounds = [int(b) for b in bounds]
 
-    def step(self, x, acc, lo, hi, out, rec, state=None):
+    def step(self, x, acc, lo, hi, out, rec, state=None, first_only=False):
         rec.zero_()
-        if state is not None and (int(state[0]) or int(state[4])):
+        if state is not None and (int(state[0]) or int(state[4]) or (first_only and int(state[1]))):
             return
         xv = x.numpy().view(np.uint32)[: self.n]
         words = acc.numpy().view(np.uint64)
@@ -60,9 +62,48 @@ class HostShardBackend:
                 state[0] = 1
                 state[2] = wit
 
-    def collect(self, lo, hi, x, out, cap, sp, state):
+    def push(self, sp_all, world, cap, acc, lo, hi, out, rbits, rlist, rcnt, state):
+        self.raised = []
+        if int(state[0]) or int(state[4]) or int(state[1]) == 0:
+            return
+        words = acc.numpy().view(np.uint64)
+        a = sp_all.numpy().reshape(world, cap + 1, 2)
+        o = out.numpy()
+        seen = set()
+        for r in range(world):
+            c = int(a[r, 0, 0]) & 0xFFFFFFFF
+            for i in range(c):
+                u, val = int(a[r, 1 + i, 0]), int(a[r, 1 + i, 1])
+                if (int(words[u >> 6]) >> (u & 63)) & 1:
+                    val = max(val, u + 1)
+                for t in self.snap.col[self.snap.off[u]: self.snap.off[u + 1]].tolist():
+                    if lo <= t < hi and val > int(o[t - lo]):
+                        o[t - lo] = val
+                        if t not in seen:
+                            seen.add(t)
+                            self.raised.append(t - lo)
+
+    def collect(self, lo, hi, x, out, cap, sp, state, lists=None):
         sp.zero_()
         if int(state[0]) or int(state[4]):
+            return
+        if lists is not None and int(state[1]) != 0:
+            rec = lists[4]
+            words = lists[3].numpy().view(np.uint64)
+            o = out.numpy()
+            sp[0] = len(self.raised)
+            wit = None
+            for i, t in enumerate(self.raised):
+                v, val = lo + t, int(o[t])
+                if i < cap:
+                    sp[2 + 2 * i] = v
+                    sp[3 + 2 * i] = val
+                if val == v + 1 and (int(words[v >> 6]) >> (v & 63)) & 1:
+                    wit = v if wit is None else min(wit, v)
+            if self.raised:
+                rec[0] = max(int(rec[0]), 1)
+            if wit is not None:
+                rec[1] = max(int(rec[1]), self.NONE - wit)
             return
         xv = x.numpy()[lo:hi]
         ov = out.numpy()[: hi - lo]
@@ -120,9 +161,9 @@ def _worker(rank, world, port, cases, q):
     for t, (n, edges, accw, early) in enumerate(cases):
         gat = R.transpose(R.build_snapshot(n, edges, True))
         bounds = sharded.shard_bounds(gat.off, world)
-        be = HostShardBackend(R, gat, n)
+        be = HostShardBackend(R, gat, n, R.build_snapshot(n, edges, True))
         # dense, sparse with overflow fallbacks (tiny capacity) and auto
-        exchange, cap = [("dense", None), ("sparse", 3), ("auto", None), ("auto", 1)][t % 4]
+        exchange, cap = [("dense", None), ("sparse", 3), ("auto", None), ("sparse", None), ("auto", 1)][t % 5]
         res = sharded.run_map_sharded(be, dist, rank, world, bounds, accw, early, exchange=exchange,
                                       sparse_cap=cap)
         out.append((res.verdict.cycle_found(), res.verdict.witness, res.stats.iterations,
@@ -140,7 +181,7 @@ def _cases():
     R = oracle.Restatement()
     rng = np.random.default_rng(88)
     cases = []
-    for t in range(6):
+    for t in range(10):
         n = int(rng.integers(20, 400))
         e = rng.integers(0, n, size=(int(n * rng.choice([1, 2, 3])), 2)).astype(np.uint32)
         acc = rng.random(n) < [0.05, 0.3][t % 2]
