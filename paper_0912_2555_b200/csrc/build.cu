@@ -2,15 +2,17 @@
 //
 // Replaces build_snapshot (reference graph.cpp:63-105) and the gather-index
 // construction of MaxPropagation (map_engine.cpp:9-19). Both are
-// single-threaded counting sorts on the CPU; here the same three phases run
-// as HBM-bound kernels over the whole log:
-//   1. row histogram     (atomics, warp-aggregated with match_any for hubs)
-//   2. exclusive scan    (reduce-then-scan, 3 launches)
-//   3. bucket scatter    (atomic cursors counting down from row ends)
-//   4. per-row sort+dedup, by row-length class: registers (<=16), one CTA in
-//      shared memory (<=4096), one CTA with a shared-memory-tiled bitonic
-//      network over global memory (larger hub rows)
-//   5. scan of unique counts, compaction into the final CSR.
+// single-threaded counting sorts on the CPU; here the phases run as
+// HBM-bound kernels over the whole log:
+//   1. bucket histogram (2^14 rows per bucket, shared-memory counters)
+//   2. two-pass partition: log -> 64-bucket super-buckets -> buckets, in
+//      sub-chunks held in registers (contiguous runs per bin)
+//   3. one CTA per bucket counting-sorts its rows in shared memory
+//   4. per-row sort+dedup by length: registers (<=16), one warp in registers
+//      (<=512), longer rows by an MSD split into ~256-value sub-buckets sorted
+//      by warps (CTA fallback for overfull ones)
+//   5. scan of unique counts, warp-flattened compaction into the final CSR.
+// (n > 2^28: a flat atomic counting sort replaces 1-3.)
 // Row offsets are u32 (snapshot edges < 2^32; checked by the caller).
 #include <algorithm>
 #include <chrono>

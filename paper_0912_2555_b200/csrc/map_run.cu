@@ -14,8 +14,10 @@
 // x_{k-2}, which differs from x_{k-1} exactly at the vertices changed in
 // step k-1 — the frontier, kept as a bitmap. Two step kinds:
 //   pull  dense over all rows of the gather index (the north_star SpMV in
-//         the (max, vertex-id) semiring); each lane walks kRows rows in
-//         lock-step so it keeps several independent gathers in flight.
+//         the (max, vertex-id) semiring); each lane walks R rows of the
+//         column-major HYB slab in lock-step (several independent gathers in
+//         flight); rows longer than kHeavyDeg as kHeavyChunk-edge warp chunks
+//         (grouped by L2-sized column blocks on large graphs).
 //   push  only frontier vertices act: each max-copies its own x_{k-1} into
 //         P[cur^1] and scatters cand = max(x_{k-1}[u], u+1 if accepting) to
 //         its targets with atomicMax. A vertex that did not change cannot
@@ -24,8 +26,8 @@
 // a one-bit-per-word summary so a sparse frontier is found without scanning
 // all n/32 words); vertices of push degree > kBigDeg are also split into
 // kChunk-edge chunks expanded by whole warps. The step kind is chosen on the
-// device from the frontier's edge count (push when edges * alpha < m):
-// direction-optimising traversal.
+// device from the frontier's edge count (push when edges * alpha < m,
+// alpha 16 by default): direction-optimising traversal.
 //
 // Self-witness (map_engine.cpp:66): exact per row in pull; push (and heavy
 // pull rows) record raises to exactly v+1 of accepting v as candidates,
