@@ -143,18 +143,18 @@ __device__ bool has_self_loop(const uint32_t* off, const uint32_t* col, uint32_t
   return false;
 }
 
-// per root r (colour r+1): size and {has accepting, has self-loop}; lanes
-// sharing a root (one giant SCC on R-MAT) combine before the atomics
-__global__ void k_scc_stats(uint32_t n, const uint32_t* __restrict__ soff,
-                            const uint32_t* __restrict__ scol, const uint64_t* __restrict__ acc,
-                            const uint32_t* inscc, const uint32_t* color, uint32_t* rsize,
-                            uint32_t* rflag) {
+// per root r (colour r+1): size and "has an accepting vertex"; lanes sharing
+// a root (one giant SCC on R-MAT) combine before the atomics. The self-loop
+// test only matters for singleton SCCs, i.e. the root alone: k_scc_apply
+// does it there (one binary search per singleton, not one per vertex).
+__global__ void k_scc_stats(uint32_t n, const uint64_t* __restrict__ acc, const uint32_t* inscc,
+                            const uint32_t* color, uint32_t* rsize, uint32_t* rflag) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
     const uint32_t v = v0 + lane_id();
     const bool in = v < n && bit(inscc, v);
     const uint32_t r = in ? color[v] - 1u : kNone;
-    const uint32_t f = in ? ((accb(acc, v) ? 1u : 0u) | (has_self_loop(soff, scol, v) ? 2u : 0u)) : 0u;
+    const uint32_t f = in && accb(acc, v) ? 1u : 0u;
     const uint32_t peers = __match_any_sync(kFull, r);
     const uint32_t fo = __reduce_or_sync(peers, f);
     if (in && (peers & lanemask_lt()) == 0) {  // lowest lane of the group
@@ -164,13 +164,15 @@ __global__ void k_scc_stats(uint32_t n, const uint32_t* __restrict__ soff,
   }
 }
 
-__global__ void k_scc_apply(uint32_t n, const uint32_t* color, uint32_t* rsize, uint32_t* rflag,
-                            const uint32_t* inscc, uint8_t* active, uint8_t* keep, uint32_t* flag) {
+__global__ void k_scc_apply(uint32_t n, const uint32_t* __restrict__ soff, const uint32_t* __restrict__ scol,
+                            const uint32_t* color, uint32_t* rsize, uint32_t* rflag, const uint32_t* inscc,
+                            uint8_t* active, uint8_t* keep, uint32_t* flag) {
   bool any = false;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     if (bit(inscc, v)) {
       const uint32_t r = color[v] - 1u;
-      keep[v] = (rflag[r] & 1u) && (rsize[r] >= 2u || (rflag[r] & 2u));
+      const uint32_t sz = rsize[r];
+      keep[v] = (rflag[r] & 1u) && (sz >= 2u || has_self_loop(soff, scol, v));
       active[v] = 0;
     }
     any |= active[v] != 0;
@@ -582,12 +584,12 @@ void scc_keep_mask(const DevCsr& snap_in, const DevCsr& gath_in, const uint64_t*
     k_clear_roots<<<grid, kT, 0, s>>>(n, color.as<uint32_t>(), inscc.as<uint32_t>(), rsize.as<uint32_t>(),
                                       rflag.as<uint32_t>());
     CYC_LAUNCHED();
-    k_scc_stats<<<grid, kT, 0, s>>>(n, A.o(), A.c(), acc, inscc.as<uint32_t>(), color.as<uint32_t>(),
-                                    rsize.as<uint32_t>(), rflag.as<uint32_t>());
+    k_scc_stats<<<grid, kT, 0, s>>>(n, acc, inscc.as<uint32_t>(), color.as<uint32_t>(), rsize.as<uint32_t>(),
+                                    rflag.as<uint32_t>());
     CYC_LAUNCHED();
     uint32_t any = 0;
     CYC_CUDA(cudaMemsetAsync(f, 0, 4, s));
-    k_scc_apply<<<grid, kT, 0, s>>>(n, color.as<uint32_t>(), rsize.as<uint32_t>(), rflag.as<uint32_t>(),
+    k_scc_apply<<<grid, kT, 0, s>>>(n, A.o(), A.c(), color.as<uint32_t>(), rsize.as<uint32_t>(), rflag.as<uint32_t>(),
                                     inscc.as<uint32_t>(), active.as<uint8_t>(), keep, f);
     CYC_LAUNCHED();
     CYC_CUDA(cudaMemcpyAsync(&any, f, 4, cudaMemcpyDeviceToHost, s));
