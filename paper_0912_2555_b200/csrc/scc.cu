@@ -628,6 +628,7 @@ void restrict_graph(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc,
   const size_t nwd = (size_t)n / 32 + 2;
   DevBuf keep((size_t)n + 1, s), kb(nwd * 4, s), pc(nwd * 4, s), wp((nwd + 1) * 4, s), scratch;
   scc_keep_mask(snap, gath, acc, s, keep.as<uint8_t>());
+  SccLog lg;
   CYC_CUDA(cudaMemsetAsync(kb.p, 0, nwd * 4, s));
   CYC_CUDA(cudaMemsetAsync(pc.p, 0, nwd * 4, s));
   if (n) {
@@ -644,8 +645,11 @@ void restrict_graph(const DevCsr& snap, const DevCsr& gath, const uint64_t* acc,
     k_kept_list<<<grid_for(n, kT, 8), kT, 0, s>>>(n, kb.as<uint32_t>(), wp.as<uint32_t>(), out_kept.as<uint32_t>());
     CYC_LAUNCHED();
   }
+  lg.mark("kept-list", 1);
   filter_csr(snap, kb.as<uint32_t>(), wp.as<uint32_t>(), out_kept.as<uint32_t>(), k, s, out_snap);
+  lg.mark("filter-snap", 1);
   filter_csr(gath, kb.as<uint32_t>(), wp.as<uint32_t>(), out_kept.as<uint32_t>(), k, s, out_gath);
+  lg.mark("filter-gath", 1);
   const size_t words = ((size_t)k + 63) / 64;
   out_acc.alloc((words + 1) * 8, s);
   CYC_CUDA(cudaMemsetAsync(out_acc.p, 0, (words + 1) * 8, s));
