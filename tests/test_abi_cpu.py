@@ -42,7 +42,7 @@ def test_library_is_sm100a_only():
 
 
 def test_generator_presets_match_oracle(eng, R):
-    for idx in (1, 2, 3, 5):
+    for idx in (1, 2, 3, 4, 5):
         a, b = eng.preset(idx), R.preset(idx)
         for f, _ in a._fields_:
             assert getattr(a, f) == getattr(b, f), (idx, f)
