@@ -680,3 +680,36 @@ def test_build_long_rows_edge_cases(eng, R):
         off, col = s.gather_index()
         gt = R.transpose(g)
         assert np.array_equal(off, gt.off) and np.array_equal(col, gt.col)
+
+
+def test_fuzz_all_entry_points(eng, R, REF):
+    """Randomised sweep over graph shapes (self loops, duplicate edges,
+    isolated vertices, hubs in either CSR, 0-60 % accepting, both
+    orientations): run_map in every step kind and both early-exit modes,
+    restriction, OWCTY and the SCC verdict against the oracle / reference."""
+    rng = np.random.default_rng(0xF022)
+    for t in range(40):
+        n = int(rng.integers(1, 3000))
+        m = int(rng.integers(0, 6 * n + 1))
+        e = rng.integers(0, n, size=(m, 2)).astype(np.uint32)
+        if t % 3 == 0 and n > 1:  # self loops and duplicates
+            k = int(rng.integers(1, 20))
+            v = rng.integers(0, n, size=k).astype(np.uint32)
+            e = np.concatenate([e, np.stack([v, v], 1), e[: min(len(e), 50)]])
+        if t % 4 == 1:
+            e = random_graph(rng, n, len(e), hubs=2)
+        acc = rng.random(n) < rng.choice([0.0, 0.01, 0.1, 0.6])
+        tr = bool(t % 2)
+        s = snap_of(eng, n, e, acc, tr)
+        g = R.build_snapshot(n, e, tr)
+        gat = R.transpose(g)
+        for early in (True, False):
+            ref = R.run_map(gat, acc, early)
+            for mode in MODES:
+                assert_same_run(eng.run_map_detailed(s, acc, eng.MapOptions(early_exit=early, mode=mode)), ref)
+        r = eng.restrict_to_accepting_sccs(s)
+        _, _, kept = R.restrict(g, acc)
+        assert np.array_equal(r.kept, kept)
+        v, st = eng.run_owcty(s)
+        assert (v.cycle_found(), v.witness, st.outer_iterations, st.final_size) == R.run_owcty(g, acc)
+        assert eng.scc_verdict(s).verdict.cycle_found() == REF.snapshot(n, e, acc, tr).scc_verdict()
