@@ -468,39 +468,64 @@ __global__ void __launch_bounds__(kPartThreads) k_bucket_hist(const uint2* __res
                                                               uint32_t n, int key_dst, uint32_t sh,
                                                               uint32_t nb, uint64_t per_block,
                                                               uint32_t* __restrict__ bcnt,
-                                                              uint32_t* __restrict__ err) {
+                                                              uint32_t* __restrict__ err,
+                                                              unsigned long long* __restrict__ changes) {
+  // also counts log positions whose bucket differs from the previous one
+  // (adjacent lanes), i.e. how many bucket runs the log order has
   extern __shared__ uint32_t h[];
+  __shared__ uint32_t sh_changes;
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+  if (threadIdx.x == 0) sh_changes = 0;
   __syncthreads();
   const uint64_t lo = blockIdx.x * per_block, hi = min(m, lo + per_block);
-  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const uint2 e = edges[i];
-    if (e.x >= n || e.y >= n) {
-      *err = 1u;
-      continue;
+  uint32_t my_changes = 0;
+  for (uint64_t i0 = lo; i0 < hi; i0 += blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    uint32_t bk = 0xFFFFFFFFu;
+    if (i < hi) {
+      const uint2 e = edges[i];
+      if (e.x >= n || e.y >= n) {
+        *err = 1u;
+      } else {
+        bk = (key_dst ? e.y : e.x) >> sh;
+        atomicAdd(&h[bk], 1u);
+      }
     }
-    atomicAdd(&h[(key_dst ? e.y : e.x) >> sh], 1u);
+    const uint32_t prev = __shfl_up_sync(kFull, bk, 1);
+    my_changes += __popc(__ballot_sync(kFull, (threadIdx.x & 31u) && bk != prev && i < hi));
   }
+  if ((threadIdx.x & 31u) == 0 && my_changes) atomicAdd(&sh_changes, my_changes);
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
     if (h[b]) atomicAdd(bcnt + b, h[b]);
+  if (threadIdx.x == 0 && sh_changes) atomicAdd(changes, (unsigned long long)sh_changes);
 }
 
-// Two-pass partition: pass 1 to super-buckets of 2^kSuperLog buckets, pass
-// 2 from super-bucket order to bucket order. A single high-radix pass wrote
-// to nb x blocks interleaved streams (4096 x 296 on config 3): L2 lines were
-// evicted half-written, costing ~3x the payload in DRAM traffic. Each block
+// Multi-pass MSD partition of the log into bucket order, kDigit bits of the
+// bucket id per pass (the first pass takes the remainder). Measured on
+// config 3 (1.07 G pairs, 4096 buckets): a pass costs ~5-6 ms at fan-out 16
+// but 8-21 ms at fan-out 64 and ~28 ms at 1024 (more concurrently open
+// output regions spread over the array); a single pass at fan-out 4096 wrote
+// L2 lines half-filled and paid ~3x the payload in DRAM traffic. Each block
 // works on kSubChunk-element sub-chunks (histogram, one reservation per bin,
 // scatter) so the second read of a sub-chunk hits L2 and every bin receives a
 // contiguous run.
-constexpr uint32_t kSuperLog = 6;
+constexpr uint32_t kDigitDefault = 4;
+static uint32_t part_digit() {
+  static const uint32_t v = [] {
+    const char* e = getenv("CYC_PART_DIGIT");  // tuning knob
+    const uint32_t d = e ? (uint32_t)atoi(e) : kDigitDefault;
+    return d >= 1 && d <= 14 ? d : kDigitDefault;
+  }();
+  return v;
+}
 constexpr uint32_t kSubChunk = 16384;
 
 template <bool FROM_EDGES>
 __global__ void __launch_bounds__(kPartThreads) k_part(const void* __restrict__ in, uint64_t m, uint32_t n,
                                                        int key_dst, uint32_t shift, uint32_t nbins,
                                                        uint32_t* __restrict__ cursor,
-                                                       unsigned long long* __restrict__ out) {
+                                                       unsigned long long* __restrict__ out, uint32_t slog) {
   // each thread keeps its kPer elements of the sub-chunk in registers between
   // the histogram and the scatter (16 independent loads in flight, one read)
   constexpr uint32_t kPer = kSubChunk / kPartThreads;
@@ -508,28 +533,31 @@ __global__ void __launch_bounds__(kPartThreads) k_part(const void* __restrict__ 
   const uint64_t nsub = (m + kSubChunk - 1) / kSubChunk;
   for (uint64_t c = blockIdx.x; c < nsub; c += gridDim.x) {
     const uint64_t lo = c * kSubChunk, hi = min(m, lo + kSubChunk);
-    // pass 2 input is in super-bucket order: only the bins of the super-buckets
-    // between the sub-chunk's first and last element can occur
+    // later passes: the input is sorted by bin >> slog, so only the bins of
+    // the groups between the sub-chunk's first and last element can occur
     uint32_t b0 = 0, b1 = nbins;
     if (!FROM_EDGES) {
       const unsigned long long* t = reinterpret_cast<const unsigned long long*>(in);
-      b0 = (((uint32_t)(t[lo] >> 32) >> shift) >> kSuperLog) << kSuperLog;
-      b1 = min(nbins, ((((uint32_t)(t[hi - 1] >> 32) >> shift) >> kSuperLog) + 1) << kSuperLog);
+      b0 = (((uint32_t)(t[lo] >> 32) >> shift) >> slog) << slog;
+      b1 = min(nbins, ((((uint32_t)(t[hi - 1] >> 32) >> shift) >> slog) + 1) << slog);
     }
     for (uint32_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) h[b - b0] = 0;
+    // all kPer loads are issued before any is used (a use between loads made
+    // the compiler wait on each one in turn); edges are validated afterwards
+    const unsigned long long* raw = reinterpret_cast<const unsigned long long*>(in);
     unsigned long long v[kPer];
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k) {
       const uint64_t i = lo + k * kPartThreads + threadIdx.x;
-      v[k] = ~0ull;  // invalid / past the end
-      if (i < hi) {
-        if (FROM_EDGES) {
-          const uint2 e = reinterpret_cast<const uint2*>(in)[i];
-          const uint32_t row = key_dst ? e.y : e.x, other = key_dst ? e.x : e.y;
-          if (e.x < n && e.y < n) v[k] = ((unsigned long long)row << 32) | other;
-        } else {
-          v[k] = reinterpret_cast<const unsigned long long*>(in)[i];
-        }
+      v[k] = i < hi ? __ldg(raw + i) : ~0ull;
+    }
+    if (FROM_EDGES) {
+#pragma unroll
+      for (uint32_t k = 0; k < kPer; ++k) {
+        if (v[k] == ~0ull) continue;
+        const uint32_t x = (uint32_t)v[k], y = (uint32_t)(v[k] >> 32);  // uint2 {src, dst}
+        const uint32_t row = key_dst ? y : x, other = key_dst ? x : y;
+        v[k] = (x < n && y < n) ? ((unsigned long long)row << 32) | other : ~0ull;
       }
     }
     __syncthreads();
@@ -542,16 +570,28 @@ __global__ void __launch_bounds__(kPartThreads) k_part(const void* __restrict__ 
       h[b - b0] = x ? atomicAdd(cursor + b, x) : 0u;
     }
     __syncthreads();
+    // reserve every slot first, then store: the stores no longer wait on
+    // each shared-memory atomic in turn
+    constexpr uint32_t kBatch = 8;
 #pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k)
-      if (v[k] != ~0ull) out[atomicAdd(&h[((uint32_t)(v[k] >> 32) >> shift) - b0], 1u)] = v[k];
+    for (uint32_t k0 = 0; k0 < kPer; k0 += kBatch) {
+      uint32_t pos[kBatch];
+#pragma unroll
+      for (uint32_t k = 0; k < kBatch; ++k)
+        pos[k] = v[k0 + k] != ~0ull ? atomicAdd(&h[((uint32_t)(v[k0 + k] >> 32) >> shift) - b0], 1u) : 0u;
+#pragma unroll
+      for (uint32_t k = 0; k < kBatch; ++k)
+        if (v[k0 + k] != ~0ull) out[pos[k]] = v[k0 + k];
+    }
     __syncthreads();
   }
 }
 
-__global__ void k_super_cursors(const uint32_t* __restrict__ bbase, uint32_t nb, uint32_t ns, uint32_t* cur) {
+// cursor of bin x at (bucket shift + slog) = start of its first bucket
+__global__ void k_super_cursors(const uint32_t* __restrict__ bbase, uint32_t nb, uint32_t ns, uint32_t* cur,
+                                uint32_t slog) {
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x)
-    cur[s] = bbase[min(nb, s << kSuperLog)];
+    cur[s] = bbase[min(nb, s << slog)];
 }
 
 __global__ void __launch_bounds__(kPartThreads) k_bucket_rows(const unsigned long long* __restrict__ tmp,
@@ -569,8 +609,20 @@ __global__ void __launch_bounds__(kPartThreads) k_bucket_rows(const unsigned lon
     const uint32_t lo = bbase[b], hi = bbase[b + 1];
     for (uint32_t j = threadIdx.x; j < rows_per; j += blockDim.x) cnt[j] = 0;
     __syncthreads();
-    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
-      atomicAdd(&cnt[(uint32_t)(tmp[i] >> 32) - r0], 1u);
+    // 4 independent loads per thread per iteration (one load in flight per
+    // thread left the bucket latency-bound)
+    constexpr uint32_t kU = 4;
+    for (uint32_t i0 = lo + threadIdx.x; i0 < hi; i0 += kU * blockDim.x) {
+      unsigned long long t[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        t[u] = i < hi ? __ldg(tmp + i) : ~0ull;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u)
+        if (t[u] != ~0ull) atomicAdd(&cnt[(uint32_t)(t[u] >> 32) - r0], 1u);
+    }
     __syncthreads();
     // exclusive scan of cnt: each thread owns per_thread consecutive rows
     uint32_t run = 0;
@@ -594,10 +646,20 @@ __global__ void __launch_bounds__(kPartThreads) k_bucket_rows(const unsigned lon
       pre += c;
     }
     __syncthreads();
-    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const unsigned long long t = tmp[i];
-      const uint32_t pos = atomicAdd(&cnt[(uint32_t)(t >> 32) - r0], 1u);
-      raw[pos] = (uint32_t)t;
+    for (uint32_t i0 = lo + threadIdx.x; i0 < hi; i0 += kU * blockDim.x) {
+      unsigned long long t[kU];
+      uint32_t pos[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        t[u] = i < hi ? __ldg(tmp + i) : ~0ull;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u)
+        pos[u] = t[u] != ~0ull ? atomicAdd(&cnt[(uint32_t)(t[u] >> 32) - r0], 1u) : 0u;
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u)
+        if (t[u] != ~0ull) raw[pos[u]] = (uint32_t)t[u];
     }
     if (b == nb - 1 && threadIdx.x == 0) roff[n] = hi;
     __syncthreads();
@@ -1009,31 +1071,68 @@ static void count_sort_rows(const uint2* e2, uint64_t m_log, uint32_t n, int key
       return true;
     }();
     (void)attr;
-    uint32_t* bcnt = ar.get<uint32_t>(ar.bcnt, ((size_t)nb + 1) * 4, s);
+    uint32_t* bcnt = ar.get<uint32_t>(ar.bcnt, ((size_t)nb + 4) * 4, s);
+    unsigned long long* changes = reinterpret_cast<unsigned long long*>(bcnt + ((nb + 2) & ~1u));
     uint32_t* bbase = ar.get<uint32_t>(ar.bbase, ((size_t)nb + 2) * 4, s);
     uint32_t* bcur = ar.get<uint32_t>(ar.bcur, ((size_t)nb + 1) * 4, s);
     unsigned long long* tmp = ar.get<unsigned long long>(ar.tmp, m_log * 8, s);
-    CYC_CUDA(cudaMemsetAsync(bcnt, 0, ((size_t)nb + 1) * 4, s));
+    CYC_CUDA(cudaMemsetAsync(bcnt, 0, ((size_t)nb + 4) * 4, s));
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((uint64_t)sm_count() * 2, (m_log + 4095) / 4096);
     const uint64_t per_block = (m_log + blocks - 1) / blocks;
     k_bucket_hist<<<blocks, kPartThreads, nb * 4, s>>>(e2, m_log, n, key_dst, sh, nb, per_block,
-                                                       bcnt, d_err);
+                                                       bcnt, d_err, changes);
     CYC_LAUNCHED();
     exclusive_scan(bcnt, bbase, nb, nullptr, s, scratch);
-    // pass 1: log -> super-bucket order (tmp2); pass 2: -> bucket order (tmp)
-    const uint32_t ns = (nb + (1u << kSuperLog) - 1) >> kSuperLog;
-    unsigned long long* tmp2 = ar.get<unsigned long long>(ar.tmp2, m_log * 8, s);
-    k_super_cursors<<<grid_for(ns, 256, 4), 256, 0, s>>>(bbase, nb, ns, bcur);
-    CYC_LAUNCHED();
-    const uint32_t pblocks = (uint32_t)std::min<uint64_t>((uint64_t)sm_count() * 2, (m_log + kSubChunk - 1) / kSubChunk);
-    k_part<true><<<pblocks, kPartThreads, ns * 4, s>>>(e2, m_log, n, key_dst, sh + kSuperLog, ns, bcur, tmp2);
-    CYC_LAUNCHED();
-    CYC_CUDA(cudaMemcpyAsync(bcur, bbase, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
     uint32_t m_ok = 0;  // valid logged edges (invalid ones were counted nowhere)
+    unsigned long long runs = 0;
     CYC_CUDA(cudaMemcpyAsync(&m_ok, bbase + nb, 4, cudaMemcpyDeviceToHost, s));
+    CYC_CUDA(cudaMemcpyAsync(&runs, changes, 8, cudaMemcpyDeviceToHost, s));
     CYC_CUDA(cudaStreamSynchronize(s));
-    k_part<false><<<pblocks, kPartThreads, nb * 4, s>>>(tmp2, m_ok, n, key_dst, sh, nb, bcur, tmp);
-    CYC_LAUNCHED();
+    // partition passes: after pass j the elements are sorted by
+    // row >> (sh + rem_j), rem_j = bucket-id bits still unsorted; the last
+    // pass lands in tmp
+    // A log whose order is already bucket-local (config 4's BFS-ordered
+    // product log: few bucket runs per sub-chunk) partitions in one pass at
+    // full fan-out (41 vs 61 ms on config 4); a scattered one (RMAT) takes
+    // kDigit-bit passes; logs of <= 256 MB at most two passes (config 2:
+    // 1.5 ms vs 1.7 for one or three).
+    uint32_t bits = 0;
+    while ((1u << bits) < nb) ++bits;
+    const bool local = (double)runs * kSubChunk <= 64.0 * (double)m_log;
+    const bool small = m_log * 8 <= (256ull << 20);
+    const uint32_t D = local ? 32u : small ? std::max(6u, (bits + 1) / 2) : part_digit();
+    const uint32_t passes = bits ? (bits + D - 1) / D : 1;
+    if (getenv("CYC_PART_DEBUG"))
+      fprintf(stderr, "partition: m %llu nb %u runs %llu (%.1f per sub-chunk) passes %u\n",
+              (unsigned long long)m_log, nb, runs, (double)runs * kSubChunk / (double)(m_log ? m_log : 1), passes);
+    unsigned long long* tmp2 = ar.get<unsigned long long>(ar.tmp2, passes > 1 ? m_log * 8 : 8, s);
+    const uint32_t pblocks = (uint32_t)std::min<uint64_t>((uint64_t)sm_count() * 2, (m_log + kSubChunk - 1) / kSubChunk);
+    const void* src = e2;
+    uint64_t m_in = m_log;
+    uint32_t rem = bits;
+    for (uint32_t j = 0; j < passes; ++j) {
+      const uint32_t take = j == 0 ? bits - D * (passes - 1) : D;
+      const uint32_t rem_in = rem;
+      rem -= std::min(rem, take);
+      const uint32_t nbins = (nb + (1u << rem) - 1) >> rem;
+      unsigned long long* dst = ((passes - 1 - j) & 1) ? tmp2 : tmp;
+      if (rem) {
+        k_super_cursors<<<grid_for(nbins, 256, 4), 256, 0, s>>>(bbase, nb, nbins, bcur, rem);
+        CYC_LAUNCHED();
+      } else {
+        CYC_CUDA(cudaMemcpyAsync(bcur, bbase, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
+      }
+      if (j == 0) {
+        k_part<true><<<pblocks, kPartThreads, nbins * 4, s>>>(src, m_in, n, key_dst, sh + rem, nbins, bcur, dst, 0);
+        CYC_LAUNCHED();
+        m_in = m_ok;
+      } else {
+        k_part<false><<<pblocks, kPartThreads, nbins * 4, s>>>(src, m_in, n, key_dst, sh + rem, nbins, bcur, dst,
+                                                               rem_in - rem);
+        CYC_LAUNCHED();
+      }
+      src = dst;
+    }
     k_bucket_rows<<<std::min<uint32_t>(nb, sm_count() * 2), kPartThreads, (1u << sh) * 4, s>>>(
         tmp, bbase, n, sh, nb, roff, raw);
     CYC_LAUNCHED();
