@@ -374,16 +374,85 @@ __global__ void k_kept_list(uint32_t n, const uint32_t* kb, const uint32_t* wp, 
 
 // One warp per kept row (rows of R-MAT hubs are long): count, then an
 // order-preserving ballot compaction of the kept columns.
+// Filtering is row-parallel over the kept rows. A warp takes 32 consecutive
+// kept rows; rows of <= kFilterLane edges are scanned by their own lane
+// (one kept[] -> off[] dependency chain per 32 rows instead of per row),
+// rows up to kBigRow by the whole warp, and longer rows (R-MAT hubs: one
+// warp on a multi-million-edge row set the whole kernel's time on config 3)
+// are cut into kChunkLen-edge chunks, one warp each: the chunk descriptors of
+// a row are reserved contiguously and in order, so the output offset of a
+// chunk is the row's offset plus an exclusive scan of the chunk counts.
+constexpr uint32_t kFilterLane = 48;
+constexpr uint32_t kBigRow = 8192;
+constexpr uint32_t kChunkLen = 4096;
+
+__device__ __forceinline__ bool filter_row_small(uint32_t b, uint32_t e) { return e - b <= kFilterLane; }
+__device__ __forceinline__ bool filter_row_big(uint32_t b, uint32_t e) { return e - b > kBigRow; }
+
 __global__ void k_filter_count(uint32_t k, const uint32_t* kept, const uint32_t* __restrict__ off,
-                               const uint32_t* __restrict__ col, const uint32_t* kb, uint32_t* cnt) {
+                               const uint32_t* __restrict__ col, const uint32_t* kb, uint32_t* cnt,
+                               uint4* desc, uint32_t* nchunks) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t a = gw; a < k; a += nw) {
-    const uint32_t v = kept[a];
+  for (uint32_t a0 = gw * 32u; a0 < k; a0 += nw * 32u) {
+    const uint32_t a = a0 + lane;
+    uint32_t b = 0, e = 0;
+    if (a < k) {
+      const uint32_t v = kept[a];
+      b = off[v];
+      e = off[v + 1];
+    }
     uint32_t c = 0;
-    for (uint32_t i = off[v] + lane; i < off[v + 1]; i += 32u) c += kbit(kb, col[i]);
+    if (filter_row_small(b, e)) {
+#pragma unroll 4
+      for (uint32_t i = b; i < e; ++i) c += kbit(kb, __ldg(col + i));
+    } else if (filter_row_big(b, e)) {  // counted by k_filter_chunk_count
+      const uint32_t nc = (e - b + kChunkLen - 1) / kChunkLen;
+      const uint32_t j0 = atomicAdd(nchunks, nc);
+      for (uint32_t t = 0; t < nc; ++t)
+        desc[j0 + t] = make_uint4(a, b + t * kChunkLen, min(e, b + (t + 1) * kChunkLen), j0);
+    }
+    const bool warp_row = !filter_row_small(b, e) && !filter_row_big(b, e);
+    for (uint32_t hb = __ballot_sync(kFull, warp_row); hb; hb &= hb - 1u) {
+      const uint32_t l = __ffs(hb) - 1u;
+      const uint32_t bb = __shfl_sync(kFull, b, l), ee = __shfl_sync(kFull, e, l);
+      uint32_t cc = 0;
+      for (uint32_t i = bb + lane; i < ee; i += 32u) cc += kbit(kb, __ldg(col + i));
+      cc = __reduce_add_sync(kFull, cc);
+      if (lane == l) c = cc;
+    }
+    if (a < k) cnt[a] = c;
+  }
+}
+
+__global__ void k_filter_chunk_count(const uint4* __restrict__ desc, const uint32_t* nchunks,
+                                     const uint32_t* __restrict__ col, const uint32_t* kb, uint32_t* cch,
+                                     uint32_t* cnt) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t C = *nchunks;
+  for (uint32_t j = gw; j < C; j += nw) {
+    const uint4 d = desc[j];
+    uint32_t c = 0;
+    for (uint32_t i = d.y + lane; i < d.z; i += 32u) c += kbit(kb, __ldg(col + i));
     c = __reduce_add_sync(kFull, c);
-    if (lane == 0) cnt[a] = c;
+    if (lane == 0) {
+      cch[j] = c;
+      atomicAdd(cnt + d.x, c);
+    }
+  }
+}
+
+__device__ __forceinline__ void filter_fill_warp(uint32_t b, uint32_t e, uint32_t o, const uint32_t* col,
+                                                 const uint32_t* kb, const uint32_t* wp, uint32_t* ncol) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t i0 = b; i0 < e; i0 += 32u) {
+    const uint32_t i = i0 + lane;
+    const uint32_t w = i < e ? __ldg(col + i) : 0u;
+    const bool in = i < e && kbit(kb, w);
+    const uint32_t bal = __ballot_sync(kFull, in);
+    if (in) ncol[o + __popc(bal & lanemask_lt())] = knew(kb, wp, w);
+    o += __popc(bal);
   }
 }
 
@@ -392,18 +461,38 @@ __global__ void k_filter_fill(uint32_t k, const uint32_t* kept, const uint32_t* 
                               const uint32_t* noff, uint32_t* ncol) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t a = gw; a < k; a += nw) {
-    const uint32_t v = kept[a];
-    uint32_t o = noff[a];
-    const uint32_t b = off[v], e = off[v + 1];
-    for (uint32_t i0 = b; i0 < e; i0 += 32u) {
-      const uint32_t i = i0 + lane;
-      const uint32_t w = i < e ? col[i] : 0u;
-      const bool in = i < e && kbit(kb, w);
-      const uint32_t bal = __ballot_sync(kFull, in);
-      if (in) ncol[o + __popc(bal & lanemask_lt())] = knew(kb, wp, w);
-      o += __popc(bal);
+  for (uint32_t a0 = gw * 32u; a0 < k; a0 += nw * 32u) {
+    const uint32_t a = a0 + lane;
+    uint32_t b = 0, e = 0, o = 0;
+    if (a < k) {
+      const uint32_t v = kept[a];
+      b = off[v];
+      e = off[v + 1];
+      o = noff[a];
     }
+    if (filter_row_small(b, e)) {
+#pragma unroll 4
+      for (uint32_t i = b; i < e; ++i) {
+        const uint32_t w = __ldg(col + i);
+        if (kbit(kb, w)) ncol[o++] = knew(kb, wp, w);
+      }
+    }
+    const bool warp_row = !filter_row_small(b, e) && !filter_row_big(b, e);
+    for (uint32_t hb = __ballot_sync(kFull, warp_row); hb; hb &= hb - 1u) {
+      const uint32_t l = __ffs(hb) - 1u;
+      filter_fill_warp(__shfl_sync(kFull, b, l), __shfl_sync(kFull, e, l), __shfl_sync(kFull, o, l), col, kb,
+                       wp, ncol);
+    }
+  }
+}
+
+__global__ void k_filter_chunk_fill(const uint4* __restrict__ desc, uint32_t C, const uint32_t* __restrict__ col,
+                                    const uint32_t* kb, const uint32_t* wp, const uint32_t* noff,
+                                    const uint32_t* __restrict__ pre, uint32_t* ncol) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t j = gw; j < C; j += nw) {
+    const uint4 d = desc[j];
+    filter_fill_warp(d.y, d.z, noff[d.x] + pre[j] - pre[d.w], col, kb, wp, ncol);
   }
 }
 
@@ -478,19 +567,35 @@ void filter_csr(const DevCsr& in, const uint32_t* kb, const uint32_t* wp, const 
   out.n = k;
   out.off.alloc(((size_t)k + 1) * 4, s);
   DevBuf cnt(((size_t)k + 1) * 4, s), scratch;
+  const size_t max_chunks = (size_t)in.m / kChunkLen + in.m / kBigRow + 1;
+  DevBuf desc(max_chunks * sizeof(uint4), s), cch((max_chunks + 1) * 4, s), pre((max_chunks + 1) * 4, s);
+  DevBuf nch(4, s);
+  CYC_CUDA(cudaMemsetAsync(nch.p, 0, 4, s));
   if (k) {
-    k_filter_count<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), kb, cnt.as<uint32_t>());
+    k_filter_count<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), kb, cnt.as<uint32_t>(),
+                                                 desc.as<uint4>(), nch.as<uint32_t>());
+    CYC_LAUNCHED();
+    k_filter_chunk_count<<<sm_count() * 8, kT, 0, s>>>(desc.as<uint4>(), nch.as<uint32_t>(), in.c(), kb,
+                                                       cch.as<uint32_t>(), cnt.as<uint32_t>());
     CYC_LAUNCHED();
   }
   exclusive_scan(cnt.as<uint32_t>(), out.off.as<uint32_t>(), k, nullptr, s, scratch);
-  uint32_t m = 0;
-  CYC_CUDA(cudaMemcpyAsync(&m, out.off.as<uint32_t>() + k, 4, cudaMemcpyDeviceToHost, s));
+  uint32_t h[2] = {0, 0};
+  CYC_CUDA(cudaMemcpyAsync(&h[0], out.off.as<uint32_t>() + k, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaMemcpyAsync(&h[1], nch.p, 4, cudaMemcpyDeviceToHost, s));
   CYC_CUDA(cudaStreamSynchronize(s));
+  const uint32_t m = h[0], C = h[1];
   out.m = m;
   out.col.alloc(((size_t)m + 1) * 4, s);
+  if (C) exclusive_scan(cch.as<uint32_t>(), pre.as<uint32_t>(), C, nullptr, s, scratch);
   if (k) {
     k_filter_fill<<<sm_count() * 8, kT, 0, s>>>(k, kept, in.o(), in.c(), kb, wp, out.off.as<uint32_t>(),
                                                 out.col.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
+  if (C) {
+    k_filter_chunk_fill<<<grid_for((uint64_t)C * 32, kT, 8), kT, 0, s>>>(
+        desc.as<uint4>(), C, in.c(), kb, wp, out.off.as<uint32_t>(), pre.as<uint32_t>(), out.col.as<uint32_t>());
     CYC_LAUNCHED();
   }
 }
