@@ -61,7 +61,8 @@ struct OpSameColor {  // backward reach from roots through equal colours
   uint32_t* inscc;
   __device__ uint32_t token(uint32_t w) const { return __ldcg(color + w); }
   __device__ bool relax(uint32_t, uint32_t tok, uint32_t v, uint32_t) const {
-    return __ldcg(color + v) == tok && test_and_set_bit(inscc, v);
+    // membership first: the bitmap is L2-resident, colours are not
+    return !bit(inscc, v) && __ldcg(color + v) == tok && test_and_set_bit(inscc, v);
   }
 };
 
@@ -286,7 +287,7 @@ __global__ void k_same_pull(uint32_t n, const uint32_t* __restrict__ off, const 
     if (cv == kNoColor || bit(inscc, v) || off[v + 1] - off[v] > heavy) continue;
     for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
       const uint32_t w = col[i];
-      if (color[w] == cv && bit(inscc, w)) {
+      if (bit(inscc, w) && color[w] == cv) {
         atomicOr(inscc + (v >> 5), 1u << (v & 31u));
         ep[v] = p;
         ++c;
@@ -310,7 +311,7 @@ __global__ void k_same_pull_chunks(const uint4* __restrict__ chunks, uint32_t nc
     bool hit = false;
     for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) {
       const uint32_t w = col[i];
-      hit |= color[w] == cv && bit(inscc, w);
+      hit |= bit(inscc, w) && color[w] == cv;
     }
     if (__any_sync(kFull, hit) && lane == 0 && test_and_set_bit(inscc, ch.x)) {
       ep[ch.x] = p;
