@@ -34,6 +34,91 @@ thread_local int g_parse[3] = {0, 0, 0};  // code, line, col of the last CYC_E_P
                         what + " [" + file + ":" + std::to_string(line) + "]");
 }
 
+namespace {
+struct BigBlock {
+  void* p;
+  size_t cap;
+  int device;
+  cudaEvent_t ready;  // recorded on the releasing stream
+};
+std::mutex g_big_mu;
+std::vector<BigBlock> g_big_free;
+
+void big_drop_all(int device, cudaStream_t st) {  // caller holds g_big_mu
+  for (size_t i = 0; i < g_big_free.size();) {
+    BigBlock& b = g_big_free[i];
+    if (b.device != device) {
+      ++i;
+      continue;
+    }
+    cudaStreamWaitEvent(st, b.ready, 0);
+    cudaEventDestroy(b.ready);
+    cudaFreeAsync(b.p, st);
+    g_big_free[i] = g_big_free.back();
+    g_big_free.pop_back();
+  }
+}
+}  // namespace
+
+namespace {
+void big_trim(int device, cudaStream_t st) {  // a context goes away: hand the cached blocks back
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  big_drop_all(device, st);
+}
+}  // namespace
+
+void* cyc::big_alloc(size_t n, cudaStream_t st, size_t* cap) {
+  int dev = 0;
+  CYC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  size_t best = SIZE_MAX;
+  for (size_t i = 0; i < g_big_free.size(); ++i) {
+    const BigBlock& b = g_big_free[i];
+    if (b.device == dev && b.cap >= n && b.cap <= n + n / 4 + (64ull << 20) &&
+        (best == SIZE_MAX || b.cap < g_big_free[best].cap))
+      best = i;
+  }
+  if (best != SIZE_MAX) {
+    BigBlock b = g_big_free[best];
+    g_big_free[best] = g_big_free.back();
+    g_big_free.pop_back();
+    CYC_CUDA(cudaStreamWaitEvent(st, b.ready, 0));
+    cudaEventDestroy(b.ready);
+    *cap = b.cap;
+    return b.p;
+  }
+  const size_t c = (n + (2ull << 20) - 1) & ~((2ull << 20) - 1);
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, c, st);
+  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry
+    cudaGetLastError();
+    big_drop_all(dev, st);
+    e = cudaMallocAsync(&p, c, st);
+  }
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw Error(CYC_E_RESOURCE, "device memory exhausted allocating " + std::to_string(n) + " bytes");
+  }
+  CYC_CUDA(e);
+  *cap = c;
+  return p;
+}
+
+void cyc::big_free(void* p, size_t cap, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(ev, st) != cudaSuccess) {
+    cudaGetLastError();
+    if (ev) cudaEventDestroy(ev);
+    cudaFreeAsync(p, st);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  g_big_free.push_back(BigBlock{p, cap, dev, ev});
+}
+
 // A context lives until cyc_ctx_destroy was called AND its last graph is gone
 // (graphs keep a reference), so teardown order between them does not matter.
 struct cyc_ctx {
@@ -47,11 +132,13 @@ struct cyc_ctx {
 };
 
 namespace {
+void big_trim(int device, cudaStream_t st);
 void ctx_release(cyc_ctx* ctx) {
   if (ctx->refs.fetch_sub(1) != 1) return;
   cudaSetDevice(ctx->device);
   ctx->flush.release();
   ctx->arena = cyc::BuildArena();
+  big_trim(ctx->device, ctx->s);
   cudaStreamSynchronize(ctx->s);
   cudaEventDestroy(ctx->e0);
   cudaEventDestroy(ctx->e1);

@@ -41,10 +41,21 @@ extern std::atomic<uint64_t> g_launches;
 
 inline uint32_t div_up(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
 
+// Blocks of >= kBigBlock (16 MB) go through a process-wide grow-only cache
+// (abi.cu) instead of straight back to the pool: the pool splits freed
+// multi-GB blocks for small requests, and the fragmentation made later GB-sized
+// requests map new memory — 100-700 ms stalls per call on config 3
+// (restriction outputs). Cached blocks are reused whole (stream-ordered via
+// an event recorded at release) and given back to the pool on exhaustion.
+constexpr size_t kBigBlock = 16ull << 20;
+void* big_alloc(size_t n, cudaStream_t st, size_t* cap);
+void big_free(void* p, size_t cap, cudaStream_t st);
+
 // Stream-ordered device allocation from the context's pool.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  size_t cap = 0;  // > 0: block from the big-block cache
   cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(size_t n, cudaStream_t st) { alloc(n, st); }
@@ -54,8 +65,8 @@ struct DevBuf {
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; bytes = o.bytes; s = o.s;
-      o.p = nullptr; o.bytes = 0;
+      p = o.p; bytes = o.bytes; cap = o.cap; s = o.s;
+      o.p = nullptr; o.bytes = 0; o.cap = 0;
     }
     return *this;
   }
@@ -65,6 +76,11 @@ struct DevBuf {
     s = st;
     bytes = n;
     if (n == 0) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (n >= kBigBlock && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+      p = big_alloc(n, st, &cap);
+      return;
+    }
     cudaError_t e = cudaMallocAsync(&p, n, st);
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
@@ -74,9 +90,11 @@ struct DevBuf {
     CYC_CUDA(e);
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && cap) big_free(p, cap, s);
+    else if (p) cudaFreeAsync(p, s);
     p = nullptr;
     bytes = 0;
+    cap = 0;
   }
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
