@@ -713,3 +713,34 @@ def test_fuzz_all_entry_points(eng, R, REF):
         v, st = eng.run_owcty(s)
         assert (v.cycle_found(), v.witness, st.outer_iterations, st.final_size) == R.run_owcty(g, acc)
         assert eng.scc_verdict(s).verdict.cycle_found() == REF.snapshot(n, e, acc, tr).scc_verdict()
+
+
+def test_restrict_hub_rows(eng, R):
+    """Restriction of rows far longer than the compaction's chunk (8192):
+    a hub inside the big SCC whose rows also reference dropped vertices (sink
+    tails without a path back), in both CSRs and both orientations."""
+    rng = np.random.default_rng(77)
+    core, tail = 30000, 6000
+    n = core + tail
+    ring = np.stack([np.arange(core), (np.arange(core) + 1) % core], 1)
+    hub_out = np.stack([np.zeros(n - 1, dtype=np.int64), np.arange(1, n)], 1)  # also into the tails
+    hub_in = np.stack([np.arange(1, core), np.zeros(core - 1, dtype=np.int64)], 1)
+    rnd = rng.integers(0, core, size=(40000, 2))
+    tails = np.stack([rng.integers(core, n, size=5000), rng.integers(core, n, size=5000)], 1)
+    e = np.concatenate([ring, hub_out, hub_in, rnd, tails]).astype(np.uint32)
+    rng.shuffle(e)
+    acc = np.zeros(n, dtype=bool)
+    acc[rng.integers(0, n, size=200)] = True
+    acc[5] = True
+    for tr in (True, False):
+        s = snap_of(eng, n, e, acc, tr)
+        g = R.build_snapshot(n, e, tr)
+        rg, racc, kept = R.restrict(g, acc)
+        assert len(kept) == core
+        r = eng.restrict_to_accepting_sccs(s)
+        assert np.array_equal(r.kept, kept)
+        assert np.array_equal(r.snapshot.row_offsets, rg.off)
+        assert np.array_equal(r.snapshot.col_indices, rg.col)
+        off, col = r.snapshot.gather_index()
+        gt = R.transpose(rg)
+        assert np.array_equal(off, gt.off) and np.array_equal(col, gt.col)
