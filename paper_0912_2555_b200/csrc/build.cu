@@ -381,25 +381,47 @@ __global__ void k_compact_rows(uint32_t n, const uint32_t* __restrict__ roff, co
 __global__ void k_compact_list(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cnt,
                                const uint32_t* __restrict__ roff, const uint32_t* __restrict__ off,
                                const uint32_t* __restrict__ raw, uint32_t* __restrict__ col) {
+  // one warp per long row (a CTA per row spent its time on the per-row
+  // offset loads of short-ish rows)
   const uint32_t nrows = *cnt;
-  for (uint32_t r = blockIdx.x; r < nrows; r += gridDim.x) {
-    uint32_t v = rows[r];
-    uint32_t b = roff[v], o = off[v], u = off[v + 1] - o;
-    for (uint32_t i = threadIdx.x; i < u; i += blockDim.x) col[o + i] = raw[b + i];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = gw; r < nrows; r += nw) {
+    const uint32_t v = rows[r];
+    const uint32_t b = roff[v], o = off[v], u = off[v + 1] - o;
+#pragma unroll 4
+    for (uint32_t i = lane; i < u; i += 32u) col[o + i] = __ldg(raw + b + i);
   }
 }
 
 __global__ void k_heavy_chunks(uint32_t n, const uint32_t* __restrict__ off, uint32_t heavy,
                                uint32_t chunk, uint4* __restrict__ out, uint32_t* __restrict__ cnt) {
+  // warp-aggregated reservation, descriptors written by the whole warp (a hub
+  // row has thousands of chunks)
+  const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-    uint32_t b = off[v], e = off[v + 1];
-    if (e - b <= heavy) continue;
-    uint32_t nc = (e - b + chunk - 1) / chunk;
-    uint32_t base = atomicAdd(cnt, nc);
-    for (uint32_t c = 0; c < nc; ++c) {
-      uint32_t cb = b + c * chunk;
-      out[base + c] = make_uint4(v, cb, min(e, cb + chunk), 0u);
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane;
+    uint32_t b = 0, e = 0;
+    if (v < n) {
+      b = off[v];
+      e = off[v + 1];
+    }
+    const uint32_t nc = v < n && e - b > heavy ? (e - b + chunk - 1) / chunk : 0u;
+    const uint32_t incl = warp_incl_scan(nc);
+    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+    if (!tot) continue;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(cnt, tot);
+    base = __shfl_sync(kFull, base, 0) + incl - nc;
+    for (uint32_t hb = __ballot_sync(kFull, nc != 0); hb; hb &= hb - 1u) {
+      const uint32_t l = __ffs(hb) - 1u;
+      const uint32_t lb = __shfl_sync(kFull, b, l), le = __shfl_sync(kFull, e, l);
+      const uint32_t ln = __shfl_sync(kFull, nc, l), lbase = __shfl_sync(kFull, base, l);
+      for (uint32_t c = lane; c < ln; c += 32u) {
+        const uint32_t cb = lb + c * chunk;
+        out[lbase + c] = make_uint4(v0 + l, cb, min(le, cb + chunk), 0u);
+      }
     }
   }
 }
@@ -420,25 +442,46 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* p, uint32_t 
 __global__ void k_heavy_blocks(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
                                uint32_t heavy, uint32_t chunk, uint32_t ncb, uint32_t width,
                                uint32_t* __restrict__ bcount, uint32_t* __restrict__ bcur, uint4* __restrict__ out) {
+  // warp-aggregated per-block reservations (one atomic per warp and column
+  // block instead of one per heavy row), descriptors written by the warp
+  const uint32_t lane = threadIdx.x & 31u;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-    const uint32_t b = off[v], e = off[v + 1];
-    if (e - b <= heavy) continue;
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane;
+    uint32_t b = 0, e = 0;
+    if (v < n) {
+      b = off[v];
+      e = off[v + 1];
+    }
+    const bool hv = v < n && e - b > heavy;
+    if (!__any_sync(kFull, hv)) continue;
     uint32_t lo = 0;
     for (uint32_t j = 0; j < ncb; ++j) {
-      const uint64_t bound = (uint64_t)(j + 1) * width;
-      const uint32_t hi = j + 1 == ncb || bound > 0xFFFFFFFFull
-                              ? e - b
-                              : lo + lower_bound_u32(col + b + lo, e - b - lo, (uint32_t)bound);
-      const uint32_t nc = (hi - lo + chunk - 1) / chunk;
-      if (nc) {
+      uint32_t hi = 0, nc = 0;
+      if (hv) {
+        const uint64_t bound = (uint64_t)(j + 1) * width;
+        hi = j + 1 == ncb || bound > 0xFFFFFFFFull
+                 ? e - b
+                 : lo + lower_bound_u32(col + b + lo, e - b - lo, (uint32_t)bound);
+        nc = (hi - lo + chunk - 1) / chunk;
+      }
+      const uint32_t incl = warp_incl_scan(nc);
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);
+      if (tot) {
         if (!out) {
-          atomicAdd(bcount + j, nc);
+          if (lane == 0) atomicAdd(bcount + j, tot);
         } else {
-          const uint32_t base = atomicAdd(bcur + j, nc);
-          for (uint32_t c = 0; c < nc; ++c) {
-            const uint32_t cb = b + lo + c * chunk;
-            out[base + c] = make_uint4(v, cb, min(b + hi, cb + chunk), 0u);
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(bcur + j, tot);
+          base = __shfl_sync(kFull, base, 0) + incl - nc;
+          for (uint32_t hb = __ballot_sync(kFull, nc != 0); hb; hb &= hb - 1u) {
+            const uint32_t l = __ffs(hb) - 1u;
+            const uint32_t lb = __shfl_sync(kFull, b + lo, l), le = __shfl_sync(kFull, b + hi, l);
+            const uint32_t ln = __shfl_sync(kFull, nc, l), lbase = __shfl_sync(kFull, base, l);
+            for (uint32_t c = lane; c < ln; c += 32u) {
+              const uint32_t cb = lb + c * chunk;
+              out[lbase + c] = make_uint4(v0 + l, cb, min(le, cb + chunk), 0u);
+            }
           }
         }
       }
