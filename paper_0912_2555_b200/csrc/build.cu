@@ -4,9 +4,11 @@
 // construction of MaxPropagation (map_engine.cpp:9-19). Both are
 // single-threaded counting sorts on the CPU; here the phases run as
 // HBM-bound kernels over the whole log:
-//   1. bucket histogram (2^14 rows per bucket, shared-memory counters)
-//   2. two-pass partition: log -> 64-bucket super-buckets -> buckets, in
-//      sub-chunks held in registers (contiguous runs per bin)
+//   1. bucket histogram (2^14 rows per bucket, shared-memory counters; also
+//      counts bucket runs in log order)
+//   2. MSD partition log -> buckets in sub-chunks held in registers
+//      (contiguous runs per bin): one pass for a bucket-local log, 4-bit
+//      digits per pass for a scattered one
 //   3. one CTA per bucket counting-sorts its rows in shared memory
 //   4. per-row sort+dedup by length: registers (<=16), one warp in registers
 //      (<=512), longer rows by an MSD split into ~256-value sub-buckets sorted
