@@ -8,6 +8,8 @@
 // prebuilt into oracle/_ref/ and shipped); exits non-zero on any mismatch.
 #include <algorithm>
 #include <cstdio>
+#include <cstdio>
+#include <cstdlib>
 #include <random>
 
 #include "cycheck/graph.hpp"
@@ -30,6 +32,8 @@ int main(int argc, char** argv) {
     for (uint32_t v = 0; v < n; ++v) log.add_vertex(rng() % 100 < (t % 2 ? 5u : 30u));
     for (uint64_t i = 0; i < m; ++i) log.append_edge(rng() % n, rng() % n);
     for (Orientation o : {Orientation::transposed, Orientation::forward}) {
+      if (std::getenv("DROPIN_TRACE")) std::fprintf(stderr, "trial %d orient %d n %u m %llu\n", t, (int)o, n,
+                                                    (unsigned long long)m);
       CsrSnapshot ref = build_snapshot(log, o);
       b200::Snapshot dev = b200::build_snapshot(gpu, log, o);
       CsrSnapshot back;
@@ -81,6 +85,7 @@ int main(int argc, char** argv) {
           }
         }
       }
+      if (std::getenv("DROPIN_TRACE")) std::fprintf(stderr, "  run_map done\n");
       // OWCTY and the SCC verdict through the drop-in (owcty.hpp, oracle.hpp)
       auto [ov, os] = run_owcty(ref, ref.accepting);
       auto [gov, gos] = b200::run_owcty<Verdict, OwctyStats>(dev, ref.accepting);
@@ -93,6 +98,7 @@ int main(int argc, char** argv) {
         std::printf("trial %d: scc_verdict differs\n", t);
         ++bad;
       }
+      if (std::getenv("DROPIN_TRACE")) std::fprintf(stderr, "  owcty+scc done\n");
       SccRestriction rr = restrict_to_accepting_sccs(ref);
       auto [gr, kept] = b200::restrict_to_accepting_sccs(dev);
       CsrSnapshot grb;

@@ -67,6 +67,22 @@ void big_trim(int device, cudaStream_t st) {  // a context goes away: hand the c
 }
 }  // namespace
 
+namespace {
+std::mutex g_coop_mu;
+cudaEvent_t g_coop_last[64] = {};  // per device: completion of the latest cooperative grid
+}  // namespace
+
+void cyc::coop_launch(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
+  int dev = 0;
+  CYC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_coop_mu);
+  cudaEvent_t& last = g_coop_last[dev & 63];
+  if (last) CYC_CUDA(cudaStreamWaitEvent(st, last, 0));
+  else CYC_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
+  CYC_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, st));
+  CYC_CUDA(cudaEventRecord(last, st));
+}
+
 void* cyc::big_alloc(size_t n, cudaStream_t st, size_t* cap) {
   int dev = 0;
   CYC_CUDA(cudaGetDevice(&dev));

@@ -48,6 +48,13 @@ inline uint32_t div_up(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) /
 // (restriction outputs). Cached blocks are reused whole (stream-ordered via
 // an event recorded at release) and given back to the pool on exhaustion.
 constexpr size_t kBigBlock = 16ull << 20;
+
+// Every persistent (cooperative) kernel of the process goes through here:
+// it is ordered after the previous one on the device, whatever its stream.
+// Two grids spinning at grid barriers on different streams (contexts on
+// separate threads) could each be partly resident and wait for each other
+// forever; regular kernels beside one grid only delay it.
+void coop_launch(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st);
 void* big_alloc(size_t n, cudaStream_t st, size_t* cap);
 void big_free(void* p, size_t cap, cudaStream_t st);
 

@@ -324,8 +324,7 @@ void run_frontier(const uint32_t* off, const uint32_t* col, const FrontierBufs& 
   const uint32_t* a0 = off;
   const uint32_t* a1 = col;
   void* args[] = {(void*)&a0, (void*)&a1, (void*)&f, (void*)&o};
-  CYC_CUDA(cudaLaunchCooperativeKernel((const void*)k_frontier<Op>, dim3(grid), dim3(kFrontierThreads), args,
-                                       0, s));
+  coop_launch((const void*)k_frontier<Op>, dim3(grid), dim3(kFrontierThreads), args, 0, s);
   CYC_LAUNCHED();
 }
 

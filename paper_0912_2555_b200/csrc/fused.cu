@@ -333,7 +333,7 @@ void FusedShard::run(const uint64_t* acc_words, int early_exit, cudaStream_t s, 
     return sm_count();
   }();
   void* args[] = {&a};
-  CYC_CUDA(cudaLaunchCooperativeKernel((const void*)k_fused_run, dim3(grid), dim3(kFT), args, 0, s));
+  coop_launch((const void*)k_fused_run, dim3(grid), dim3(kFT), args, 0, s);
   CYC_LAUNCHED();
   CYC_CUDA(cudaMemcpyAsync(hres, dres.p, 7 * 8, cudaMemcpyDeviceToHost, s));
   CYC_CUDA(cudaStreamSynchronize(s));

@@ -1362,7 +1362,7 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
   dim3 grid((unsigned)(sm_count() * blocks_per_sm)), block(kRunThreads);
   void* args[] = {&a};
   CYC_CUDA(cudaEventRecord(e0, s));
-  CYC_CUDA(cudaLaunchCooperativeKernel((const void*)k_map_run, grid, block, args, 0, s));
+  coop_launch((const void*)k_map_run, grid, block, args, 0, s);
   CYC_LAUNCHED();
   CYC_CUDA(cudaEventRecord(e1, s));
   RunCtl host;

@@ -39,10 +39,13 @@ __device__ __forceinline__ bool accb(const uint64_t* acc, uint32_t v) {
 __device__ __forceinline__ bool bit(const uint32_t* b, uint32_t v) { return (b[v >> 5] >> (v & 31u)) & 1u; }
 
 // ---- frontier ops
-struct OpReach {  // mark = vertices reached so far (seeds included)
+struct OpReach {  // mark = vertices reached so far (seeds included); act: optional vertex filter
   uint32_t* mark;
+  const uint8_t* act = nullptr;
   __device__ uint32_t token(uint32_t) const { return 0u; }
-  __device__ bool relax(uint32_t, uint32_t, uint32_t w, uint32_t) const { return test_and_set_bit(mark, w); }
+  __device__ bool relax(uint32_t, uint32_t, uint32_t w, uint32_t) const {
+    return (!act || act[w]) && test_and_set_bit(mark, w);
+  }
 };
 
 struct OpColor {  // colour[w] = max(colour[w], colour[u]) along the relation
@@ -128,6 +131,40 @@ __global__ void k_trim(uint32_t n, const uint32_t* __restrict__ soff, const uint
   if (ch) *flag = 1;
 }
 
+// FW-BW from one pivot before colouring: the active vertex of largest total
+// degree (an R-MAT hub, inside the giant SCC) — its SCC is fw ∩ bw of two
+// bitmap reach closures restricted to the active vertices, instead of
+// several max-colour passes that gather 4 B colours of every vertex.
+__global__ void k_pivot(uint32_t n, const uint32_t* __restrict__ aoff, const uint32_t* __restrict__ boff,
+                        const uint8_t* active, unsigned long long* best) {
+  unsigned long long m = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (active[v]) {
+      const unsigned long long d = (unsigned long long)(aoff[v + 1] - aoff[v]) + (boff[v + 1] - boff[v]);
+      m = max(m, (d << 32) | v);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(kFull, m, o));
+  if ((threadIdx.x & 31u) == 0 && m) atomicMax(best, m);
+}
+
+__global__ void k_and_act(uint32_t n, const uint8_t* active, const uint32_t* fw, uint8_t* out) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    out[v] = active[v] && bit(fw, v);
+}
+
+__global__ void k_pivot_scc(uint32_t n, const uint32_t* fw, const uint32_t* bw, const uint8_t* active,
+                            uint32_t pivot, uint32_t* inscc, uint32_t* color) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; v0 < n; v0 += stride) {
+    const uint32_t v = v0 + lane_id();
+    const bool in = v < n && active[v] && bit(fw, v) && bit(bw, v);
+    const uint32_t word = __ballot_sync(kFull, in);
+    if (lane_id() == 0) inscc[v0 >> 5] = word;
+    if (in) color[v] = pivot + 1u;
+  }
+}
+
 __global__ void k_color_init(uint32_t n, const uint8_t* active, uint32_t* color) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
     color[v] = active[v] ? v + 1u : kNoColor;
@@ -190,12 +227,13 @@ __device__ __forceinline__ void count_changes(uint32_t c, unsigned long long* cn
 }
 
 __global__ void k_reach_pull(uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                             uint32_t heavy, uint32_t* mark, uint8_t* ep, uint8_t p, unsigned long long* cnt) {
+                             uint32_t heavy, uint32_t* mark, uint8_t* ep, uint8_t p, unsigned long long* cnt,
+                             const uint8_t* act) {
   uint32_t c = 0;
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; w0 < n; w0 += stride) {
     const uint32_t w = w0 + lane_id();
-    if (w >= n || bit(mark, w) || off[w + 1] - off[w] > heavy) continue;
+    if (w >= n || bit(mark, w) || (act && !act[w]) || off[w + 1] - off[w] > heavy) continue;
     for (uint32_t i = off[w]; i < off[w + 1]; ++i) {
       if (bit(mark, col[i])) {
         atomicOr(mark + (w >> 5), 1u << (w & 31u));
@@ -231,13 +269,13 @@ __device__ __forceinline__ void chunk_cols(const uint4 (&ch)[kCB], const bool (&
 
 __global__ void k_reach_pull_chunks(const uint4* __restrict__ chunks, uint32_t nch,
                                     const uint32_t* __restrict__ col, uint32_t* mark, uint8_t* ep, uint8_t p,
-                                    unsigned long long* cnt) {
+                                    unsigned long long* cnt, const uint8_t* act) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   uint32_t c = 0;
   for (uint32_t k = gw; k < nch; k += nw) {
     const uint4 ch = chunks[k];
-    if (bit(mark, ch.x)) continue;
+    if (bit(mark, ch.x) || (act && !act[ch.x])) continue;
     bool hit = false;
     for (uint32_t i = ch.y + lane; i < ch.z; i += 32u) hit |= bit(mark, col[i]);
     if (__any_sync(kFull, hit) && lane == 0 && test_and_set_bit(mark, ch.x)) {
@@ -728,20 +766,21 @@ void scc_keep_mask(const DevCsr& snap_in, const DevCsr& gath_in, const uint64_t*
   unsigned long long* dc = reinterpret_cast<unsigned long long*>(f + 4);
   const uint32_t cg = sm_count() * 8;
   auto hv = [](const DevCsr& g) { return g.n_heavy_chunks ? g.heavy_deg : kNone; };
-  auto reach = [&](const DevCsr& push, const DevCsr& pull, DevBuf& mark) {
+  auto reach = [&](const DevCsr& push, const DevCsr& pull, DevBuf& mark, const uint8_t* act) {
     return hybrid_closure(n, ep.as<uint8_t>(), dc, [&](uint8_t p) {
-      k_reach_pull<<<grid, kT, 0, s>>>(n, pull.o(), pull.c(), hv(pull), mark.as<uint32_t>(), ep.as<uint8_t>(), p, dc);
+      k_reach_pull<<<grid, kT, 0, s>>>(n, pull.o(), pull.c(), hv(pull), mark.as<uint32_t>(), ep.as<uint8_t>(), p, dc,
+                                       act);
       CYC_LAUNCHED();
       if (pull.n_heavy_chunks) {
         k_reach_pull_chunks<<<cg, kT, 0, s>>>(pull.heavy.as<uint4>(), pull.n_heavy_chunks, pull.c(),
-                                              mark.as<uint32_t>(), ep.as<uint8_t>(), p, dc);
+                                              mark.as<uint32_t>(), ep.as<uint8_t>(), p, dc, act);
         CYC_LAUNCHED();
       }
-    }, push, fb, OpReach{mark.as<uint32_t>()}, s);
+    }, push, fb, OpReach{mark.as<uint32_t>(), act}, s);
   };
-  int np = reach(A, B, fw);
+  int np = reach(A, B, fw, nullptr);
   lg.mark("reach-A", np);
-  np = reach(B, A, bw);
+  np = reach(B, A, bw, nullptr);
   lg.mark("reach-B", np);
   k_and_bits<<<grid, kT, 0, s>>>(n, fw.as<uint32_t>(), bw.as<uint32_t>(), active.as<uint8_t>());
   CYC_LAUNCHED();
@@ -751,6 +790,60 @@ void scc_keep_mask(const DevCsr& snap_in, const DevCsr& gath_in, const uint64_t*
       CYC_LAUNCHED();
     });
     lg.mark("trim", np);
+    if (round == 0) {
+      unsigned long long* best = reinterpret_cast<unsigned long long*>(f + 6);
+      unsigned long long hb = 0;
+      CYC_CUDA(cudaMemsetAsync(best, 0, 8, s));
+      k_pivot<<<grid, kT, 0, s>>>(n, A.o(), B.o(), active.as<uint8_t>(), best);
+      CYC_LAUNCHED();
+      CYC_CUDA(cudaMemcpyAsync(&hb, best, 8, cudaMemcpyDeviceToHost, s));
+      CYC_CUDA(cudaStreamSynchronize(s));
+      if (hb) {  // some vertex is active
+        const uint32_t pivot = (uint32_t)hb, word = 1u << (pivot & 31u);
+        CYC_CUDA(cudaMemsetAsync(fw.p, 0, words * 4, s));
+        CYC_CUDA(cudaMemsetAsync(bw.p, 0, words * 4, s));
+        CYC_CUDA(cudaMemcpyAsync(fw.as<uint32_t>() + (pivot >> 5), &word, 4, cudaMemcpyHostToDevice, s));
+        CYC_CUDA(cudaMemcpyAsync(bw.as<uint32_t>() + (pivot >> 5), &word, 4, cudaMemcpyHostToDevice, s));
+        np = reach(A, B, fw, active.as<uint8_t>());
+        lg.mark("pivot-fw", np);
+        // the pivot's SCC lies inside its forward set: the backward closure
+        // only explores fw (config 2's pivot is a DAG connector: 63 backward
+        // passes over the whole graph otherwise)
+        uint8_t* act2 = stamp.as<uint8_t>();  // scratch until the colour closure
+        k_and_act<<<grid, kT, 0, s>>>(n, active.as<uint8_t>(), fw.as<uint32_t>(), act2);
+        CYC_LAUNCHED();
+        np = reach(B, A, bw, act2);
+        lg.mark("pivot-bw", np);
+        k_pivot_scc<<<grid, kT, 0, s>>>(n, fw.as<uint32_t>(), bw.as<uint32_t>(), active.as<uint8_t>(), pivot,
+                                        inscc.as<uint32_t>(), color.as<uint32_t>());
+        CYC_LAUNCHED();
+        k_clear_roots<<<grid, kT, 0, s>>>(n, color.as<uint32_t>(), inscc.as<uint32_t>(), rsize.as<uint32_t>(),
+                                          rflag.as<uint32_t>());
+        CYC_LAUNCHED();
+        k_scc_stats<<<grid, kT, 0, s>>>(n, acc, inscc.as<uint32_t>(), color.as<uint32_t>(), rsize.as<uint32_t>(),
+                                        rflag.as<uint32_t>());
+        CYC_LAUNCHED();
+        uint32_t any = 0;
+        CYC_CUDA(cudaMemsetAsync(f, 0, 4, s));
+        k_scc_apply<<<grid, kT, 0, s>>>(n, A.o(), A.c(), color.as<uint32_t>(), rsize.as<uint32_t>(),
+                                        rflag.as<uint32_t>(), inscc.as<uint32_t>(), active.as<uint8_t>(), keep, f);
+        CYC_LAUNCHED();
+        CYC_CUDA(cudaMemcpyAsync(&any, f, 4, cudaMemcpyDeviceToHost, s));
+        CYC_CUDA(cudaStreamSynchronize(s));
+        lg.mark("pivot-apply", 1);
+        if (lg.on) {
+          unsigned long long cnt_scc = 0;
+          std::vector<uint32_t> hw(words);
+          CYC_CUDA(cudaMemcpyAsync(hw.data(), inscc.p, words * 4, cudaMemcpyDeviceToHost, s));
+          CYC_CUDA(cudaStreamSynchronize(s));
+          for (uint32_t x : hw) cnt_scc += __builtin_popcount(x);
+          std::fprintf(stderr, "[cyc scc]   pivot %u deg %llu scc %llu (n %u, m %u)\n", pivot, hb >> 32, cnt_scc, n,
+                       snap_in.m);
+        }
+        if (!any) break;
+        continue;  // trim what the pivot's SCC leaves, then colour it
+      }
+    }
     k_color_init<<<grid, kT, 0, s>>>(n, active.as<uint8_t>(), color.as<uint32_t>());
     CYC_LAUNCHED();
     CYC_CUDA(cudaMemsetAsync(stamp.p, 0, (size_t)n * 4, s));

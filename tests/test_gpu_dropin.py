@@ -16,7 +16,12 @@ BIN = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
 def test_cpp_dropin_matches_reference():
     if not os.path.exists(BIN):
         pytest.skip("oracle/_ref/dropin_test not built (needs the reference sources)")
-    out = subprocess.run([BIN, "150"], capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, DROPIN_TRACE="1")
+    try:
+        out = subprocess.run([BIN, "150"], capture_output=True, text=True, timeout=90, env=env)
+    except subprocess.TimeoutExpired as ex:
+        err = ex.stderr.decode() if isinstance(ex.stderr, bytes) else (ex.stderr or "")
+        pytest.fail("dropin_test timed out; last progress:\n" + err[-600:])
     print(out.stdout[-2000:])
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "0 mismatches" in out.stdout
