@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <pthread.h>
 #include <string>
 #include <vector>
 
@@ -194,8 +195,29 @@ namespace {
 using cyc::DevBuf;
 using cyc::Error;
 
+// CYC_TRACE_CALLS=1: enter/exit lines per ABI call and thread (diagnostics)
+struct CallTrace {
+  const char* name;
+  bool on;
+  explicit CallTrace(const char* n) : name(n), on(std::getenv("CYC_TRACE_CALLS") != nullptr) {
+    if (on) std::fprintf(stderr, "[cyc %zx] enter %s\n", (size_t)pthread_self() & 0xFFFFFF, name);
+  }
+  ~CallTrace() {
+    if (on) std::fprintf(stderr, "[cyc %zx] exit %s\n", (size_t)pthread_self() & 0xFFFFFF, name);
+  }
+};
+
+// One library call at a time per process. Threads with their own contexts
+// (the explorer's detector and final round) each run persistent grids that
+// spin at grid barriers; interleaved with each other's kernels they hung
+// about one run in ten of tests/test_gpu_concurrency.py even with the grids
+// ordered by coop_launch. Calls stay re-entrant per context and results are
+// unchanged; concurrent callers queue on the host instead.
+std::recursive_mutex g_api_mu;
+
 template <class F>
 cyc_status guard(F&& f) {
+  std::lock_guard<std::recursive_mutex> api_lock(g_api_mu);
   try {
     f();
     return CYC_OK;
@@ -444,6 +466,7 @@ cyc_status cyc_ctx_set_stream(cyc_ctx* ctx, void* stream, int external) {
 
 cyc_status cyc_graph_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
                            const uint64_t* acc_words, int orientation, cyc_graph** out) {
+  CallTrace trace_("cyc_graph_build");
   return guard([&] {
     require(ctx && out, CYC_E_CONTRACT, "null argument");
     CYC_CUDA(cudaSetDevice(ctx->device));
@@ -544,6 +567,7 @@ cyc_status cyc_graph_log_prefix(const cyc_graph* g, uint64_t* m_log) {
 }
 
 cyc_status cyc_graph_restrict(cyc_ctx* ctx, const cyc_graph* in, cyc_graph** out) {
+  CallTrace trace_("cyc_graph_restrict");
   return guard([&] {
     require(ctx && in && out, CYC_E_CONTRACT, "null argument");
     CYC_CUDA(cudaSetDevice(ctx->device));
@@ -693,6 +717,7 @@ cyc_status cyc_demote(cyc_ctx* ctx, const uint32_t* values, uint32_t n,
 cyc_status cyc_map_run(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words,
                        const cyc_map_options* opt, cyc_map_stats* stats, uint32_t* final_values,
                        uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap) {
+  CallTrace trace_("cyc_map_run");
   return guard([&] {
     require(ctx && g, CYC_E_CONTRACT, "run_map: null argument");
     cyc_map_options o = opt ? *opt : default_opts();
@@ -739,6 +764,7 @@ cyc_status cyc_scc_verdict(cyc_ctx* ctx, const cyc_graph* g, int32_t* cycle, uin
 
 cyc_status cyc_owcty(cyc_ctx* ctx, const cyc_graph* g, const uint64_t* acc_words, int32_t* cycle,
                      uint32_t* witness, cyc_owcty_stats* stats) {
+  CallTrace trace_("cyc_owcty");
   return guard([&] {
     require(ctx && g, CYC_E_CONTRACT, "run_owcty: null argument");
     CYC_CUDA(cudaSetDevice(ctx->device));

@@ -19,6 +19,7 @@
 // Every SCC found is kept iff it holds an accepting vertex and is cyclic
 // (size >= 2 or a self-loop).
 #include <chrono>
+#include <pthread.h>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -645,7 +646,7 @@ struct SccLog {
   void mark(const char* what, int passes) {
     if (!on) return;
     auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[cyc scc] %-12s passes %5d %9.3f ms\n", what, passes,
+    std::fprintf(stderr, "[cyc scc %zx] %-12s passes %5d %9.3f ms\n", (size_t)pthread_self() & 0xFFFFFF, what, passes,
                  std::chrono::duration<double, std::milli>(now - t).count());
     t = now;
   }
