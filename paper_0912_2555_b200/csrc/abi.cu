@@ -8,7 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <mutex>
+#include <thread>
 #include <pthread.h>
 #include <string>
 #include <vector>
@@ -145,6 +147,11 @@ struct cyc_ctx {
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   cyc::DevBuf flush;
   cyc::BuildArena arena;  // grow-only build temporaries, reused by every build
+  // the second CSR of a large build runs on its own stream / arena / host
+  // thread, overlapping the first (created on first use)
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cyc::BuildArena arena2;
   std::atomic<int> refs{1};
 };
 
@@ -155,6 +162,7 @@ void ctx_release(cyc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ctx->flush.release();
   ctx->arena = cyc::BuildArena();
+  ctx->arena2 = cyc::BuildArena();
   big_trim(ctx->device, ctx->s);
   cudaStreamSynchronize(ctx->s);
   cudaEventDestroy(ctx->e0);
@@ -162,6 +170,12 @@ void ctx_release(cyc_ctx* ctx) {
   cudaEventDestroy(ctx->e2);
   cudaEventDestroy(ctx->e3);
   cudaStreamDestroy(ctx->own);
+  if (ctx->s2) {
+    cudaStreamSynchronize(ctx->s2);
+    cudaStreamDestroy(ctx->s2);
+    cudaEventDestroy(ctx->ev_in);
+    cudaEventDestroy(ctx->ev_out);
+  }
   delete ctx;
 }
 }  // namespace
@@ -324,6 +338,8 @@ __global__ void k_gen(cyc_gen_params p, uint32_t* edges, uint64_t* acc, uint64_t
   }
 }
 
+constexpr uint64_t kOverlapEdges = 1ull << 24;  // smaller logs build both CSRs in sequence
+
 void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
                  const uint64_t* acc_words, int orientation, cyc_graph* g) {
   require(orientation == CYC_FORWARD || orientation == CYC_TRANSPOSED, CYC_E_CONTRACT,
@@ -339,8 +355,41 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   g->orientation = orientation;
   g->m_log = m_log;
   const int snap_key_dst = orientation == CYC_TRANSPOSED;
-  cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>(), ctx->arena);
-  cyc::build_csr(de, m_log, n, !snap_key_dst, s, g->gath, err.as<uint32_t>(), ctx->arena);
+  if (m_log >= kOverlapEdges) {
+    // the two CSRs are independent given the log: the gather index is built
+    // on a second stream by a helper thread (every phase has host syncs, so
+    // one thread cannot keep both streams busy), overlapping the snapshot
+    if (!ctx->s2) {
+      CYC_CUDA(cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking));
+      CYC_CUDA(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+      CYC_CUDA(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+    }
+    CYC_CUDA(cudaEventRecord(ctx->ev_in, s));
+    std::exception_ptr helper_err;
+    std::thread helper([&] {
+      try {
+        CYC_CUDA(cudaSetDevice(ctx->device));
+        CYC_CUDA(cudaStreamWaitEvent(ctx->s2, ctx->ev_in, 0));
+        cyc::build_csr(de, m_log, n, !snap_key_dst, ctx->s2, g->gath, err.as<uint32_t>(), ctx->arena2);
+        CYC_CUDA(cudaEventRecord(ctx->ev_out, ctx->s2));
+      } catch (...) {
+        helper_err = std::current_exception();
+      }
+    });
+    std::exception_ptr main_err;
+    try {
+      cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>(), ctx->arena);
+    } catch (...) {
+      main_err = std::current_exception();
+    }
+    helper.join();
+    if (main_err) std::rethrow_exception(main_err);
+    if (helper_err) std::rethrow_exception(helper_err);
+    CYC_CUDA(cudaStreamWaitEvent(s, ctx->ev_out, 0));
+  } else {
+    cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>(), ctx->arena);
+    cyc::build_csr(de, m_log, n, !snap_key_dst, s, g->gath, err.as<uint32_t>(), ctx->arena);
+  }
   const bool dbg = std::getenv("CYC_DEBUG_TIMING") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
   uint32_t herr = 0;
