@@ -336,6 +336,7 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  static_assert(32u * R <= kRowPad && kRowPad % (32u * R) == 0, "a row group must not run past the row padding");
   const uint32_t np = a.n_pad;
   for (uint32_t base = gw * (32u * R); base < np; base += nw * (32u * R)) {
     uint32_t own[R], best[R];
