@@ -29,7 +29,7 @@ t0 = time.perf_counter()
 _abi.check(L.cyc_gen_fill(ctx.handle, C.byref(p), de, da))
 print(f"config {cfg}: n={p.n} m_log={p.m} generated in {time.perf_counter()-t0:.2f}s", flush=True)
 for early in (True, False):
-    opt = eng.MapOptions(early_exit=early, mode=mode).to_c()
+    opt = eng.MapOptions(early_exit=early, mode=mode, push_alpha=int(os.environ.get("ALPHA", "0"))).to_c()
     for rep in range(int(os.environ.get("REPS", "2"))):
         st = _abi.MapStatsC()
         ms = (C.c_double * 4)()
