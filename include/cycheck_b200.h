@@ -58,7 +58,18 @@ typedef struct cyc_map_options {
   uint64_t max_steps;      /* 0 = unbounded; else stop the first fixpoint after k steps */
   uint32_t push_alpha;     /* push when frontier edges * alpha < m (0 = default 16) */
   uint32_t trace_cap;      /* > 0: record up to this many steps (cyc_map_trace) */
+  int32_t layout;          /* CYC_LAYOUT_*: storage order of the map vector (default AUTO) */
+  int32_t reserved;
 } cyc_map_options;
+
+/* Storage order of the map vector and CSRs inside run_map (results are the
+ * same in every layout). DEGREE stores vertices by descending gather count so
+ * the hot words of a power-law graph share L2 sectors; AUTO picks it when the
+ * vector is larger than ~1/3 of L2 and the n/8 most-gathered vertices take at
+ * least half of the gathers. The plan is built once per graph and layout. */
+#define CYC_LAYOUT_AUTO 0
+#define CYC_LAYOUT_IDENTITY 1
+#define CYC_LAYOUT_DEGREE 2
 
 /* reference map_engine.hpp:101-106 MapStats + types.hpp:18-27 Verdict, plus
  * device-side evidence for the roofline. */

@@ -63,6 +63,19 @@ def bools_from_words(words, n: int) -> np.ndarray:
     return np.unpackbits(w.view(np.uint8), bitorder="little")[:n].astype(bool)
 
 
+class GenParams(C.Structure):
+    """Mirror of cyc_gen_params (include/cyc_gen.h), kept here so the checker
+    never imports the engine package (the reference arm must not map it)."""
+
+    _fields_ = [("kind", C.c_int32), ("n", C.c_uint32), ("m", C.c_uint64), ("seed", C.c_uint64),
+                ("deg", C.c_uint32), ("acc_thr", C.c_uint64), ("L", C.c_uint32), ("W", C.c_uint32),
+                ("S", C.c_uint32), ("exit_all", C.c_uint32), ("acc_all", C.c_uint32),
+                ("scale", C.c_uint32), ("edgefactor", C.c_uint32), ("thr_a", C.c_uint64),
+                ("thr_ab", C.c_uint64), ("thr_abc", C.c_uint64), ("perm_mul1", C.c_uint64),
+                ("perm_mul2", C.c_uint64), ("grid_bits", C.c_uint32), ("region", C.c_uint32),
+                ("plant", C.c_uint32), ("reserved", C.c_uint32)]
+
+
 class _Csr(C.Structure):
     _fields_ = [("n", C.c_uint32), ("m", C.c_uint64), ("off", C.POINTER(C.c_uint64)),
                 ("col", C.POINTER(C.c_uint32))]
@@ -226,7 +239,6 @@ class Restatement:
 
     # --- generators (include/cyc_gen.h)
     def preset(self, index: int):
-        from paper_0912_2555_b200._abi import GenParams
         p = GenParams()
         if self.lib.cyo_gen_preset(index, C.byref(p)) != 0:
             raise ValueError(f"unknown config {index}")

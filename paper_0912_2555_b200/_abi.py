@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libcycheck_b200.so")
+# CYC_LIB_PATH: an alternative build of the same library (tuning experiments)
+LIB_PATH = os.environ.get("CYC_LIB_PATH") or os.path.join(_HERE, "_lib", "libcycheck_b200.so")
 
 
 class CycheckError(RuntimeError):
@@ -44,6 +45,7 @@ _ERRORS = {1: ContractError, 2: ResourceLimitError, 3: CudaError, 4: CycheckErro
 
 CYC_FORWARD, CYC_TRANSPOSED = 0, 1
 CYC_MODE_AUTO, CYC_MODE_PULL, CYC_MODE_PUSH = 0, 1, 2
+CYC_LAYOUT_AUTO, CYC_LAYOUT_IDENTITY, CYC_LAYOUT_DEGREE = 0, 1, 2
 
 
 class MapOptionsC(C.Structure):
@@ -54,6 +56,8 @@ class MapOptionsC(C.Structure):
         ("max_steps", C.c_uint64),
         ("push_alpha", C.c_uint32),
         ("trace_cap", C.c_uint32),
+        ("layout", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -151,7 +155,7 @@ _SIGS = {
                             C.POINTER(MapOptionsC), C.POINTER(MapStatsC), C.POINTER(C.c_double)]),
     "cyc_scc_verdict": (C.c_int, [_P, _P, C.POINTER(C.c_int32), _U32P, _P, _U64P]),
     "cyc_owcty": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int32), _U32P, C.POINTER(OwctyStatsC)]),
-    "cyc_gen_fill": (C.c_int, [_P, C.POINTER(GenParams), _P, _P]),
+    "cyc_gen_fill": (C.c_int, [_P, _P, _P, _P]),  # any cyc_gen_params mirror (oracle has its own)
     "cyc_gen_preset": (C.c_int, [C.c_int, C.POINTER(GenParams)]),
     "cyc_gen_prepare": (C.c_int, [C.POINTER(GenParams)]),
     "cyc_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_P)]),

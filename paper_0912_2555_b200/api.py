@@ -556,13 +556,18 @@ class MapOptions:
     mode: str = "auto"            # "auto" | "pull" | "push"
     push_alpha: int = 0
     trace_cap: int = 0            # > 0: keep a per-step device trace (map_trace)
+    layout: str = "auto"          # "auto" | "identity" | "degree": storage order (same results)
 
     def to_c(self, max_iterations: int = 0, max_steps: int = 0) -> _abi.MapOptionsC:
         modes = {"auto": _abi.CYC_MODE_AUTO, "pull": _abi.CYC_MODE_PULL, "push": _abi.CYC_MODE_PUSH}
+        layouts = {"auto": _abi.CYC_LAYOUT_AUTO, "identity": _abi.CYC_LAYOUT_IDENTITY,
+                   "degree": _abi.CYC_LAYOUT_DEGREE}
         if self.mode not in modes:
             raise ContractError(f"unknown mode {self.mode!r}")
+        if self.layout not in layouts:
+            raise ContractError(f"unknown layout {self.layout!r}")
         return _abi.MapOptionsC(int(bool(self.early_exit)), modes[self.mode], max_iterations,
-                                max_steps, int(self.push_alpha), int(self.trace_cap))
+                                max_steps, int(self.push_alpha), int(self.trace_cap), layouts[self.layout], 0)
 
 
 @dataclass

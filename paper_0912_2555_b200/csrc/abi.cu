@@ -21,6 +21,7 @@
 #include "gen.cuh"
 #include "ingest.cuh"
 #include "map_run.cuh"
+#include "plan.cuh"
 #include "owcty.cuh"
 #include "scc.cuh"
 
@@ -201,6 +202,7 @@ struct cyc_graph {
   cyc::DevBuf acc;   // u64 words
   cyc::DevBuf kept;  // u32[n] original ids (restricted graphs)
   cyc::RunWs ws;
+  cyc::MapPlan plan;  // storage layout of the MAP loop (plan.cuh), built on first use
   uint32_t n() const { return gath.n; }
 };
 
@@ -440,19 +442,32 @@ cyc::RunOut run_loop(cyc_ctx* ctx, cyc_graph* g, const uint64_t* acc_words,
   cudaStream_t s = ctx->s;
   const uint32_t n = g->n();
   require(o.mode >= CYC_MODE_AUTO && o.mode <= CYC_MODE_PUSH, CYC_E_CONTRACT, "bad mode");
-  g->ws.ensure(n, g->gath.m, g->snap.o(), s);
+  require(o.layout >= CYC_LAYOUT_AUTO && o.layout <= CYC_LAYOUT_DEGREE, CYC_E_CONTRACT, "bad layout");
+  cyc::build_plan(g->snap, g->gath, o.layout, g->plan, s);
+  const bool rl = g->plan.relabel;
+  const cyc::DevCsr& snap = rl ? g->plan.snap : g->snap;
+  const cyc::DevCsr& gath = rl ? g->plan.gath : g->gath;
+  const uint32_t* orig = rl ? g->plan.orig.as<uint32_t>() : nullptr;
+  const uint32_t* perm = rl ? g->plan.perm.as<uint32_t>() : nullptr;
+  g->ws.ensure(n, gath.m, snap.o(), s);
   const size_t nw = acc_words64(n);
+  DevBuf fin;  // accepting words in vertex-id order, permuted into storage order below
+  if (rl) fin.alloc((nw + 1) * 8, s);
+  uint64_t* F = rl ? fin.as<uint64_t>() : g->ws.F.as<uint64_t>();
   if (acc_words) {
-    CYC_CUDA(cudaMemcpyAsync(g->ws.F.p, acc_words, nw * 8, cudaMemcpyDefault, s));
+    CYC_CUDA(cudaMemcpyAsync(F, acc_words, nw * 8, cudaMemcpyDefault, s));
   } else {
-    CYC_CUDA(cudaMemcpyAsync(g->ws.F.p, g->acc.p, nw * 8, cudaMemcpyDeviceToDevice, s));
+    CYC_CUDA(cudaMemcpyAsync(F, g->acc.p, nw * 8, cudaMemcpyDeviceToDevice, s));
   }
   if (nw) {
-    k_trim_tail<<<1, 1, 0, s>>>(g->ws.F.as<uint64_t>(), n);
+    k_trim_tail<<<1, 1, 0, s>>>(F, n);
     CYC_LAUNCHED();
   }
+  if (rl) cyc::permute_bits(reinterpret_cast<const uint32_t*>(F), orig, n, g->ws.F.as<uint32_t>(), s);
   cyc::RunOut out;
-  cyc::launch_map_run(g->snap, g->gath, g->ws, o.early_exit != 0, o.mode, o.max_iterations,
+  cyc::launch_map_run(snap, gath, orig, perm, rl ? g->plan.sdesc.as<uint4>() : nullptr,
+                      rl ? g->plan.sell.as<uint32_t>() : nullptr, rl ? g->plan.hcol.as<uint32_t>() : nullptr,
+                      rl ? g->plan.hrow.as<uint32_t>() : nullptr, rl ? g->plan.n_hchunks : 0u, g->ws, o.early_exit != 0, o.mode, o.max_iterations,
                       o.max_steps, o.push_alpha, cap, o.trace_cap, s, ctx->e0, ctx->e1, out);
   return out;
 }

@@ -34,6 +34,8 @@
 // confirmed after the barrier by reading the new buffer.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/cyc_gen.h"
@@ -46,12 +48,55 @@ namespace cyc {
 namespace {
 
 constexpr int kRunThreads = 1024;
+// threads of the degree-ordered instantiation (C3 loop, 8 steps: 512 -> 28.9
+// ms, 768 -> 25.8, 1024 -> 24.8; scripts/build_variant.sh)
+#ifndef CYC_RL_THREADS
+#define CYC_RL_THREADS 1024
+#endif
+constexpr int kRunThreadsRL = CYC_RL_THREADS;
+#ifndef CYC_SLAB_B
+#define CYC_SLAB_B 2
+#endif
+template <bool RL>
+constexpr int run_threads() { return RL ? kRunThreadsRL : kRunThreads; }
 constexpr int kModePull = 1, kModePush = 2;
 constexpr int kRows = 4;            // rows per lane in a pull step (the ovf test below assumes 4)
 static_assert(kRows == 4, "pull overflow test unrolled for 4 rows");
 constexpr int kBatch = 4;           // frontier vertices per lane in a push step
 constexpr int kHeavyPerLane = kHeavyChunk / 32;  // pull heavy chunk edges per lane
 constexpr int kHeavyBatch = 4;                     // heavy chunks in flight per warp
+
+// Column streams (slab, sliced ELL, heavy chunks and their descriptors) are
+// read once per step: load them evict-first so they do not push the hot map
+// words out of L2 (ld.global.cs).
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
+
+// Frontier filter of a pull step on a degree-ordered plan. Step k's pull
+// only needs the sources that changed in step k-1: x_{k-1}[v] already
+// dominates cand_{k-2}(u) for every gathered u, and F is fixed within a
+// fixpoint, so an unchanged source cannot raise anyone (map_engine.cpp:56-63
+// computes the same maximum over all sources). The previous step's frontier
+// bits of positions [0, k) -- the most-gathered vertices, ~65 % of all
+// gathers on config 3 for k = 2^19 -- are staged in shared memory; a gather
+// from such a position is issued only if its bit is set. Measured: the random
+// L2 gathers are what bounds a dense step (~283 G/s per GPU,
+// scripts/micro/gather_bw.cu), so every skipped one counts.
+// (the array is referenced directly, not through a pointer, so the compiler
+// addresses it in the shared window without per-access conversions)
+extern __shared__ uint32_t hot_sh[];
+
+struct Hot {
+  uint32_t k;  // positions with staged frontier bits (0: no filter)
+};
+
+__device__ __forceinline__ uint32_t ld_word(const Hot& h, const uint32_t* __restrict__ P, uint32_t u) {
+  bool need = true;
+  if (u < h.k) need = (hot_sh[u >> 5] >> (u & 31u)) & 1u;
+  uint32_t w = 0;  // NIL: contributes nothing to the maximum
+  if (need) w = __ldca(P + u);
+  return w;
+}
 
 __device__ __forceinline__ bool bit_of(const uint32_t* words, uint32_t v) {
   return (__ldcg(words + (v >> 5)) >> (v & 31u)) & 1u;
@@ -77,9 +122,21 @@ __device__ __forceinline__ void phase_mark(const RunArgs& a, unsigned long long 
   }
 }
 
-// candidate value a vertex u with map word w contributes to its successors
-__device__ __forceinline__ uint32_t cand_of(uint32_t w, uint32_t u) {
-  return (w & kFlag) ? max(w & kCode, u + 1u) : w;
+// vertex id of storage position p (plan.cuh; identity without a plan)
+// (RL: the run uses a relabelled plan; a separate instantiation keeps the
+// identity layout's loops free of the lookups)
+template <bool RL>
+__device__ __forceinline__ uint32_t oid(const RunArgs& a, uint32_t p) {
+  if constexpr (RL) return __ldg(a.orig + p);
+  return p;
+}
+
+// candidate value the vertex at position u with map word w contributes to its
+// successors: max(x[u], id(u)+1 if accepting) (map_engine.cpp:56-63)
+template <bool RL>
+__device__ __forceinline__ uint32_t cand_of(const RunArgs& a, uint32_t w, uint32_t u) {
+  if constexpr (RL) return (w & kFlag) ? max(w & kCode, oid<RL>(a, u) + 1u) : w;
+  return max(w & kCode, (w >> 31) * (u + 1u));
 }
 
 // ---------------------------------------------------------- block helpers
@@ -286,7 +343,7 @@ struct PushCtx {
 // Batched Jacobi push of val[r] into tgt[r], as predicated stages (read the
 // frozen value, fire-and-forget atomicMax, frontier mark, big-vertex chunks)
 // so the R chains of a lane overlap.
-template <int R>
+template <bool RL, int R>
 __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
                                             const uint32_t (&tgt)[R], const uint32_t (&val)[R],
                                             StepAcc& acc) {
@@ -318,18 +375,63 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
     acc.first += first[r];
     acc.fedges += e[r] - b[r];
     if ((bw[r] >> (tgt[r] & 31u)) & 1u) acc.fedges += enlist(a, tgt[r], c.bc, c.nchunk, c.sh);
-    if (go[r] && (old[r] & kFlag) && val[r] == tgt[r] + 1u) c.Cn[atomicAdd(c.ccnt, 1u)] = tgt[r];
+    if (go[r] && (old[r] & kFlag) && val[r] == oid<RL>(a, tgt[r]) + 1u) c.Cn[atomicAdd(c.ccnt, 1u)] = tgt[r];
   }
 }
 
 // ------------------------------------------------------------------ pull
+// End of a light row group (R rows per lane, rows base + 32k + lane): write
+// the new words (rows flagged in `skip` belong to the heavy-chunk pass), the
+// exact self-witness, the next frontier words and big-vertex chunks.
+template <bool RL, int R>
+__device__ __forceinline__ void rows_epilogue(const RunArgs& a, uint32_t base, const uint32_t (&own)[R],
+                                              const uint32_t (&best)[R], uint32_t skip, uint32_t* __restrict__ Q,
+                                              uint32_t* fb, BlockSh* sh, uint32_t* fp, uint4* bc, SlotCtl* sl,
+                                              StepAcc& acc) {
+  const uint32_t lane = lane_id();
+  uint32_t words[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const uint32_t v = base + 32u * k + lane;
+    const bool up = !((skip >> k) & 1u) && best[k] > (own[k] & kCode);
+    if (!((skip >> k) & 1u)) Q[v] = (own[k] & kFlag) | best[k];
+    if ((own[k] & kFlag) && !((skip >> k) & 1u)) {
+      const uint32_t id = oid<RL>(a, v);
+      if (best[k] == id + 1u) atomicMin(&sl->wit, id);
+    }
+    words[k] = __ballot_sync(kFull, up);
+    acc.raised += up;
+    acc.first += up;
+  }
+  // next frontier words (the bitmap is zero at step start; heavy rows are
+  // disjoint): fire-and-forget ORs, previous frontier words consumed
+  if (lane < (uint32_t)R) {
+    uint32_t wd = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) wd = lane == (uint32_t)k ? words[k] : wd;
+    const uint32_t wi = (base >> 5) + lane;
+    fp[wi] = 0u;
+    if (wd) {
+      atomicOr(fb + wi, wd);
+      note_word(sh, wi);
+    }
+  }
+  // raised vertices of big push degree: chunks for the next push step
+  uint32_t big[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) big[k] = words[k] ? __ldcg(a.bigm + (base >> 5) + k) & words[k] : 0u;
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    if ((big[k] >> lane) & 1u) acc.fedges += enlist(a, base + 32u * k + lane, bc, &sl->nchunk, sh);
+}
+
 // Light rows of a pull step. Each lane owns R rows (32*R consecutive rows per
 // warp, rows padded to a multiple of kRowPad so no bound checks). Their first
 // K columns come from the column-major HYB slab; absent entries point at the
 // always-NIL padding slot, so every gather is unconditional and the inner loop
 // is straight-line: one round trip for own values + slab, one for gathers.
 // Rows flagged in `ovf` (longer than K, or heavy) take a slow path.
-template <int K, int R>
+template <bool RL, int K, int R>
 __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __restrict__ P,
                                            uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh,
                                            uint32_t* fp, uint4* bc, SlotCtl* sl, StepAcc& acc) {
@@ -350,11 +452,11 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
     for (int j = 0; j < K; ++j) {
       uint32_t u[R];
 #pragma unroll
-      for (int k = 0; k < R; ++k) u[k] = __ldg(a.ell + (size_t)j * np + base + 32u * k + lane);
+      for (int k = 0; k < R; ++k) u[k] = ld_stream(a.ell + (size_t)j * np + base + 32u * k + lane);
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const uint32_t w = __ldca(P + u[k]);
-        const uint32_t c = max(w & kCode, (w >> 31) * (u[k] + 1u));
+        const uint32_t c = cand_of<RL>(a, w, u[k]);
         best[k] = j == 0 ? max(own[k] & kCode, c) : max(best[k], c);
       }
     }
@@ -374,43 +476,71 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
           } else {
             for (uint32_t i = b + K; i < e; ++i) {
               const uint32_t u = __ldg(a.gcol + i);
-              best[k] = max(best[k], cand_of(__ldca(P + u), u));
+              best[k] = max(best[k], cand_of<RL>(a, __ldca(P + u), u));
             }
           }
         }
       }
     }
-    uint32_t words[R];
+    rows_epilogue<RL, R>(a, base, own, best, skip, Q, fb, sh, fp, bc, sl, acc);
+  }
+}
+
+// Light rows from the sliced-ELL layout of a degree-ordered plan (plan.cuh):
+// slice s = rows [32s, 32s+32), padded to its own widest row, column-major, so
+// every column load is one coalesced 128 B line and no row takes a serial
+// overflow path (rows of similar length are neighbours in degree order). A
+// warp takes R slices; J columns of each per round, all R*J gathers in flight.
+template <bool RL, int R, int J>
+__device__ __forceinline__ void pull_sell(const RunArgs& a, const uint32_t* __restrict__ P,
+                                          uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh,
+                                          uint32_t* fp, uint4* bc, SlotCtl* sl, StepAcc& acc, const Hot& hot) {
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  static_assert((kRowPad / 32u) % R == 0, "slices per row padding must be a multiple of R");
+  const uint32_t np = a.n_pad, nsl = a.n_pad / 32u;
+  for (uint32_t s0 = gw * R; s0 < nsl; s0 += nw * R) {
+    const uint32_t base = s0 * 32u;
+    uint4 d[R];
+    uint32_t own[R], best[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const uint32_t v = base + 32u * k + lane;
-      const bool up = !((skip >> k) & 1u) && best[k] > (own[k] & kCode);
-      if (!((skip >> k) & 1u)) Q[v] = (own[k] & kFlag) | best[k];
-      if ((own[k] & kFlag) && best[k] == v + 1u && !((skip >> k) & 1u)) atomicMin(&sl->wit, v);
-      words[k] = __ballot_sync(kFull, up);
-      acc.raised += up;
-      acc.first += up;
+      d[k] = __ldg(a.sdesc + s0 + k);
+      own[k] = __ldca(P + base + 32u * k + lane);
     }
-    // next frontier words (the bitmap is zero at step start; heavy rows are
-    // disjoint): fire-and-forget ORs, previous frontier words consumed
-    if (lane < (uint32_t)R) {
-      uint32_t wd = 0;
+    uint32_t wmax = 0, skip = 0;
 #pragma unroll
-      for (int k = 0; k < R; ++k) wd = lane == (uint32_t)k ? words[k] : wd;
-      const uint32_t wi = (base >> 5) + lane;
-      fp[wi] = 0u;
-      if (wd) {
-        atomicOr(fb + wi, wd);
-        note_word(sh, wi);
+    for (int k = 0; k < R; ++k) {
+      best[k] = own[k] & kCode;
+      wmax = max(wmax, d[k].y);
+      skip |= ((d[k].z >> lane) & 1u) << k;
+    }
+    for (uint32_t j = 0; j < wmax; j += J) {
+      uint32_t u[R][J], w[R][J];
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int t = 0; t < J; ++t)
+          u[k][t] = j + t < d[k].y ? ld_stream(a.sell + ((size_t)d[k].x + j + t) * 32u + lane) : np;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int t = 0; t < J; ++t) w[k][t] = ld_word(hot, P, u[k][t]);
+      if constexpr (RL) {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int t = 0; t < J; ++t)
+            if (w[k][t] & kFlag) u[k][t] = __ldg(a.orig + u[k][t]);
       }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int t = 0; t < J; ++t)
+          best[k] = max(best[k], max(w[k][t] & kCode, (w[k][t] >> 31) * (u[k][t] + 1u)));
     }
-    // raised vertices of big push degree: chunks for the next push step
-    uint32_t big[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) big[k] = words[k] ? __ldcg(a.bigm + (base >> 5) + k) & words[k] : 0u;
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-      if ((big[k] >> lane) & 1u) acc.fedges += enlist(a, base + 32u * k + lane, bc, &sl->nchunk, sh);
+    rows_epilogue<RL, R>(a, base, own, best, skip, Q, fb, sh, fp, bc, sl, acc);
   }
 }
 
@@ -418,7 +548,7 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
 // most 32*kHeavyPerLane edges at once, every lane issuing all its loads
 // together; lane k finalises chunk k (own value prefetched) with an atomicMax
 // into Q (Q holds x_{k-2}, never larger).
-template <int B, bool PRE>
+template <bool RL, int B, bool PRE>
 __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __restrict__ P,
                                            uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh, uint4* bc,
                                            SlotCtl* sl, uint32_t* Cn, StepAcc& acc) {
@@ -432,27 +562,40 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       const uint32_t c = c0 + (uint32_t)k;
-      ch[k] = c < a.n_heavy ? a.heavy[c] : make_uint4(0u, 0u, 0u, 0u);
+      ch[k] = c < a.n_heavy ? ld_stream(a.heavy + c) : make_uint4(0u, 0u, 0u, 0u);
     }
     uint32_t own = 0;
 #pragma unroll
     for (int k = 0; k < B; ++k)
       if (lane == (uint32_t)k && ch[k].z > ch[k].y) own = __ldca(P + ch[k].x);
-    uint32_t u[B][kHeavyPerLane];
+    // every gather unconditional (absent edges read the always-NIL slot
+    // n_pad), all issued before any is used: B*kHeavyPerLane in flight per lane
+    uint32_t u[B][kHeavyPerLane], w[B][kHeavyPerLane];
 #pragma unroll
     for (int k = 0; k < B; ++k)
 #pragma unroll
       for (int r = 0; r < kHeavyPerLane; ++r) {
         const uint32_t i = ch[k].y + lane + 32u * r;
-        u[k][r] = i < ch[k].z ? __ldg(a.gcol + i) : kNone;
+        u[k][r] = i < ch[k].z ? ld_stream(a.gcol + i) : a.n_pad;
       }
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int r = 0; r < kHeavyPerLane; ++r) w[k][r] = __ldca(P + u[k][r]);
+    if constexpr (RL) {  // ids of the accepting sources only, again all in flight together
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+#pragma unroll
+        for (int r = 0; r < kHeavyPerLane; ++r)
+          if (w[k][r] & kFlag) u[k][r] = __ldg(a.orig + u[k][r]);
+    }
     uint32_t best[B];
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       best[k] = 0;
 #pragma unroll
       for (int r = 0; r < kHeavyPerLane; ++r)
-        if (u[k][r] != kNone) best[k] = max(best[k], cand_of(__ldca(P + u[k][r]), u[k][r]));
+        best[k] = max(best[k], max(w[k][r] & kCode, (w[k][r] >> 31) * (u[k][r] + 1u)));
     }
 #pragma unroll
     for (int k = 0; k < B; ++k) best[k] = __reduce_max_sync(kFull, best[k]);
@@ -479,12 +622,134 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
           ++acc.first;
           if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
         }
-        if ((own & kFlag) && mine == v + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
+        if ((own & kFlag) && mine == oid<RL>(a, v) + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
       }
     }
   }
 }
 
+// Finished heavy rows, one per lane (pv = row, pm = max of its chunks seen by
+// this warp, po = its frozen word): written back together so the dependent
+// round trips (Q precheck, frontier mark) are paid once per 32 rows.
+template <bool RL>
+__device__ __forceinline__ void heavy_flush(const RunArgs& a, bool live, uint32_t pv, uint32_t pm, uint32_t po,
+                                            uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh, uint4* bc,
+                                            SlotCtl* sl, uint32_t* Cn, StepAcc& acc) {
+  if (!live) return;
+  const uint32_t mine = max(pm, po & kCode), word = (po & kFlag) | mine;
+  // a row split between two warps is merged by atomicMax (Q holds x_{k-2} <= x_{k-1})
+  if (word > __ldcg(Q + pv)) atomicMax(Q + pv, word);
+  if (mine > (po & kCode)) {
+    ++acc.raised;
+    if (mark(fb, sh, pv, true)) {
+      ++acc.first;
+      if (bit_of(a.bigm, pv)) acc.fedges += enlist(a, pv, bc, &sl->nchunk, sh);
+    }
+    if ((po & kFlag) && mine == oid<RL>(a, pv) + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = pv;
+  }
+}
+
+// Heavy rows of a degree-ordered plan: chunk c = 128 columns at hcol[128c..]
+// (padded with the NIL slot n_pad), row hrow[c]; a row's chunks are
+// consecutive. A warp owns a contiguous chunk range and walks it B chunks per
+// round with the next round's columns, rows and own words prefetched, so the
+// critical path is one gather round trip per round. Rows are merged in
+// registers while the warp stays on them (a hub row's thousands of chunks
+// cost one write-back per warp, not one atomic per chunk).
+template <bool RL>
+__device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t* __restrict__ P,
+                                                uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh, uint4* bc,
+                                                SlotCtl* sl, uint32_t* Cn, StepAcc& acc, const Hot& hot) {
+  constexpr int B = CYC_SLAB_B, H = kHeavyPerLane;
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nh = a.n_hchunks, np = a.n_pad;
+  const uint32_t cb = (uint32_t)((uint64_t)gw * nh / nw), ce = (uint32_t)((uint64_t)(gw + 1u) * nh / nw);
+  if (cb >= ce) return;
+  uint32_t u[B][H], rr[B], ro[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    const bool ok = cb + k < ce;
+    rr[k] = ok ? ld_stream(a.hrow + cb + k) : kNone;
+#pragma unroll
+    for (int r = 0; r < H; ++r) u[k][r] = ok ? ld_stream(a.hcol + (size_t)(cb + k) * kHeavyChunk + 32u * r + lane) : np;
+  }
+#pragma unroll
+  for (int k = 0; k < B; ++k) ro[k] = rr[k] != kNone ? __ldca(P + rr[k]) : 0u;
+  uint32_t row = kNone, rmax = 0, rown = 0;       // the row this warp is on (uniform)
+  uint32_t pv = 0, pm = 0, po = 0, npend = 0;     // finished rows awaiting write-back
+  for (uint32_t c = cb; c < ce; c += B) {
+    uint32_t w[B][H];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int r = 0; r < H; ++r) w[k][r] = ld_word(hot, P, u[k][r]);
+    uint32_t un[B][H], rn[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const bool ok = c + B + k < ce;
+      rn[k] = ok ? ld_stream(a.hrow + c + B + k) : kNone;
+#pragma unroll
+      for (int r = 0; r < H; ++r)
+        un[k][r] = ok ? ld_stream(a.hcol + (size_t)(c + B + k) * kHeavyChunk + 32u * r + lane) : np;
+    }
+    if constexpr (RL) {
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+#pragma unroll
+        for (int r = 0; r < H; ++r)
+          if (w[k][r] & kFlag) u[k][r] = __ldg(a.orig + u[k][r]);
+    }
+    uint32_t best[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      best[k] = 0;
+#pragma unroll
+      for (int r = 0; r < H; ++r) best[k] = max(best[k], max(w[k][r] & kCode, (w[k][r] >> 31) * (u[k][r] + 1u)));
+      best[k] = __reduce_max_sync(kFull, best[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (rr[k] == kNone) continue;
+      if (rr[k] != row) {
+        if (row != kNone) {
+          if (lane == npend) {
+            pv = row;
+            pm = rmax;
+            po = rown;
+          }
+          if (++npend == 32u) {
+            heavy_flush<RL>(a, true, pv, pm, po, Q, fb, sh, bc, sl, Cn, acc);
+            npend = 0;
+          }
+        }
+        row = rr[k];
+        rmax = 0;
+        rown = ro[k];
+      }
+      rmax = max(rmax, best[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {  // next round's own words: its rows have arrived by now
+      rr[k] = rn[k];
+      ro[k] = rn[k] != kNone ? __ldca(P + rn[k]) : 0u;
+#pragma unroll
+      for (int r = 0; r < H; ++r) u[k][r] = un[k][r];
+    }
+  }
+  if (row != kNone) {
+    if (lane == npend) {
+      pv = row;
+      pm = rmax;
+      po = rown;
+    }
+    ++npend;
+  }
+  heavy_flush<RL>(a, lane < npend, pv, pm, po, Q, fb, sh, bc, sl, Cn, acc);
+}
+
+template <bool RL>
 __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, unsigned long long tk) {
   const uint32_t* __restrict__ P = a.P[cur];
   uint32_t* __restrict__ Q = a.P[cur ^ 1];
@@ -497,17 +762,27 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
+  Hot hot{0u};
+  if (RL && a.hot_k) {  // stage the previous step's frontier bits of the hottest positions
+    for (uint32_t i = threadIdx.x; i < a.hot_k / 32u; i += blockDim.x) hot_sh[i] = __ldcg(fp + i);
+    // rows_epilogue clears fp words as it goes: every CTA stages first
+    cg::this_grid().sync();
+    hot.k = a.hot_k;
+  }
   // many chunks per warp (R-MAT hubs): four in flight, and reads before the
   // contended atomics; few (config 2's connectors): one per warp, spread over
   // more warps, no extra round trip
-  if (a.n_heavy > 4u * nw) pull_heavy<kHeavyBatch, true>(a, P, Q, fb, sh, bc, sl, Cn, acc);
-  else pull_heavy<1, false>(a, P, Q, fb, sh, bc, sl, Cn, acc);
+  if (a.hcol) pull_heavy_slab<RL>(a, P, Q, fb, sh, bc, sl, Cn, acc, hot);
+  else if (a.n_heavy > 4u * nw) pull_heavy<RL, kHeavyBatch, true>(a, P, Q, fb, sh, bc, sl, Cn, acc);
+  else pull_heavy<RL, 1, false>(a, P, Q, fb, sh, bc, sl, Cn, acc);
   phase_mark(a, tk, 0);
-  switch (a.ell_k) {
-    case 1: pull_light<1, 8>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
-    case 2: pull_light<2, 8>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
-    case 4: pull_light<4, 4>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
-    default: pull_light<8, 4>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
+  if (a.sdesc) {
+    pull_sell<RL, 2, 4>(a, P, Q, fb, sh, fp, bc, sl, acc, hot);
+  } else switch (a.ell_k) {
+    case 1: pull_light<RL, 1, 8>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
+    case 2: pull_light<RL, 2, 8>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
+    case 4: pull_light<RL, 4, 4>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
+    default: pull_light<RL, 8, 4>(a, P, Q, fb, sh, fp, bc, sl, acc); break;
   }
   phase_mark(a, tk, 1);
   step_flags(a, acc, sl, sh, a.WL[g & 1u], a.wl_cap, a.BC[g & 1u]);
@@ -515,6 +790,7 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
 }
 
 // ------------------------------------------------------------------ push
+template <bool RL>
 __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, unsigned long long tk) {
   SlotCtl* sl = &a.ctl->slot[g % 3u];
   const SlotCtl* pl = &a.ctl->slot[(g - 1u) % 3u];
@@ -542,7 +818,7 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t nch = min(__ldca(&pl->nchunk), a.chunk_cap);
   for (uint32_t k = gw; k < nch; k += nw) {
     const uint4 ch = bp[k];
-    const uint32_t vv = cand_of(__ldca(c.Pc + ch.x), ch.x);
+    const uint32_t vv = cand_of<RL>(a, __ldca(c.Pc + ch.x), ch.x);
     uint32_t t[kChunk / 32], val[kChunk / 32];
 #pragma unroll
     for (int r = 0; r < (int)(kChunk / 32); ++r) {
@@ -550,7 +826,7 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
       t[r] = i < ch.z ? __ldg(a.pcol + i) : kNone;
       val[r] = vv;
     }
-    raise_batch(a, c, t, val, acc);
+    raise_batch<RL>(a, c, t, val, acc);
   }
   phase_mark(a, tk, 0);
   // every frontier vertex: max-copy itself into the new buffer, and push its
@@ -595,7 +871,7 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
         b[r] = __ldg(a.poff + v[r]);
         e[r] = __ldg(a.poff + v[r] + 1);
         atomicMax(c.Pn + v[r], xu);  // bring x_{k-2} up to x_{k-1}
-        val[r] = cand_of(xu, v[r]);
+        val[r] = cand_of<RL>(a, xu, v[r]);
         if ((bwv >> (v[r] & 31u)) & 1u) e[r] = b[r];  // big: chunks push its edges
       }
     }
@@ -608,7 +884,7 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
         any |= t[r] != kNone;
       }
       if (!any) break;
-      raise_batch(a, c, t, val, acc);
+      raise_batch<RL>(a, c, t, val, acc);
     }
   }
   phase_mark(a, tk, 1);
@@ -620,6 +896,7 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
 // Dense pass over the fixpoint vector: iteration hash, full self-witness (for
 // early_exit = false, map_engine.cpp:108-112) and the "used" bitmap of demote
 // (map_engine.cpp:124-126).
+template <bool RL>
 __device__ void finish_pass(const RunArgs& a, int cur, uint64_t t, bool mark_used, BlockSh* sh) {
   const uint32_t* P = a.P[cur];
   RunCtl* ctl = a.ctl;
@@ -633,14 +910,16 @@ __device__ void finish_pass(const RunArgs& a, int cur, uint64_t t, bool mark_use
     uint32_t code = 0;
     if (v < a.n) {
       const uint32_t x = __ldcg(P + v);
+      const uint32_t id = oid<RL>(a, v);
       code = x & kCode;
-      h += cyc_splitmix64(((unsigned long long)v << 32) | code);
-      if ((x & kFlag) && code == v + 1u) fw = min(fw, v);
+      h += cyc_splitmix64(((unsigned long long)id << 32) | code);
+      if ((x & kFlag) && code == id + 1u) fw = min(fw, id);
     }
     if (mark_used) {
       const uint32_t peers = __match_any_sync(kFull, code);
       if (code && (__ffs(peers) - 1) == (int)lane) {
-        const uint32_t u = code - 1u, bit = 1u << (u & 31u);
+        // the value is a vertex id + 1; its accepting bit lives at its position
+        const uint32_t u = RL ? __ldg(a.perm + (code - 1u)) : code - 1u, bit = 1u << (u & 31u);
         if (!(__ldcg(a.used + (u >> 5)) & bit)) atomicOr(a.used + (u >> 5), bit);
       }
     }
@@ -742,7 +1021,8 @@ __device__ __forceinline__ void reset_slot(RunCtl* c, uint32_t s) {
   sl.wl_over = 0;
 }
 
-__global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
+template <bool RL>
+__global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
   __shared__ BlockSh sh;
   // run statistics live in shared memory of block 0 (kept out of registers)
   __shared__ unsigned long long stat[kResTag + 1];
@@ -804,13 +1084,13 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
             stat[kResBytes] += 8ull * fe + 12ull * nr;
             stat[kResPushSteps] += 1;
           }
-          push_step(a, g, cur, &sh, a.trace ? tkk : ~0ull);
+          push_step<RL>(a, g, cur, &sh, a.trace ? tkk : ~0ull);
         } else {
           CYC_STAT(kResEdges, a.m);
           CYC_STAT(kResRows, a.n);
           CYC_STAT(kResBytes, 8ull * a.m + 12ull * a.n + 4ull);
           CYC_STAT(kResPullSteps, 1);
-          pull_step(a, g, cur, &sh, a.trace ? tkk : ~0ull);
+          pull_step<RL>(a, g, cur, &sh, a.trace ? tkk : ~0ull);
         }
         grid.sync();
         cur ^= 1;
@@ -833,7 +1113,8 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
           uint32_t mine = kNone;
           for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
             const uint32_t c = __ldcg(Cn + i);
-            if ((__ldcg(Pn + c) & kCode) == c + 1u) mine = min(mine, c);
+            const uint32_t id = oid<RL>(a, c);
+            if ((__ldcg(Pn + c) & kCode) == id + 1u) mine = min(mine, id);
           }
           w = min(w, block_min(mine, &sh));
         }
@@ -854,7 +1135,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_map_run(RunArgs a) {
         CYC_STAT(kResKernelCalls, steps);
         break;
       }
-      finish_pass(a, cur, t, !cycle, &sh);
+      finish_pass<RL>(a, cur, t, !cycle, &sh);
       grid.sync();
       if (!a.early_exit) {
         const uint32_t fw = __ldca(&ctl->it_finwit[t & 1u]);
@@ -911,6 +1192,13 @@ __global__ void k_big_mask(uint32_t n, const uint32_t* __restrict__ poff, uint32
 __global__ void k_strip(const uint32_t* __restrict__ P, uint32_t n, uint32_t* __restrict__ out) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) out[v] = P[v] & kCode;
+}
+
+// storage positions back to vertex ids: out[orig[p]] = code(P[p])
+__global__ void k_strip_perm(const uint32_t* __restrict__ P, const uint32_t* __restrict__ orig, uint32_t n,
+                             uint32_t* __restrict__ out) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) out[__ldg(orig + p)] = P[p] & kCode;
 }
 
 // ----------------------------------------------------- standalone kernels
@@ -1266,7 +1554,15 @@ __global__ void k_demote_list(uint32_t nwords, const uint32_t* __restrict__ acc,
 }  // namespace
 
 void RunWs::ensure(uint32_t nn, uint32_t mm, const uint32_t* poff, cudaStream_t s) {
-  if (ctl.p && n == nn && m == mm) return;
+  if (ctl.p && n == nn && m == mm) {
+    if (poff != bigm_src && nn) {  // layout changed: big-degree mask of the new push rows
+      k_big_mask<<<grid_for((uint64_t)nn, 256, 8), 256, 0, s>>>(nn, poff, bigm.as<uint32_t>());
+      CYC_LAUNCHED();
+      bigm_src = poff;
+    }
+    return;
+  }
+  bigm_src = poff;
   n = nn;
   m = mm;
   n_pad = (uint32_t)(((uint64_t)nn + kRowPad - 1) / kRowPad * kRowPad);
@@ -1296,7 +1592,9 @@ void RunWs::ensure(uint32_t nn, uint32_t mm, const uint32_t* poff, cudaStream_t 
   ctl.alloc(sizeof(RunCtl), s);
 }
 
-void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early_exit, int mode,
+void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig, const uint32_t* perm,
+                    const uint4* sdesc, const uint32_t* sell, const uint32_t* hcol, const uint32_t* hrow,
+                    uint32_t n_hchunks, RunWs& ws, int early_exit, int mode,
                     unsigned long long max_iterations, unsigned long long max_steps,
                     uint32_t alpha, unsigned long long cap, uint32_t trace_cap, cudaStream_t s,
                     cudaEvent_t e0, cudaEvent_t e1, RunOut& out) {
@@ -1336,6 +1634,34 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
   a.wl_cap = ws.wl_cap;
   a.F = ws.F.as<uint32_t>();
   a.used = ws.used.as<uint32_t>();
+  a.orig = orig;
+  a.perm = perm;
+  a.sdesc = sdesc;
+  a.sell = sell;
+  a.hcol = hcol;
+  a.hrow = hrow;
+  a.n_hchunks = n_hchunks;
+  // shared-memory staging of the hottest map words (degree-ordered plans only)
+  static const size_t hot_cap = [] {  // thread-safe one-time init
+    int dev = 0, optin = 0;
+    CYC_CUDA(cudaGetDevice(&dev));
+    CYC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    CYC_CUDA(cudaFuncGetAttributes(&fa, k_map_run<true>));
+    // measured (scripts/micro/gather_mix.cu): random L2 gathers hold ~283 G/s
+    // per GPU with up to 128 KB of shared memory per SM and halve at 200 KB
+    // (the L1 carve-out that tracks in-flight loads shrinks), so stop at 128 KB
+    size_t cap = (size_t)optin > fa.sharedSizeBytes + 1024 ? (size_t)optin - fa.sharedSizeBytes - 1024 : 0;
+    cap = std::min<size_t>(cap, 128u << 10);
+    CYC_CUDA(cudaFuncSetAttribute(k_map_run<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+    return cap;
+  }();
+  // frontier bits of the first CYC_HOT_POS positions (tested at 2^19 = 64 KB)
+  const char* hk = std::getenv("CYC_HOT_POS");
+  uint64_t hot_pos = hk ? std::strtoull(hk, nullptr, 10) : 0ull;  // off by default: no gain measured on C3
+  hot_pos = orig ? std::min<uint64_t>({hot_pos, (uint64_t)hot_cap * 8, (uint64_t)ws.n_pad}) : 0;
+  a.hot_k = (uint32_t)(hot_pos / 32u * 32u);
+  ws.orig = orig;
   a.nwords = (uint32_t)(((uint64_t)n + 31) / 32);
   a.nwords_pad = ws.n_pad / 32u;
   a.chunk_cap = ws.chunk_cap;
@@ -1357,13 +1683,19 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
 
   static const int blocks_per_sm = [] {  // thread-safe one-time init
     int b = 0;
-    CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_map_run, kRunThreads, 0));
+    CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_map_run<false>, kRunThreads, 0));
     return b > 0 ? b : 1;
   }();
-  dim3 grid((unsigned)(sm_count() * blocks_per_sm)), block(kRunThreads);
+  const size_t dyn = (size_t)a.hot_k / 8;
+  int bps = blocks_per_sm;
+  if (orig) {
+    CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_map_run<true>, kRunThreadsRL, dyn));
+    if (bps < 1) bps = 1;
+  }
+  dim3 grid((unsigned)(sm_count() * bps)), block(orig ? kRunThreadsRL : kRunThreads);
   void* args[] = {&a};
   CYC_CUDA(cudaEventRecord(e0, s));
-  coop_launch((const void*)k_map_run, grid, block, args, 0, s);
+  coop_launch(orig ? (const void*)k_map_run<true> : (const void*)k_map_run<false>, grid, block, args, dyn, s);
   CYC_LAUNCHED();
   CYC_CUDA(cudaEventRecord(e1, s));
   RunCtl host;
@@ -1379,7 +1711,11 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early
 
 void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream_t s) {
   if (!n) return;
-  k_strip<<<grid_for(n, 256, 8), 256, 0, s>>>(ws.P[cur].as<uint32_t>(), n, dst);
+  if (ws.orig) {
+    k_strip_perm<<<grid_for(n, 256, 8), 256, 0, s>>>(ws.P[cur].as<uint32_t>(), ws.orig, n, dst);
+  } else {
+    k_strip<<<grid_for(n, 256, 8), 256, 0, s>>>(ws.P[cur].as<uint32_t>(), n, dst);
+  }
   CYC_LAUNCHED();
 }
 

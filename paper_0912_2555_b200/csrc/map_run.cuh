@@ -49,6 +49,12 @@ struct RunArgs {
   const uint32_t* ell;   // HYB slab of the gather index (column-major, ell_k wide)
   const uint32_t* ovf;   // bit v: gather row v is longer than ell_k (or heavy)
   uint32_t ell_k;
+  const uint4* sdesc;    // sliced ELL of a degree-ordered plan: {off/32, width, heavy rows mask, 0} per 32 rows
+  const uint32_t* sell;  //   (null: HYB slab above)
+  const uint32_t* hcol;  // heavy rows of a plan as padded 128-column chunks (null: `heavy` below)
+  const uint32_t* hrow;  //   row of each chunk
+  uint32_t n_hchunks;
+  uint32_t hot_k;        // positions [0, hot_k) whose frontier bits pull steps stage in shared memory
   uint32_t n_pad;        // rows padded to kRowPad; P[n_pad] is the NIL sentinel slot
   const uint4* heavy;    // gather rows longer than heavy_deg, split into chunks
   uint32_t n_heavy, heavy_deg;
@@ -60,6 +66,8 @@ struct RunArgs {
   uint32_t* C[2];                  // self-witness candidates
   uint32_t* F;                     // accepting set, u32 words (demoted in place)
   uint32_t* used;                  // scratch bitmap, zero between iterations
+  const uint32_t* orig;            // storage position -> vertex id (null: identity layout, plan.cuh)
+  const uint32_t* perm;            // vertex id -> storage position (null: identity)
   uint32_t nwords, nwords_pad;     // FB words for n and for the padded rows
   uint32_t chunk_cap;
   RunCtl* ctl;
@@ -79,6 +87,8 @@ struct RunWs {
   uint32_t wl_cap = 0;
   uint32_t chunk_cap = 0;
   uint32_t trace_len = 0;
+  const uint32_t* orig = nullptr;  // layout of the last run (plan.cuh); strip_codes maps back
+  const uint32_t* bigm_src = nullptr;  // push offsets bigm was computed from
   void ensure(uint32_t n, uint32_t m, const uint32_t* poff, cudaStream_t s);
 };
 
@@ -89,12 +99,16 @@ struct RunOut {
 };
 
 // Runs the device-resident MAP loop. F must already hold the accepting words.
-void launch_map_run(const DevCsr& snap, const DevCsr& gath, RunWs& ws, int early_exit, int mode,
+// snap/gath are in storage order; orig/perm describe it (null: identity).
+void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig, const uint32_t* perm,
+                    const uint4* sdesc, const uint32_t* sell, const uint32_t* hcol, const uint32_t* hrow,
+                    uint32_t n_hchunks, RunWs& ws, int early_exit, int mode,
                     unsigned long long max_iterations, unsigned long long max_steps,
                     uint32_t alpha, unsigned long long cap, uint32_t trace_cap, cudaStream_t s,
                     cudaEvent_t e0, cudaEvent_t e1, RunOut& out);
 
-// Writes the codes (flag bit stripped) of workspace buffer `cur` into dst.
+// Writes the codes (flag bit stripped) of workspace buffer `cur` into dst,
+// in vertex-id order (ws.orig set: dst[orig[p]] = code of position p).
 void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream_t s);
 
 // Dense single Jacobi step (MaxPropagation::step) on plain codes.
