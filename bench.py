@@ -1,18 +1,27 @@
 #!/usr/bin/env python3
 """MAP propagation GTEPS and time-to-verdict on B200 (BASELINE.json metric).
 
-Workload (N=1 headline): config 2 of BASELINE.json — the 2^22-vertex layered
-DAG of SCCs (L=64 layers, W=4096 rings of S=16 per layer, accepting
-connectors; include/cyc_gen.h) run through run_map with early_exit, no SCC
-restriction (restriction keeps 0 vertices on this family). It
-forces L+1 = 65 MAP iterations and (L+1)^2 = 4225 propagation steps.
+Workload (N=1 headline): BASELINE config 3 — R-MAT (Graph500 .57/.19/.19)
+scale 26, edgefactor 16 (2^30 logged edges, 1.06 G snapshot edges after
+dedup), 1 % accepting, seeded vertex permutation (include/cyc_gen.h),
+transposed snapshot, no restriction:
 
-One bench "step" = one full run_map to verdict over the device-resident
-snapshot (value) / one cyc_check call from a pinned host edge log through
-H2D + CSR build + run_map (e2e). GTEPS = m x kernel_calls / time.
+* value (steady state): run_map with early_exit off on the device-resident
+  snapshot — the reference's `MaxPropagation::step` loop to fixpoint
+  (map_engine.cpp:94-121, 8 Jacobi steps on this graph). One bench step = one
+  run_map; GTEPS = m x kernel_calls / device time of the loop kernel.
+* e2e: the same metric through the C ABI from a pinned HOST edge log
+  (cyc_check: H2D + both CSRs + storage plan + run_map + stats D2H).
+* time_to_verdict_ms: early_exit on (the `cycheck graph` default), device-
+  resident and from host memory, plus the first (cold) call of the process.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
   N>1 under torchrun: independent replicas.
+
+The reference arm (--impl reference) never loads the engine: it times the
+reference's own MaxPropagation::step with WorkerPool(nproc) on the same graph
+(built for it by a parallel setup builder equal to build_snapshot) and prints
+the same metric/config; see run_reference_arm.
 """
 from __future__ import annotations
 
@@ -31,6 +40,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "MAP propagation GTEPS and time-to-verdict at 1/2/4/8 B200 vs CPU ref"
 L2_FLUSH_BYTES = 512 << 20
+REF_TTV_FILE = os.path.join(ROOT, "profiles", "r02_ref_ttv_c3.json")
 
 
 def dist_env():
@@ -79,6 +89,16 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -133,15 +153,38 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def make_params(eng, args):
-    p = eng.preset(args.config)
+def gen_params(args, reference: bool = False):
+    """Generator parameters of include/cyc_gen.h: the engine's presets for the
+    B200 arm, the oracle's own mirror for the reference arm (which must never
+    load the engine library). Both come from the same header."""
+    if reference:
+        import oracle
+
+        src = oracle.Restatement()
+    else:
+        import paper_0912_2555_b200 as src
+    p = src.preset(args.config)
     for k in ("L", "W", "S", "scale", "edgefactor"):
         v = getattr(args, k, None)
         if v:
             setattr(p, k, v)
-    if args.n_override:
-        p.n = args.n_override
-    return eng.prepare(p)
+    return src.prepare(p)
+
+
+WORKLOADS = {
+    1: "config1: uniform random digraph 2^16 x 4, 5% accepting",
+    2: "config2: layered DAG of SCCs 2^22 (L=64 W=4096 S=16), accepting connectors",
+    3: "config3: R-MAT scale 26 edgefactor 16 (a,b,c=.57,.19,.19), 1% accepting",
+    4: "config4: product graph 2^13 x 2^13 torus x 4-state Buchi, 2^28 states",
+    5: "config5: chain of SCCs 2^24 (L=64 W=512 S=512), sink accepting",
+}
+
+
+def bench_config(args, p):
+    """The `config` dict, identical in both arms (a function of the arguments only)."""
+    return {"workload": WORKLOADS.get(args.config, f"config{args.config}"), "n": int(p.n), "m_log": int(p.m),
+            "orientation": "transposed", "early_exit": False, "scc_restriction": False,
+            "step": "one run_map to fixpoint (MaxPropagation::step loop)", "gteps": "m x kernel_calls / time"}
 
 
 def load_traffic():
@@ -155,69 +198,94 @@ def load_traffic():
         return None, None
 
 
+def recorded_ref_ttv():
+    try:
+        with open(REF_TTV_FILE) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------- reference arm
 _REF_SNAP = {}
 
 
 def cpu_reference_sample(params, seconds: float, workers: int):
-    """Times the reference's own MaxPropagation::step (WorkerPool of `workers`
-    threads) on the same seeded graph: first Jacobi steps of MAP iteration 1,
-    bounded to `seconds`. Returns (gteps, steps, step_seconds, m, info)."""
+    """The reference's own MaxPropagation (gather-index build, map_engine.cpp:
+    9-19, then Jacobi steps from all-NIL, map_engine.cpp:21-79) with a
+    WorkerPool of `workers` threads on the same seeded graph, bounded to
+    `seconds` of steps. The CsrSnapshot it runs on comes from the parallel
+    setup builder (oracle ref_snapshot_gen_fast, equal to build_snapshot by
+    tests/test_oracle.py) — setup, not timed. Returns (gteps, steps, step_s, m, info)."""
     import oracle
 
     key = bytes(params)
     if key not in _REF_SNAP:
         ref = oracle.Reference()
         t0 = time.perf_counter()
-        _REF_SNAP[key] = (ref.snapshot_gen(params, True), time.perf_counter() - t0)
+        _REF_SNAP[key] = (ref.snapshot_gen_fast(params, True), time.perf_counter() - t0)
     snap, t_snap = _REF_SNAP[key]
     gather_s, steps_s, k = snap.time_steps(workers, 1 << 40, seconds)
     gteps = snap.m * k / steps_s / 1e9 if steps_s > 0 else 0.0
     return gteps, k, steps_s, snap.m, {"gather_build_s": round(gather_s, 3),
-                                       "log_fill_plus_build_snapshot_s": round(t_snap, 3)}
+                                       "setup_snapshot_s": round(t_snap, 3)}
+
+
+def ref_ttv_summary(args):
+    """CPU time to verdict (early exit) of the reference, phase by phase
+    (cycheck_main.cpp:88-97: csr = build_snapshot, kernel = run_map incl. its
+    gather-index build) at W=1 and W=nproc. A full config-3 run takes ~10
+    minutes of host time, too long for every bench call, so it is RECORDED by
+    scripts/ref_ttv.py on a GPU box host (same oracle/_ref build) and quoted
+    from profiles/r02_ref_ttv_c3.json; None for other configs."""
+    rec = recorded_ref_ttv()
+    if not rec or rec.get("config") != args.config:
+        return None
+    return {"recorded": os.path.relpath(REF_TTV_FILE, ROOT), "cpu_model": rec.get("cpu_model"),
+            "nproc": rec.get("nproc"), "build_snapshot_s": rec.get("build_snapshot_s"),
+            "log_fill_s": rec.get("log_fill_s"), "run_map_s_by_workers": rec.get("run_map_s"),
+            "ttv_s_by_workers": {w: round(rec["build_snapshot_s"] + t, 3) for w, t in rec["run_map_s"].items()},
+            "verdict_by_workers": rec.get("stats")}
 
 
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    import paper_0912_2555_b200 as eng
-
-    params = make_params(eng, args)
     import oracle
 
+    params = gen_params(args, reference=True)
     workers = os.cpu_count() or 1
     vals = []
     info = None
     m = 0
-    # each bench step is one bounded sample of propagation steps
     for i in range(args.warmup + args.steps):
         g, k, secs, m, info = cpu_reference_sample(params, args.ref_seconds, workers)
         if i >= args.warmup:
             vals.append((g, k, secs))
     gteps = statistics.median(v[0] for v in vals)
-    sample = (f"config {args.config}: first {vals[0][1]} Jacobi steps of MAP iteration 1 "
-              f"(MaxPropagation::step, WorkerPool({workers})) per step, ~{args.ref_seconds}s each")
+    sample = (f"{WORKLOADS.get(args.config)}: reference MaxPropagation::step with WorkerPool({workers}), "
+              f"Jacobi steps of the first fixpoint from all-NIL (restarted at the fixpoint), "
+              f"~{args.ref_seconds}s per bench step ({vals[0][1]} steps)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gteps, 5), "unit": "GTEPS",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000 * statistics.median(v[2] for v in vals), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded include/cyc_gen.h)",
-        "config": {"workload": f"config{args.config}", "n": int(params.n), "m_log": int(params.m),
-                   "m": int(m), "parallelism": "cpu-threads"},
-        "cpu_baseline": {"value": round(gteps, 5), "unit": "GTEPS", "cores": workers,
-                         "kind": "reference", "sample": sample, **(info or {})},
-        "e2e": {"value": round(gteps, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "config": bench_config(args, params),
+        "cpu_baseline": {"value": round(gteps, 5), "unit": "GTEPS", "cores": workers, "kind": "reference",
+                         "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count(), **(info or {}),
+                         "time_to_verdict": ref_ttv_summary(args)},
+        "e2e": {"value": round(gteps, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    # the reference arm must not have mapped the engine library
+    assert "paper_0912_2555_b200" not in sys.modules
     print(json.dumps(line))
     return 0
 
 
 # ----------------------------------------------------------------- B200 arm
 def run_b200(args, rank, world, local):
-    import numpy as np
-
     import paper_0912_2555_b200 as eng
     from paper_0912_2555_b200 import _abi
 
@@ -229,44 +297,58 @@ def run_b200(args, rank, world, local):
         device = torch.device("cuda", local)
     ctx = eng.Context(local)
     L = _abi.lib()
-    params = make_params(eng, args)
+    params = gen_params(args)
     n, m_log = int(params.n), int(params.m)
-    # device-resident input (value) and pinned host input (e2e)
+    nw64 = (n + 63) // 64
+    # device-resident input (value, TTV) and a pinned host copy (e2e)
     d_edges, d_acc = C.c_void_p(), C.c_void_p()
     _abi.check(L.cyc_device_alloc(ctx.handle, m_log * 8, C.byref(d_edges)))
-    _abi.check(L.cyc_device_alloc(ctx.handle, ((n + 63) // 64) * 8, C.byref(d_acc)))
+    _abi.check(L.cyc_device_alloc(ctx.handle, nw64 * 8, C.byref(d_acc)))
     _abi.check(L.cyc_gen_fill(ctx.handle, C.byref(params), d_edges, d_acc))
     h_edges, h_acc = C.c_void_p(), C.c_void_p()
     _abi.check(L.cyc_host_alloc(m_log * 8, C.byref(h_edges)))
-    _abi.check(L.cyc_host_alloc(((n + 63) // 64) * 8, C.byref(h_acc)))
+    _abi.check(L.cyc_host_alloc(nw64 * 8, C.byref(h_acc)))
     _abi.check(L.cyc_memcpy(ctx.handle, h_edges, d_edges, m_log * 8))
-    _abi.check(L.cyc_memcpy(ctx.handle, h_acc, d_acc, ((n + 63) // 64) * 8))
-
+    _abi.check(L.cyc_memcpy(ctx.handle, h_acc, d_acc, nw64 * 8))
+    _abi.check(L.cyc_ctx_synchronize(ctx.handle))
+    u32p, u64p = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
     orient = _abi.CYC_TRANSPOSED
+    ttv_opt = eng.MapOptions(early_exit=True, mode=args.mode).to_c()
+    full_opt = eng.MapOptions(early_exit=False, mode=args.mode).to_c()
+
+    def check_call(edges, acc, opt):
+        st, ms = _abi.MapStatsC(), (C.c_double * 4)()
+        _abi.check(L.cyc_flush_l2(ctx.handle, L2_FLUSH_BYTES))
+        _abi.check(L.cyc_ctx_synchronize(ctx.handle))
+        t0 = time.perf_counter()
+        _abi.check(L.cyc_check(ctx.handle, C.cast(edges, u32p), m_log, n, C.cast(acc, u64p), orient, 0,
+                               C.byref(opt), C.byref(st), ms))
+        return (time.perf_counter() - t0) * 1e3, list(ms), st
+
+    # the first call of the process: first touch of the pools (cold TTV)
+    cold_ms, cold_phases, cold_st = check_call(h_edges, h_acc, ttv_opt)
+
     g = C.c_void_p()
-    t0 = time.perf_counter()
-    _abi.check(L.cyc_graph_build(ctx.handle, C.cast(d_edges, C.POINTER(C.c_uint32)), m_log, n,
-                                 C.cast(d_acc, C.POINTER(C.c_uint64)), orient, C.byref(g)))
-    build_ms_first = (time.perf_counter() - t0) * 1e3
+    _abi.check(L.cyc_graph_build(ctx.handle, C.cast(d_edges, u32p), m_log, n, C.cast(d_acc, u64p), orient,
+                                 C.byref(g)))
     snap = eng.CsrSnapshot(g, ctx)
     m = snap.m
-    opt = eng.MapOptions(early_exit=True, mode=args.mode).to_c()
     st = _abi.MapStatsC()
 
     def one_run():
         _abi.check(L.cyc_flush_l2(ctx.handle, L2_FLUSH_BYTES))
-        _abi.check(L.cyc_map_run(ctx.handle, g, None, C.byref(opt), C.byref(st), None, None, None, 0))
+        _abi.check(L.cyc_map_run(ctx.handle, g, None, C.byref(full_opt), C.byref(st), None, None, None, 0))
         return float(st.loop_ms)
 
+    one_run()  # builds the storage plan (cached on the snapshot)
+    plan_ms = float(st.plan_ms)
     for _ in range(args.warmup):
         one_run()
     barrier(dist, device)
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = eng.launch_count()
-    loop_ms = []
-    for _ in range(args.steps):
-        loop_ms.append(one_run())
+    loop_ms = [one_run() for _ in range(args.steps)]
     _abi.check(L.cyc_ctx_synchronize(ctx.handle))
     launches = eng.launch_count() - launches0
     barrier(dist, device)
@@ -276,76 +358,73 @@ def run_b200(args, rank, world, local):
     kernel_calls = int(stats.kernel_calls)
     value = world * m * kernel_calls / (ms_per_step * 1e-3) / 1e9
 
-    # device-resident time to verdict: CSR build from the resident log + run_map
-    ttv = []
-    for _ in range(max(1, min(args.steps, 5))):
-        _abi.check(L.cyc_flush_l2(ctx.handle, L2_FLUSH_BYTES))
-        _abi.check(L.cyc_ctx_synchronize(ctx.handle))
-        ms = (C.c_double * 4)()
-        s2 = _abi.MapStatsC()
-        _abi.check(L.cyc_check(ctx.handle, C.cast(d_edges, C.POINTER(C.c_uint32)), m_log, n,
-                               C.cast(d_acc, C.POINTER(C.c_uint64)), orient, 0, C.byref(opt),
-                               C.byref(s2), ms))
-        ttv.append(list(ms))
-    # e2e: pinned host log -> verdict through the C ABI (H2D inside)
-    e2e = []
-    for _ in range(max(1, min(args.steps, 5))):
-        _abi.check(L.cyc_flush_l2(ctx.handle, L2_FLUSH_BYTES))
-        _abi.check(L.cyc_ctx_synchronize(ctx.handle))
-        ms = (C.c_double * 4)()
-        s3 = _abi.MapStatsC()
-        t0 = time.perf_counter()
-        _abi.check(L.cyc_check(ctx.handle, C.cast(h_edges, C.POINTER(C.c_uint32)), m_log, n,
-                               C.cast(h_acc, C.POINTER(C.c_uint64)), orient, 0, C.byref(opt),
-                               C.byref(s3), ms))
-        e2e.append((time.perf_counter() - t0) * 1e3)
-        assert (s3.cycle_found, s3.kernel_calls) == (stats.cycle_found, stats.kernel_calls)
+    reps = max(1, min(args.steps, 5))
+    # time to verdict (early exit): device-resident log and pinned host log
+    ttv_dev = [check_call(d_edges, d_acc, ttv_opt) for _ in range(reps)]
+    ttv_host = [check_call(h_edges, h_acc, ttv_opt) for _ in range(reps)]
+    # e2e of the headline metric: host log -> steady-state verdict through the C ABI
+    e2e = [check_call(h_edges, h_acc, full_opt) for _ in range(reps)]
     clk = clocks.stop()
-    e2e_ms = max_over_ranks(dist, statistics.median(e2e), device)
-    ttv_ms = max_over_ranks(dist, statistics.median(t[3] for t in ttv), device)
+    for _, _, s3 in e2e:
+        assert (s3.cycle_found, s3.kernel_calls) == (stats.cycle_found, stats.kernel_calls)
+    e2e_ms = max_over_ranks(dist, statistics.median(x[0] for x in e2e), device)
     e2e_value = world * m * kernel_calls / (e2e_ms * 1e-3) / 1e9
+    ttv_st = ttv_dev[0][2]
 
     peak, peak_src = peaks()
     loop_s = statistics.median(loop_ms) * 1e-3
     achieved = stats.algorithmic_bytes / loop_s / 1e9 if loop_s > 0 else 0.0
     traffic, traffic_src = load_traffic()
+    med = lambda xs: round(statistics.median(xs), 3)  # noqa: E731
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded include/cyc_gen.h, generated on device)",
-        "config": {"workload": f"config{args.config}: layered DAG of SCCs, L={params.L} W={params.W} "
-                               f"S={params.S}" if args.config in (2, 5) else f"config{args.config}",
-                   "n": n, "m_log": m_log, "m": m, "orientation": "transposed",
-                   "early_exit": True, "scc_restriction": False, "mode": args.mode,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": f"flushed ({L2_FLUSH_BYTES >> 20} MiB write) before every timed step"},
-        "verdict": {"cycle_found": bool(stats.cycle_found), "iterations": int(stats.iterations),
-                    "kernel_calls": kernel_calls, "demoted_total": int(stats.demoted_total)},
-        "time_to_verdict_ms": {"device_resident": round(ttv_ms, 3), "e2e_host": round(e2e_ms, 3),
-                               "build_ms": round(statistics.median(t[0] for t in ttv), 3),
-                               "loop_ms": round(statistics.median(loop_ms), 3)},
+        "config": bench_config(args, params),
+        "setup": {"m": m, "mode": args.mode, "layout": "degree" if stats.layout == 2 else "identity",
+                  "parallelism": f"replicas{world}" if world > 1 else "single",
+                  "l2": f"flushed ({L2_FLUSH_BYTES >> 20} MiB write) before every timed call",
+                  "grid": [int(stats.grid_blocks), int(stats.block_threads)]},
+        "verdict": {"cycle_found": bool(stats.cycle_found), "witness": int(stats.witness),
+                    "iterations": int(stats.iterations), "kernel_calls": kernel_calls,
+                    "demoted_total": int(stats.demoted_total)},
+        "time_to_verdict_ms": {
+            "early_exit": True, "cycle_found": bool(ttv_st.cycle_found), "witness": int(ttv_st.witness),
+            "kernel_calls": int(ttv_st.kernel_calls),
+            "device_resident": med([x[0] for x in ttv_dev]),
+            "device_resident_phases": {"build": med([x[1][0] for x in ttv_dev]),
+                                       "plan_plus_loop": med([x[1][2] for x in ttv_dev])},
+            "e2e_host": med([x[0] for x in ttv_host]),
+            "cold_first_call_e2e_host": round(cold_ms, 3),
+            "steady_state_plan_build_ms": round(plan_ms, 3)},
         "steps_detail": {"pull_steps": int(stats.pull_steps), "push_steps": int(stats.push_steps),
-                         "edges_touched": int(stats.edges_touched), "rows_touched": int(stats.rows_touched),
-                         "grid": [int(stats.grid_blocks), int(stats.block_threads)]},
-        "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "h2d_bytes_per_step": m_log * 8 + ((n + 63) // 64) * 8,
-                "d2h_bytes_per_step": C.sizeof(_abi.MapStatsC)},
+                         "edges_touched": int(stats.edges_touched), "rows_touched": int(stats.rows_touched)},
+        "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "ms": round(e2e_ms, 3),
+                "h2d_bytes_per_step": m_log * 8 + nw64 * 8, "d2h_bytes_per_step": C.sizeof(_abi.MapStatsC),
+                "what": "cyc_check from a pinned host edge log: H2D + both CSRs + storage plan + run_map "
+                        "(early_exit off) + stats D2H"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "k_map_run (persistent, one launch per run_map)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": int(stats.algorithmic_bytes),
+                     "bytes_model": "sum over steps of 8*E_s + 12*V_s (pull: E=m, V=n; push: touched)",
                      "traffic": traffic, "traffic_source": traffic_src},
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            g_cpu, k, secs, m_ref, info = cpu_reference_sample(params, args.ref_seconds, os.cpu_count() or 1)
-            line["cpu_baseline"] = {"value": round(g_cpu, 5), "unit": "GTEPS", "cores": os.cpu_count(),
-                                    "kind": "reference",
-                                    "sample": f"first {k} Jacobi steps of MAP iteration 1 of the same "
-                                              f"graph, reference MaxPropagation::step with "
-                                              f"WorkerPool({os.cpu_count()}), {secs:.1f}s", **info}
+            workers = os.cpu_count() or 1
+            g_cpu, k, secs, m_ref, info = cpu_reference_sample(gen_params(args, reference=True), args.ref_seconds,
+                                                               workers)
+            assert m_ref == m
+            line["cpu_baseline"] = {
+                "value": round(g_cpu, 5), "unit": "GTEPS", "cores": workers, "kind": "reference",
+                "cpu_model": cpu_model(),
+                "sample": f"reference MaxPropagation::step, WorkerPool({workers}), {k} Jacobi steps of the "
+                          f"first fixpoint of the same graph in {secs:.1f}s", **info,
+                "time_to_verdict": ref_ttv_summary(args)}
         except Exception as ex:  # reference build missing on this box
             line["cpu_baseline"] = {"value": None, "unit": "GTEPS", "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {ex}"}
@@ -377,7 +456,7 @@ def run_b200_sharded(args, rank, world, local):
         os.environ.setdefault("MASTER_PORT", "29531")
         dist.init_process_group("nccl", rank=rank, world_size=world)
     ctx = eng.Context(local)
-    params = make_params(eng, args)
+    params = gen_params(args)
     n, m_log = int(params.n), int(params.m)
     e = np.zeros((m_log, 2), np.uint32)
     a = np.zeros((n + 63) // 64, np.uint64)
@@ -432,14 +511,13 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--mode", default="auto", choices=["auto", "pull", "push"])
     ap.add_argument("--L", type=int, default=0)
     ap.add_argument("--W", type=int, default=0)
     ap.add_argument("--S", type=int, default=0)
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--edgefactor", type=int, default=0)
-    ap.add_argument("--n-override", type=int, default=0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fused", action="store_true",

@@ -87,6 +87,9 @@ typedef struct cyc_map_stats {
   uint64_t algorithmic_bytes;  /* sum over steps of 8*E_s + 12*V_s */
   double loop_ms;              /* device time of the loop kernel(s), CUDA events */
   uint32_t grid_blocks, block_threads;
+  double plan_ms;              /* host time building the storage plan in this call (0: cached) */
+  int32_t layout;              /* CYC_LAYOUT_IDENTITY or CYC_LAYOUT_DEGREE: the layout that ran */
+  int32_t reserved;
 } cyc_map_stats;
 
 /* ---- context ------------------------------------------------------------ */

@@ -301,6 +301,8 @@ class Reference:
         L.ref_time_steps.argtypes = [_P, C.c_int, C.c_uint64, C.c_double, _P, C.POINTER(C.c_uint64)]
         L.ref_time_build.argtypes = [_P, C.c_int, C.POINTER(C.c_double)]
         L.ref_hw_threads.restype = C.c_int
+        L.ref_ttv.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P, C.c_int, _P, _P]
+        L.ref_snapshot_gen_fast.argtypes = [_P, C.c_int, C.c_int, C.POINTER(_P)]
 
     def _ok(self, rc: int) -> None:
         if rc != 0:
@@ -346,6 +348,14 @@ class Reference:
         self._ok(self.lib.ref_snapshot_gen(C.byref(params), int(transposed), C.byref(h)))
         return RefSnapshot(self, h)
 
+    def snapshot_gen_fast(self, params, transposed: bool = True, threads: int = 0) -> "RefSnapshot":
+        """SETUP ONLY: build_snapshot's result for a generated config, built
+        with `threads` host threads (ref_driver.cpp ref_snapshot_gen_fast)."""
+        h = _P()
+        self._ok(self.lib.ref_snapshot_gen_fast(C.byref(params), int(transposed), threads or (os.cpu_count() or 1),
+                                                C.byref(h)))
+        return RefSnapshot(self, h)
+
     def demote(self, x, acc):
         x = np.ascontiguousarray(np.asarray(x, np.uint32))
         n = len(x)
@@ -361,6 +371,19 @@ class Reference:
         s = C.c_double()
         self._ok(self.lib.ref_time_build(C.byref(params), int(transposed), C.byref(s)))
         return float(s.value)
+
+    def ttv(self, params, workers=(1,), transposed: bool = True, restrict: bool = False, early_exit: bool = True):
+        """CPU time to verdict, phase by phase (ref_driver.cpp ref_ttv): returns
+        {"log_fill_s", "build_snapshot_s", "restrict_s", "run_map_s": {w: s},
+        "stats": {w: (cycle, witness, iterations, kernel_calls, demoted)}}."""
+        w = np.asarray(list(workers), np.int32)
+        t = np.zeros(3 + len(w), np.float64)
+        st = np.zeros(5 * len(w), np.uint64)
+        self._ok(self.lib.ref_ttv(C.byref(params), int(transposed), int(restrict), int(early_exit),
+                                  w.ctypes.data, len(w), t.ctypes.data, st.ctypes.data))
+        return {"log_fill_s": float(t[0]), "build_snapshot_s": float(t[1]), "restrict_s": float(t[2]),
+                "run_map_s": {int(x): float(t[3 + i]) for i, x in enumerate(w)},
+                "stats": {int(x): tuple(int(v) for v in st[5 * i:5 * i + 5]) for i, x in enumerate(w)}}
 
     def hw_threads(self) -> int:
         return int(self.lib.ref_hw_threads())

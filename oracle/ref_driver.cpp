@@ -9,6 +9,7 @@
 // run_map does not return the map vector (map_engine.cpp:139-162), so
 // ref_run_map replays its loop with the public fixpoint()/demote() and checks
 // the replica's MapStats against run_map's own before reporting.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -384,5 +385,152 @@ int ref_time_build(const void* params, int transposed, double* seconds) {
 }
 
 int ref_hw_threads() { return (int)std::thread::hardware_concurrency(); }
+
+// SETUP ONLY (not timed, not the reference's code): the CsrSnapshot that
+// build_snapshot (graph.cpp:63-105) produces for a generated config, built
+// with `threads` threads so that the bench's CPU arm can time the reference's
+// own MaxPropagation on config 3 without first spending minutes in the
+// single-threaded reference build. Same content: rows keyed by dst
+// (transposed) or src, columns ascending and deduplicated, accepting frozen.
+// tests/test_oracle.py checks it against build_snapshot itself.
+int ref_snapshot_gen_fast(const void* params, int transposed, int threads, void** out) {
+  REF_TRY
+  const auto* p = static_cast<const cyc_gen_params*>(params);
+  if (p->kind == CYC_GEN_PRODUCT) return ref_snapshot_gen(params, transposed, out);
+  const uint32_t n = p->n;
+  const uint64_t m = p->m;
+  const int T = threads > 0 ? threads : 1;
+  auto par = [&](auto&& body) {  // body(thread index, begin, end) over [0, m)
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t] { body(t, m * t / T, m * (t + 1) / T); });
+    for (auto& x : th) x.join();
+  };
+  std::vector<std::vector<uint32_t>> cnt(T, std::vector<uint32_t>(n + 1, 0));
+  par([&](int t, uint64_t b, uint64_t e) {
+    for (uint64_t i = b; i < e; ++i) {
+      uint32_t sv, dv;
+      cyc_gen_edge(p, i, &sv, &dv);
+      ++cnt[t][transposed ? dv : sv];
+    }
+  });
+  // raw offsets: row-major, thread-minor (each thread's slice of a row contiguous)
+  std::vector<uint64_t> roff(n + 1, 0);
+  {
+    uint64_t acc = 0;
+    for (uint32_t v = 0; v < n; ++v) {
+      roff[v] = acc;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t c = cnt[t][v];
+        cnt[t][v] = (uint32_t)acc;  // becomes the thread's cursor (relative base fits: see below)
+        acc += c;
+      }
+    }
+    roff[n] = acc;
+  }
+  std::vector<uint32_t> raw(m ? m : 1);
+  // cursors may exceed 2^32 for m >= 2^32; the device limit is m < 2^32 anyway
+  par([&](int t, uint64_t b, uint64_t e) {
+    for (uint64_t i = b; i < e; ++i) {
+      uint32_t sv, dv;
+      cyc_gen_edge(p, i, &sv, &dv);
+      const uint32_t r = transposed ? dv : sv;
+      raw[cnt[t][r]++] = transposed ? sv : dv;
+    }
+  });
+  cnt.clear();
+  cnt.shrink_to_fit();
+  std::vector<uint32_t> ucnt(n, 0);
+  {  // sort + dedup each row in place, rows split over threads
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t] {
+        for (uint64_t v = t; v < n; v += T) {
+          uint32_t* b = raw.data() + roff[v];
+          uint32_t* e = raw.data() + roff[v + 1];
+          std::sort(b, e);
+          ucnt[v] = (uint32_t)(std::unique(b, e) - b);
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  auto* s = new Snap;
+  CsrSnapshot& sn = s->snap;
+  sn.orientation = transposed ? Orientation::transposed : Orientation::forward;
+  sn.n = n;
+  sn.row_offsets.assign(n + 1ull, 0);
+  for (uint32_t v = 0; v < n; ++v) sn.row_offsets[v + 1] = sn.row_offsets[v] + ucnt[v];
+  sn.m = sn.row_offsets[n];
+  sn.col_indices.resize(sn.m);
+  {
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t] {
+        for (uint64_t v = t; v < n; v += T)
+          std::copy(raw.data() + roff[v], raw.data() + roff[v] + ucnt[v], sn.col_indices.data() + sn.row_offsets[v]);
+      });
+    for (auto& x : th) x.join();
+  }
+  sn.accepting = Bitset(n);
+  for (uint32_t v = 0; v < n; ++v)
+    if (cyc_gen_accepting(p, v)) sn.accepting.set(v);
+  *out = s;
+  return 0;
+  REF_CATCH
+}
+
+// CPU time to verdict of the reference, phase by phase, the way
+// cycheck_main.cpp:88-97 splits it (csr_ms = build_snapshot, kernel_ms =
+// run_map) and explore.cpp:93-101 adds the final-round restriction:
+//   t[0] log fill (EdgeLog::append_edge for every generated edge, not the
+//        reference's work but its input), t[1] build_snapshot,
+//   t[2] restrict_to_accepting_sccs (0 if restrict_ == 0),
+//   t[3 + i] run_map with MapOptions{workers[i], early_exit} (includes the
+//        MaxPropagation gather-index build, map_engine.cpp:144).
+// stats[5 i ..] = {cycle, witness (in the log's ids), iterations, kernel_calls,
+// demoted_total} of run i.
+int ref_ttv(const void* params, int transposed, int restrict_, int early, const int* workers, int nw,
+            double* t, uint64_t* stats) {
+  REF_TRY
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  const auto* p = static_cast<const cyc_gen_params*>(params);
+  EdgeLog::Limits lim;
+  lim.max_vertices = p->n > 0 ? p->n : 1;
+  lim.max_edges = p->m > 0 ? p->m : 1;
+  auto t0 = clk::now();
+  EdgeLog log(lim);
+  fill_log(p, log);
+  auto t1 = clk::now();
+  CsrSnapshot snap = build_snapshot(log, transposed ? Orientation::transposed : Orientation::forward);
+  auto t2 = clk::now();
+  t[0] = secs(t0, t1);
+  t[1] = secs(t1, t2);
+  t[2] = 0;
+  SccRestriction r;
+  const CsrSnapshot* run_on = &snap;
+  if (restrict_) {
+    auto t3 = clk::now();
+    r = restrict_to_accepting_sccs(snap);
+    t[2] = secs(t3, clk::now());
+    run_on = &r.snapshot;
+  }
+  for (int i = 0; i < nw; ++i) {
+    MapOptions o;
+    o.workers = workers[i];
+    o.early_exit = early != 0;
+    auto t4 = clk::now();
+    auto [verdict, st] = run_map(*run_on, run_on->accepting, o);
+    t[3 + i] = secs(t4, clk::now());
+    uint64_t* out = stats + 5 * i;
+    out[0] = verdict.cycle_found();
+    out[1] = verdict.witness ? (restrict_ ? r.kept[*verdict.witness] : *verdict.witness) : 0xFFFFFFFFull;
+    out[2] = st.iterations;
+    out[3] = st.kernel_calls;
+    out[4] = st.demoted_total;
+  }
+  return 0;
+  REF_CATCH
+}
 
 }  // extern "C"

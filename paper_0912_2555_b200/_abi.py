@@ -86,6 +86,9 @@ class MapStatsC(C.Structure):
         ("loop_ms", C.c_double),
         ("grid_blocks", C.c_uint32),
         ("block_threads", C.c_uint32),
+        ("plan_ms", C.c_double),
+        ("layout", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

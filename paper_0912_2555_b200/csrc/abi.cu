@@ -357,7 +357,7 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   g->orientation = orientation;
   g->m_log = m_log;
   const int snap_key_dst = orientation == CYC_TRANSPOSED;
-  if (m_log >= kOverlapEdges) {
+  if (m_log >= kOverlapEdges && !std::getenv("CYC_BUILD_SEQUENTIAL")) {
     // the two CSRs are independent given the log: the gather index is built
     // on a second stream by a helper thread (every phase has host syncs, so
     // one thread cannot keep both streams busy), overlapping the snapshot
@@ -385,9 +385,17 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
       main_err = std::current_exception();
     }
     helper.join();
-    if (main_err) std::rethrow_exception(main_err);
-    if (helper_err) std::rethrow_exception(helper_err);
+    if (main_err || helper_err) {
+      // nothing queued on s2 may outlive the staged log and err (allocated on s)
+      cudaStreamSynchronize(ctx->s2);
+      std::rethrow_exception(main_err ? main_err : helper_err);
+    }
     CYC_CUDA(cudaStreamWaitEvent(s, ctx->ev_out, 0));
+    // the gather CSR was allocated on s2; release it on s, after everything
+    // that reads it (DevBuf frees on its stream, and the block cache reuses
+    // blocks in that stream's order)
+    g->gath.off.s = s;
+    g->gath.col.s = s;
   } else {
     cyc::build_csr(de, m_log, n, snap_key_dst, s, g->snap, err.as<uint32_t>(), ctx->arena);
     cyc::build_csr(de, m_log, n, !snap_key_dst, s, g->gath, err.as<uint32_t>(), ctx->arena);
@@ -427,6 +435,8 @@ void fill_stats(const cyc::RunOut& o, cyc_map_stats* st) {
   st->loop_ms = o.ms;
   st->grid_blocks = o.grid;
   st->block_threads = o.block;
+  st->plan_ms = o.plan_ms;
+  st->layout = o.layout;
 }
 
 cyc_map_options default_opts() {
@@ -443,7 +453,10 @@ cyc::RunOut run_loop(cyc_ctx* ctx, cyc_graph* g, const uint64_t* acc_words,
   const uint32_t n = g->n();
   require(o.mode >= CYC_MODE_AUTO && o.mode <= CYC_MODE_PUSH, CYC_E_CONTRACT, "bad mode");
   require(o.layout >= CYC_LAYOUT_AUTO && o.layout <= CYC_LAYOUT_DEGREE, CYC_E_CONTRACT, "bad layout");
-  cyc::build_plan(g->snap, g->gath, o.layout, g->plan, s);
+  const auto tp = std::chrono::steady_clock::now();
+  const bool planned = cyc::build_plan(g->snap, g->gath, o.layout, g->plan, s);
+  const double plan_ms =
+      planned ? std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp).count() : 0.0;
   const bool rl = g->plan.relabel;
   const cyc::DevCsr& snap = rl ? g->plan.snap : g->snap;
   const cyc::DevCsr& gath = rl ? g->plan.gath : g->gath;
@@ -465,6 +478,8 @@ cyc::RunOut run_loop(cyc_ctx* ctx, cyc_graph* g, const uint64_t* acc_words,
   }
   if (rl) cyc::permute_bits(reinterpret_cast<const uint32_t*>(F), orig, n, g->ws.F.as<uint32_t>(), s);
   cyc::RunOut out;
+  out.plan_ms = plan_ms;
+  out.layout = rl ? CYC_LAYOUT_DEGREE : CYC_LAYOUT_IDENTITY;
   cyc::launch_map_run(snap, gath, orig, perm, rl ? g->plan.sdesc.as<uint4>() : nullptr,
                       rl ? g->plan.sell.as<uint32_t>() : nullptr, rl ? g->plan.hcol.as<uint32_t>() : nullptr,
                       rl ? g->plan.hrow.as<uint32_t>() : nullptr, rl ? g->plan.n_hchunks : 0u, g->ws, o.early_exit != 0, o.mode, o.max_iterations,

@@ -87,7 +87,9 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
 extern __shared__ uint32_t hot_sh[];
 
 struct Hot {
-  uint32_t k;  // positions with staged frontier bits (0: no filter)
+  uint32_t k;     // positions with staged frontier bits (0: no filter)
+  uint32_t vmax;  // the largest value of this fixpoint (max id+1 over F): a row
+                  // already holding it cannot rise, its gathers are skipped
 };
 
 __device__ __forceinline__ uint32_t ld_word(const Hot& h, const uint32_t* __restrict__ P, uint32_t u) {
@@ -129,6 +131,14 @@ template <bool RL>
 __device__ __forceinline__ uint32_t oid(const RunArgs& a, uint32_t p) {
   if constexpr (RL) return __ldg(a.orig + p);
   return p;
+}
+
+// A self-witness candidate (raised to exactly id+1): appended while the
+// list has room; a step whose candidates overflow it (a vertex can be raised to
+// id+1 by several sources) is confirmed by a dense scan instead.
+__device__ __forceinline__ void add_cand(const RunArgs& a, uint32_t* Cn, unsigned int* cnt, uint32_t v) {
+  const uint32_t pos = atomicAdd(cnt, 1u);
+  if (pos < a.cand_cap) Cn[pos] = v;
 }
 
 // candidate value the vertex at position u with map word w contributes to its
@@ -375,7 +385,7 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
     acc.first += first[r];
     acc.fedges += e[r] - b[r];
     if ((bw[r] >> (tgt[r] & 31u)) & 1u) acc.fedges += enlist(a, tgt[r], c.bc, c.nchunk, c.sh);
-    if (go[r] && (old[r] & kFlag) && val[r] == oid<RL>(a, tgt[r]) + 1u) c.Cn[atomicAdd(c.ccnt, 1u)] = tgt[r];
+    if (go[r] && (old[r] & kFlag) && val[r] == oid<RL>(a, tgt[r]) + 1u) add_cand(a, c.Cn, c.ccnt, tgt[r]);
   }
 }
 
@@ -516,13 +526,16 @@ __device__ __forceinline__ void pull_sell(const RunArgs& a, const uint32_t* __re
       wmax = max(wmax, d[k].y);
       skip |= ((d[k].z >> lane) & 1u) << k;
     }
+    uint32_t wlim[R];  // a saturated row reads no columns at all
+#pragma unroll
+    for (int k = 0; k < R; ++k) wlim[k] = best[k] == hot.vmax ? 0u : d[k].y;
     for (uint32_t j = 0; j < wmax; j += J) {
       uint32_t u[R][J], w[R][J];
 #pragma unroll
       for (int k = 0; k < R; ++k)
 #pragma unroll
         for (int t = 0; t < J; ++t)
-          u[k][t] = j + t < d[k].y ? ld_stream(a.sell + ((size_t)d[k].x + j + t) * 32u + lane) : np;
+          u[k][t] = j + t < wlim[k] ? ld_stream(a.sell + ((size_t)d[k].x + j + t) * 32u + lane) : np;
 #pragma unroll
       for (int k = 0; k < R; ++k)
 #pragma unroll
@@ -622,7 +635,7 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
           ++acc.first;
           if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
         }
-        if ((own & kFlag) && mine == oid<RL>(a, v) + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = v;
+        if ((own & kFlag) && mine == oid<RL>(a, v) + 1u) add_cand(a, Cn, &sl->cand_cnt, v);
       }
     }
   }
@@ -645,7 +658,7 @@ __device__ __forceinline__ void heavy_flush(const RunArgs& a, bool live, uint32_
       ++acc.first;
       if (bit_of(a.bigm, pv)) acc.fedges += enlist(a, pv, bc, &sl->nchunk, sh);
     }
-    if ((po & kFlag) && mine == oid<RL>(a, pv) + 1u) Cn[atomicAdd(&sl->cand_cnt, 1u)] = pv;
+    if ((po & kFlag) && mine == oid<RL>(a, pv) + 1u) add_cand(a, Cn, &sl->cand_cnt, pv);
   }
 }
 
@@ -681,6 +694,11 @@ __device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t
   uint32_t pv = 0, pm = 0, po = 0, npend = 0;     // finished rows awaiting write-back
   for (uint32_t c = cb; c < ce; c += B) {
     uint32_t w[B][H];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      if ((ro[k] & kCode) == hot.vmax)  // saturated row: its chunk cannot raise it
+#pragma unroll
+        for (int r = 0; r < H; ++r) u[k][r] = np;
 #pragma unroll
     for (int k = 0; k < B; ++k)
 #pragma unroll
@@ -750,7 +768,8 @@ __device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t
 }
 
 template <bool RL>
-__device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, unsigned long long tk) {
+__device__ void pull_step(const RunArgs& a, uint32_t g, int cur, uint32_t vmax, BlockSh* sh,
+                          unsigned long long tk) {
   const uint32_t* __restrict__ P = a.P[cur];
   uint32_t* __restrict__ Q = a.P[cur ^ 1];
   SlotCtl* sl = &a.ctl->slot[g % 3u];
@@ -762,7 +781,7 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   StepAcc acc;
-  Hot hot{0u};
+  Hot hot{0u, vmax};
   if (RL && a.hot_k) {  // stage the previous step's frontier bits of the hottest positions
     for (uint32_t i = threadIdx.x; i < a.hot_k / 32u; i += blockDim.x) hot_sh[i] = __ldcg(fp + i);
     // rows_epilogue clears fp words as it goes: every CTA stages first
@@ -967,7 +986,8 @@ __device__ void demote_pass(const RunArgs& a, unsigned int* dcount, unsigned lon
 // Start of a fixpoint (setup tag g): both map buffers all-NIL with the
 // accepting bit; the initial frontier is the accepting set itself (every
 // accepting u offers cand = u+1), FB[(g+1)&1] cleared.
-__device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
+template <bool RL>
+__device__ void reset_pass(const RunArgs& a, uint32_t g, uint64_t t, BlockSh* sh) {
   uint32_t* fb = a.FB[g & 1u];
   uint32_t* fz = a.FB[(g + 1u) & 1u];
   SlotCtl* sl = &a.ctl->slot[g % 3u];
@@ -976,6 +996,7 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   unsigned long long fe = 0;
+  uint32_t vm = 0;  // max id+1 over F: no map value of this fixpoint can exceed it
   // 32 words (1024 vertices) per warp iteration
   for (uint32_t s = gw; s * 32u < a.nwords_pad; s += nw) {
     const uint32_t wi = s * 32u + lane;
@@ -994,6 +1015,7 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
         a.P[0][v] = val;
         a.P[1][v] = val;
         if (accv) {
+          vm = max(vm, oid<RL>(a, v) + 1u);
           if (bit_of(a.bigm, v)) {
             fe += enlist(a, v, bc, &sl->nchunk, sh);
           } else {
@@ -1005,7 +1027,10 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, BlockSh* sh) {
   }
   const unsigned long long bigdeg = big_flush(a, sh, bc, &sl->nchunk);
   fe = block_sum(fe, sh) + bigdeg;
+  vm = ~block_min(~vm, sh);
   if (threadIdx.x == 0 && fe) atomicAdd(&sl->fedges, fe);
+  if (threadIdx.x == 0 && vm) atomicMax(&a.ctl->it_vmax[t & 1u], vm);
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->it_vmax[(t + 1u) & 1u] = 0u;  // the next fixpoint's
   wl_flush(sh, sl, a.WL[g & 1u], a.wl_cap);
 }
 
@@ -1048,9 +1073,10 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
   // initial F count and first fixpoint setup (tag g)
   demote_pass(a, nullptr, &ctl->it_fsize[0], &sh);
   if (lead) reset_slot(ctl, (g + 1u) % 3u);
-  reset_pass(a, g, &sh);
+  reset_pass<RL>(a, g, 0, &sh);
   grid.sync();
   uint64_t t = 0;
+  uint32_t vmax = __ldcg(&ctl->it_vmax[0]);
   bool truncated = false;
   if (__ldca(&ctl->it_fsize[0]) != 0) {
     for (;;) {
@@ -1090,7 +1116,7 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
           CYC_STAT(kResRows, a.n);
           CYC_STAT(kResBytes, 8ull * a.m + 12ull * a.n + 4ull);
           CYC_STAT(kResPullSteps, 1);
-          pull_step<RL>(a, g, cur, &sh, a.trace ? tkk : ~0ull);
+          pull_step<RL>(a, g, cur, vmax, &sh, a.trace ? tkk : ~0ull);
         }
         grid.sync();
         cur ^= 1;
@@ -1111,7 +1137,16 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
           const uint32_t* Cn = a.C[g & 1u];
           const uint32_t* Pn = a.P[cur];
           uint32_t mine = kNone;
-          for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+          if (nc > a.cand_cap) {  // list overflowed: every position of the new buffer (rare)
+            for (uint32_t v = threadIdx.x; v < a.n; v += blockDim.x) {
+              const uint32_t x = __ldcg(Pn + v);
+              if (x & kFlag) {
+                const uint32_t id = oid<RL>(a, v);
+                if ((x & kCode) == id + 1u) mine = min(mine, id);
+              }
+            }
+          }
+          for (uint32_t i = threadIdx.x; i < min(nc, a.cand_cap); i += blockDim.x) {
             const uint32_t c = __ldcg(Cn + i);
             const uint32_t id = oid<RL>(a, c);
             if ((__ldcg(Pn + c) & kCode) == id + 1u) mine = min(mine, id);
@@ -1161,9 +1196,10 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
       if (__ldca(&ctl->it_fsize[t & 1u]) == 0) break;          // F' empty: no cycle
       ++g;
       if (lead) reset_slot(ctl, (g + 1u) % 3u);
-      reset_pass(a, g, &sh);
+      reset_pass<RL>(a, g, t, &sh);
       cur = 0;
       grid.sync();
+      vmax = __ldcg(&ctl->it_vmax[t & 1u]);
     }
   }
   if (lead) {
@@ -1665,6 +1701,7 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig
   a.nwords = (uint32_t)(((uint64_t)n + 31) / 32);
   a.nwords_pad = ws.n_pad / 32u;
   a.chunk_cap = ws.chunk_cap;
+  a.cand_cap = ws.n_pad + 1;
   a.ctl = ws.ctl.as<RunCtl>();
   a.iter_hash = cap ? ws.hist.as<unsigned long long>() : nullptr;
   a.iter_steps = cap ? ws.hist.as<unsigned long long>() + cap : nullptr;

@@ -31,6 +31,7 @@ struct RunCtl {
   unsigned int it_finwit[2];
   unsigned int it_dcount[2];
   unsigned long long it_fsize[2];
+  unsigned int it_vmax[2];        // per fixpoint (parity): max over F of id+1, the largest possible map value
   unsigned long long res[16];
 };
 
@@ -70,6 +71,7 @@ struct RunArgs {
   const uint32_t* perm;            // vertex id -> storage position (null: identity)
   uint32_t nwords, nwords_pad;     // FB words for n and for the padded rows
   uint32_t chunk_cap;
+  uint32_t cand_cap;               // capacity of C[k]
   RunCtl* ctl;
   unsigned long long* iter_hash;
   unsigned long long* iter_steps;
@@ -96,6 +98,8 @@ struct RunOut {
   unsigned long long res[16];
   float ms;
   uint32_t grid, block;
+  double plan_ms = 0;
+  int layout = 1;
 };
 
 // Runs the device-resident MAP loop. F must already hold the accepting words.

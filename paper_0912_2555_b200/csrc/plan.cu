@@ -287,9 +287,9 @@ void permute_bits(const uint32_t* src, const uint32_t* orig, uint32_t n, uint32_
   CYC_LAUNCHED();
 }
 
-void build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& plan, cudaStream_t s) {
+bool build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& plan, cudaStream_t s) {
   if (const char* e = std::getenv("CYC_LAYOUT")) layout = std::atoi(e);
-  if (plan.decided && plan.layout == layout) return;
+  if (plan.decided && plan.layout == layout) return false;
   const auto t0 = std::chrono::steady_clock::now();
   const bool dbg = std::getenv("CYC_DEBUG_TIMING") != nullptr;
   auto tm = t0;
@@ -304,9 +304,9 @@ void build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& pla
   plan.decided = true;
   plan.layout = layout;
   const uint32_t n = gath.n;
-  if (layout == kLayoutIdentity || n < 64) return;
+  if (layout == kLayoutIdentity || n < 64) return true;
   // a map buffer within ~1/3 of L2 stays resident in id order
-  if (layout == kLayoutAuto && (uint64_t)n * 4 <= (40ull << 20)) return;
+  if (layout == kLayoutAuto && (uint64_t)n * 4 <= (40ull << 20)) return true;
   const uint32_t nw = (uint32_t)sm_count() * kPlanWarps;
   const uint32_t per_warp = div_up(div_up(n, nw), 32) * 32;
   DevBuf T((size_t)kBuckets * nw * 4, s), base((size_t)kBuckets * nw * 4 + 4, s), tot(kBuckets * 8, s);
@@ -332,7 +332,7 @@ void build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& pla
   }
   mark("hist");
   plan.hot_share = gath.m ? std::min(1.0, hot / (double)gath.m) : 0.0;
-  if (layout == kLayoutAuto && plan.hot_share < 0.5) return;
+  if (layout == kLayoutAuto && plan.hot_share < 0.5) return true;
   plan.relabel = true;
   const uint32_t np = (uint32_t)(((uint64_t)n + kRowPad - 1) / kRowPad * kRowPad);
   plan.orig.alloc(((size_t)np + 1) * 4, s);
@@ -393,6 +393,7 @@ void build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& pla
   if (dbg)
     std::fprintf(stderr, "[cyc plan] relabel n=%u m=%u hot_share=%.3f sell_words=%llu heavy_chunks=%u %.3f ms\n", n,
                  gath.m, plan.hot_share, (unsigned long long)plan.sell_words, plan.gath.n_heavy_chunks, plan.build_ms);
+  return true;
 }
 
 }  // namespace cyc

@@ -47,7 +47,8 @@ struct MapPlan {
 // Decides the layout (kLayoutAuto: relabel when the map vector is larger than
 // ~1/3 of L2 and the n/8 hottest vertices take >= half of all gathers) and
 // builds the storage-space CSRs with their heavy chunks and HYB slab.
-void build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& plan, cudaStream_t s);
+// Returns false when the graph's plan for this layout was already built.
+bool build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& plan, cudaStream_t s);
 
 // dst bit p = src bit orig[p] for p < n (u32 words, dst has n_words words).
 void permute_bits(const uint32_t* src, const uint32_t* orig, uint32_t n, uint32_t* dst, cudaStream_t s);

@@ -744,3 +744,34 @@ def test_restrict_hub_rows(eng, R):
         off, col = r.snapshot.gather_index()
         gt = R.transpose(rg)
         assert np.array_equal(off, gt.off) and np.array_equal(col, gt.col)
+
+
+def test_overlapped_build_equals_sequential(eng, monkeypatch):
+    """Logs of >= 2^24 edges build the gather index on a second stream by a
+    helper thread (abi.cu build_graph); the result must equal the sequential
+    build bit for bit (both CSRs)."""
+    from paper_0912_2555_b200 import _abi
+
+    p = eng.preset(3)
+    p.scale, p.edgefactor = 20, 16
+    eng.prepare(p)
+    assert p.m >= 1 << 24
+    ctx = eng.default_context()
+    L, C = _abi.lib(), _abi.C
+    de, da = C.c_void_p(), C.c_void_p()
+    _abi.check(L.cyc_device_alloc(ctx.handle, p.m * 8, C.byref(de)))
+    _abi.check(L.cyc_device_alloc(ctx.handle, ((p.n + 63) // 64) * 8, C.byref(da)))
+    try:
+        _abi.check(L.cyc_gen_fill(ctx.handle, C.byref(p), de, da))
+        out = []
+        for seq in (False, True):
+            if seq:
+                monkeypatch.setenv("CYC_BUILD_SEQUENTIAL", "1")
+            s = _device_snapshot(eng, p, ctx, de, da, eng.Orientation.transposed)
+            off, col = s.gather_index()
+            out.append((s.row_offsets.copy(), s.col_indices.copy(), off.copy(), col.copy()))
+        for a, b in zip(*out):
+            assert np.array_equal(a, b)
+    finally:
+        L.cyc_device_free(ctx.handle, de)
+        L.cyc_device_free(ctx.handle, da)

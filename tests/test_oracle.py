@@ -318,3 +318,19 @@ def test_generators_deterministic(R):
         assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
     p = R.preset(2)
     assert (p.n, p.m) == (64 * (4096 * 16 + 1) + 1, 64 * 4096 * (1 + 16 + 16))
+
+
+def test_fast_snapshot_setup_equals_build_snapshot(REF, R):
+    """bench.py's CPU arm builds config 3's snapshot with the parallel setup
+    builder (ref_driver.cpp ref_snapshot_gen_fast) before timing the
+    reference's MaxPropagation; it must equal build_snapshot (graph.cpp:63-105)."""
+    for cfg, over in ((1, {}), (3, {"scale": 16}), (2, {"L": 8, "W": 64, "S": 8}), (5, {"L": 8, "W": 4, "S": 16})):
+        p = R.preset(cfg)
+        for k, v in over.items():
+            setattr(p, k, v)
+        R.prepare(p)
+        for tr in (True, False):
+            a = REF.snapshot_gen(p, tr).export()
+            b = REF.snapshot_gen_fast(p, tr, 4).export()
+            assert np.array_equal(a[0].off, b[0].off) and np.array_equal(a[0].col, b[0].col)
+            assert np.array_equal(a[1], b[1])
