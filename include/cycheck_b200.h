@@ -227,6 +227,39 @@ cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32
                      const uint64_t* acc_words, int orientation, int scc_restrict,
                      const cyc_map_options* opt, cyc_map_stats* stats, double* ms_out);
 
+/* ---- row-sharded run_map over several GPUs ----------------- */
+/* A shard is one rank's part of a graph: from the whole edge log it keeps
+ * the gather rows of an edge-balanced contiguous row range (the reference's
+ * worker partition, map_engine.cpp:35-43) and the push rows that target them,
+ * so a rank's edge memory is ~1/world. The map vector is replicated; in every
+ * step each rank stores the rows it changed straight into every peer's vector
+ * (NVLink peer memory) and the ranks meet at a system-scope barrier inside
+ * one persistent kernel each. Results equal run_map on the whole graph.
+ * Ranks in different processes connect by exchanging cyc_shard_handle()
+ * blobs (e.g. an allgather); ranks in one process with cyc_shard_connect_local
+ * (one context per device; ranks that share a device run as one grid, for
+ * tests). layout: CYC_LAYOUT_* as in cyc_map_options. */
+typedef struct cyc_shard cyc_shard;
+#define CYC_SHARD_HANDLE_BYTES 512
+cyc_status cyc_shard_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
+                           const uint64_t* acc_words, int orientation, int layout, int world, int rank,
+                           cyc_shard** out);
+/* rows [row_lo, row_hi) in storage order; local snapshot edges; device bytes
+ * of the rank's graph structures (edges ~1/world, vectors replicated). */
+cyc_status cyc_shard_info(const cyc_shard* sh, uint32_t* row_lo, uint32_t* row_hi, uint64_t* local_edges,
+                          uint64_t* device_bytes);
+cyc_status cyc_shard_handle(const cyc_shard* sh, void* out);
+/* handles: world blobs of CYC_SHARD_HANDLE_BYTES, in rank order */
+cyc_status cyc_shard_connect(cyc_shard* sh, const void* handles);
+cyc_status cyc_shard_connect_local(cyc_shard* const* shards, int world);
+/* run_map (map_engine.cpp:139-162) on the `count` ranks this process holds
+ * (1 per process, or all of them after cyc_shard_connect_local); every rank's
+ * stats are the whole graph's; final_values / iter_* from shards[0]'s replica. */
+cyc_status cyc_shard_run_map(cyc_shard* const* shards, int count, const uint64_t* acc_words,
+                             const cyc_map_options* opt, cyc_map_stats* stats, uint32_t* final_values,
+                             uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap);
+void cyc_shard_destroy(cyc_shard* sh);
+
 /* ---- synthetic inputs and buffers (bench / tests) ----------------------- */
 /* Generates a cyc_gen.h configuration's edge log and accepting words into
  * device or host buffers (edges: 2*m u32, acc: ceil(n/64) u64). */

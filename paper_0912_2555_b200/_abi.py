@@ -181,7 +181,17 @@ _SIGS = {
     "cyc_fused_connect": (C.c_int, [_P, _P]),
     "cyc_fused_run": (C.c_int, [_P, _P, C.c_int, C.POINTER(MapStatsC), _P]),
     "cyc_fused_close": (None, [_P]),
+    "cyc_shard_build": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(_P)]),
+    "cyc_shard_info": (C.c_int, [_P, _U32P, _U32P, _U64P, _U64P]),
+    "cyc_shard_handle": (C.c_int, [_P, _P]),
+    "cyc_shard_connect": (C.c_int, [_P, _P]),
+    "cyc_shard_connect_local": (C.c_int, [_P, C.c_int]),
+    "cyc_shard_run_map": (C.c_int, [_P, C.c_int, _P, C.POINTER(MapOptionsC), C.POINTER(MapStatsC), _P, _P, _P,
+                                    C.c_uint64]),
+    "cyc_shard_destroy": (None, [_P]),
 }
+SHARD_HANDLE_BYTES = 512  # CYC_SHARD_HANDLE_BYTES
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
 

@@ -22,6 +22,7 @@
 #include "ingest.cuh"
 #include "map_run.cuh"
 #include "plan.cuh"
+#include "shard.cuh"
 #include "owcty.cuh"
 #include "scc.cuh"
 
@@ -185,6 +186,11 @@ struct cyc_fused {
   cyc_ctx* ctx = nullptr;
   const cyc_graph* g = nullptr;
   cyc::FusedShard sh;
+};
+
+struct cyc_shard {
+  cyc_ctx* ctx = nullptr;
+  cyc::ShardGraph g;
 };
 
 struct cyc_explicit {
@@ -1030,6 +1036,133 @@ cyc_status cyc_check(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32
       ms_out[3] = ms(t0, t3);
     }
   });
+}
+
+cyc_status cyc_shard_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n,
+                           const uint64_t* acc_words, int orientation, int layout, int world, int rank,
+                           cyc_shard** out) {
+  CallTrace trace_("cyc_shard_build");
+  return guard([&] {
+    require(ctx && out, CYC_E_CONTRACT, "null argument");
+    require(orientation == CYC_FORWARD || orientation == CYC_TRANSPOSED, CYC_E_CONTRACT,
+            "build_snapshot: bad orientation");
+    require(layout >= CYC_LAYOUT_AUTO && layout <= CYC_LAYOUT_DEGREE, CYC_E_CONTRACT, "bad layout");
+    require(n < 0x80000000u, CYC_E_RESOURCE, "vertex count must be < 2^31");
+    require(m_log < 0xFFFFFFFFull, CYC_E_RESOURCE, "edge log prefix must be < 2^32");
+    require(m_log == 0 || edges, CYC_E_CONTRACT, "build_snapshot: null edge array");
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    DevBuf tmp, tacc;
+    const uint32_t* de = stage_in(edges, (size_t)m_log * 2, tmp, ctx->s);
+    const uint64_t* da = stage_in(acc_words, acc_words64(n), tacc, ctx->s);
+    auto* sh = new cyc_shard;
+    sh->ctx = ctx;
+    try {
+      cyc::build_shard(de, m_log, n, da, orientation, world, rank, layout, sh->g, ctx->arena, ctx->s);
+    } catch (...) {
+      delete sh;
+      throw;
+    }
+    ctx->refs.fetch_add(1);
+    *out = sh;
+  });
+}
+
+cyc_status cyc_shard_info(const cyc_shard* sh, uint32_t* row_lo, uint32_t* row_hi, uint64_t* local_edges,
+                          uint64_t* device_bytes) {
+  return guard([&] {
+    require(sh, CYC_E_CONTRACT, "null shard");
+    if (row_lo) *row_lo = sh->g.row_lo;
+    if (row_hi) *row_hi = sh->g.row_hi;
+    if (local_edges) *local_edges = sh->g.m_local;
+    if (device_bytes) *device_bytes = sh->g.device_bytes();
+  });
+}
+
+cyc_status cyc_shard_handle(const cyc_shard* sh, void* out) {
+  static_assert(sizeof(cyc::ShardHandles) <= CYC_SHARD_HANDLE_BYTES, "handle blob too small");
+  return guard([&] {
+    require(sh && out, CYC_E_CONTRACT, "null argument");
+    CYC_CUDA(cudaSetDevice(sh->g.device));
+    cyc::ShardHandles h;
+    std::memset(&h, 0, sizeof h);
+    cyc::shard_export(sh->g, h);
+    std::memset(out, 0, CYC_SHARD_HANDLE_BYTES);
+    std::memcpy(out, &h, sizeof h);
+  });
+}
+
+cyc_status cyc_shard_connect(cyc_shard* sh, const void* handles) {
+  return guard([&] {
+    require(sh && handles, CYC_E_CONTRACT, "null argument");
+    CYC_CUDA(cudaSetDevice(sh->g.device));
+    std::vector<cyc::ShardHandles> all(sh->g.world);
+    for (int p = 0; p < sh->g.world; ++p)
+      std::memcpy(&all[p], static_cast<const char*>(handles) + (size_t)p * CYC_SHARD_HANDLE_BYTES, sizeof all[p]);
+    cyc::shard_connect_ipc(sh->g, all.data(), sh->g.world);
+  });
+}
+
+cyc_status cyc_shard_connect_local(cyc_shard* const* shards, int world) {
+  return guard([&] {
+    require(shards && world >= 1 && world <= cyc::kMaxWorld, CYC_E_CONTRACT, "bad shards");
+    std::vector<cyc::ShardGraph*> gs(world);
+    for (int i = 0; i < world; ++i) {
+      require(shards[i] != nullptr, CYC_E_CONTRACT, "null shard");
+      gs[i] = &shards[i]->g;
+    }
+    cyc::shard_connect_local(gs.data(), world);
+  });
+}
+
+cyc_status cyc_shard_run_map(cyc_shard* const* shards, int count, const uint64_t* acc_words,
+                             const cyc_map_options* opt, cyc_map_stats* stats, uint32_t* final_values,
+                             uint64_t* iter_hash, uint64_t* iter_steps, uint64_t cap) {
+  CallTrace trace_("cyc_shard_run_map");
+  return guard([&] {
+    require(shards && count >= 1 && count <= cyc::kMaxWorld, CYC_E_CONTRACT, "run_map: bad shards");
+    cyc_map_options o = opt ? *opt : default_opts();
+    require(o.mode >= CYC_MODE_AUTO && o.mode <= CYC_MODE_PUSH, CYC_E_CONTRACT, "bad mode");
+    std::vector<cyc::ShardGraph*> gs(count);
+    std::vector<cudaStream_t> ss(count);
+    for (int i = 0; i < count; ++i) {
+      require(shards[i] != nullptr, CYC_E_CONTRACT, "null shard");
+      gs[i] = &shards[i]->g;
+      ss[i] = shards[i]->ctx->s;
+    }
+    require(count == 1 || count == gs[0]->world, CYC_E_CONTRACT, "run_map: pass one rank or all of them");
+    const uint64_t hcap = (iter_hash || iter_steps) ? cap : 0;
+    std::vector<cyc::RunOut> outs(count);
+    cyc::shard_run(gs.data(), count, acc_words, o.early_exit != 0, o.mode, o.max_iterations, o.max_steps,
+                   o.push_alpha, hcap, ss.data(), nullptr, nullptr, outs.data());
+    const cyc::RunOut& r = outs[0];
+    fill_stats(r, stats);
+    if (stats) stats->layout = gs[0]->relabel ? CYC_LAYOUT_DEGREE : CYC_LAYOUT_IDENTITY;
+    cyc_ctx* ctx = shards[0]->ctx;
+    CYC_CUDA(cudaSetDevice(ctx->device));
+    const uint32_t n = gs[0]->n;
+    if (final_values && n) {
+      int cur = (int)r.res[cyc::kResCur];
+      if (r.res[cyc::kResIterations] == 0) {
+        CYC_CUDA(cudaMemsetAsync(gs[0]->xP[0], 0, (size_t)n * 4, ctx->s));
+        cur = 0;
+      }
+      DevBuf tmp((size_t)n * 4, ctx->s);
+      cyc::shard_values(*gs[0], cur, tmp.as<uint32_t>(), ctx->s);
+      copy_out(final_values, tmp.as<uint32_t>(), n, ctx->s);
+    }
+    const uint64_t rec = hcap < r.res[cyc::kResIterations] ? hcap : r.res[cyc::kResIterations];
+    if (iter_hash && rec) copy_out(iter_hash, (uint64_t*)gs[0]->ws.hist.p, rec, ctx->s);
+    if (iter_steps && rec) copy_out(iter_steps, (uint64_t*)gs[0]->ws.hist.p + hcap, rec, ctx->s);
+    CYC_CUDA(cudaStreamSynchronize(ctx->s));
+  });
+}
+
+void cyc_shard_destroy(cyc_shard* sh) {
+  if (!sh) return;
+  cyc_ctx* ctx = sh->ctx;
+  cudaSetDevice(ctx->device);
+  delete sh;
+  ctx_release(ctx);
 }
 
 cyc_status cyc_gen_preset(int index, void* gen_params) {

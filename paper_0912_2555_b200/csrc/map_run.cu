@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/cyc_gen.h"
 #include "map_run.cuh"
@@ -66,9 +67,10 @@ constexpr int kBatch = 4;           // frontier vertices per lane in a push step
 constexpr int kHeavyPerLane = kHeavyChunk / 32;  // pull heavy chunk edges per lane
 constexpr int kHeavyBatch = 4;                     // heavy chunks in flight per warp
 
-// Column streams (slab, sliced ELL, heavy chunks and their descriptors) are
-// read once per step: load them evict-first so they do not push the hot map
-// words out of L2 (ld.global.cs).
+// Column streams of a degree-ordered plan (sliced ELL, heavy slab) are larger
+// than L2 and read once per step: load them evict-first so they do not push
+// the hot map words out (ld.global.cs). The identity layout's HYB slab is not
+// hinted: on L2-resident graphs (config 2) it is re-read by every step.
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
 
@@ -116,10 +118,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// This rank's view of the grid (rank-relative block and warp indices).
+__device__ __forceinline__ uint32_t vblk(const RunArgs& a) { return blockIdx.x - a.blk0; }
+__device__ __forceinline__ uint32_t gwarp(const RunArgs& a) { return (vblk(a) * blockDim.x + threadIdx.x) >> 5; }
+__device__ __forceinline__ uint32_t nwarps(const RunArgs& a) { return (a.nblk * blockDim.x) >> 5; }
+
 // Trace hook: latest time any warp passed phase `ph` of the current step.
 __device__ __forceinline__ void phase_mark(const RunArgs& a, unsigned long long k, int ph) {
   if (a.trace && k < a.trace_cap && lane_id() == 0) {
-    const uint32_t spread = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) & 15u;
+    const uint32_t spread = (gwarp(a)) & 15u;
     atomicMax(a.trace + 64u * k + 16u + 16u * ph + spread, gtimer());
   }
 }
@@ -446,8 +453,8 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
                                            uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh,
                                            uint32_t* fp, uint4* bc, SlotCtl* sl, StepAcc& acc) {
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   static_assert(32u * R <= kRowPad && kRowPad % (32u * R) == 0, "a row group must not run past the row padding");
   const uint32_t np = a.n_pad;
   for (uint32_t base = gw * (32u * R); base < np; base += nw * (32u * R)) {
@@ -462,7 +469,7 @@ __device__ __forceinline__ void pull_light(const RunArgs& a, const uint32_t* __r
     for (int j = 0; j < K; ++j) {
       uint32_t u[R];
 #pragma unroll
-      for (int k = 0; k < R; ++k) u[k] = ld_stream(a.ell + (size_t)j * np + base + 32u * k + lane);
+      for (int k = 0; k < R; ++k) u[k] = __ldg(a.ell + (size_t)j * np + base + 32u * k + lane);
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const uint32_t w = __ldca(P + u[k]);
@@ -506,12 +513,12 @@ __device__ __forceinline__ void pull_sell(const RunArgs& a, const uint32_t* __re
                                           uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh,
                                           uint32_t* fp, uint4* bc, SlotCtl* sl, StepAcc& acc, const Hot& hot) {
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   static_assert((kRowPad / 32u) % R == 0, "slices per row padding must be a multiple of R");
-  const uint32_t np = a.n_pad, nsl = a.n_pad / 32u;
+  const uint32_t np = a.n_pad, nsl = (a.row_hi - a.row_lo) / 32u;  // this rank's slices
   for (uint32_t s0 = gw * R; s0 < nsl; s0 += nw * R) {
-    const uint32_t base = s0 * 32u;
+    const uint32_t base = a.row_lo + s0 * 32u;
     uint4 d[R];
     uint32_t own[R], best[R];
 #pragma unroll
@@ -566,8 +573,8 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
                                            uint32_t* __restrict__ Q, uint32_t* fb, BlockSh* sh, uint4* bc,
                                            SlotCtl* sl, uint32_t* Cn, StepAcc& acc) {
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   // a warp takes B consecutive chunks (often of one hub row: their results
   // merge before a single finalisation); tail warps do fewer light rows
   for (uint32_t c0 = (nw - 1u - gw) * B; c0 < a.n_heavy; c0 += nw * B) {
@@ -575,7 +582,7 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       const uint32_t c = c0 + (uint32_t)k;
-      ch[k] = c < a.n_heavy ? ld_stream(a.heavy + c) : make_uint4(0u, 0u, 0u, 0u);
+      ch[k] = c < a.n_heavy ? a.heavy[c] : make_uint4(0u, 0u, 0u, 0u);
     }
     uint32_t own = 0;
 #pragma unroll
@@ -589,7 +596,7 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
 #pragma unroll
       for (int r = 0; r < kHeavyPerLane; ++r) {
         const uint32_t i = ch[k].y + lane + 32u * r;
-        u[k][r] = i < ch[k].z ? ld_stream(a.gcol + i) : a.n_pad;
+        u[k][r] = i < ch[k].z ? __ldg(a.gcol + i) : a.n_pad;
       }
 #pragma unroll
     for (int k = 0; k < B; ++k)
@@ -675,8 +682,8 @@ __device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t
                                                 SlotCtl* sl, uint32_t* Cn, StepAcc& acc, const Hot& hot) {
   constexpr int B = CYC_SLAB_B, H = kHeavyPerLane;
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   const uint32_t nh = a.n_hchunks, np = a.n_pad;
   const uint32_t cb = (uint32_t)((uint64_t)gw * nh / nw), ce = (uint32_t)((uint64_t)(gw + 1u) * nh / nw);
   if (cb >= ce) return;
@@ -778,8 +785,8 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, uint32_t vmax, 
   uint4* bc = a.BC[g & 1u];
   uint32_t* Cn = a.C[g & 1u];
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   StepAcc acc;
   Hot hot{0u, vmax};
   if (RL && a.hot_k) {  // stage the previous step's frontier bits of the hottest positions
@@ -787,6 +794,22 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, uint32_t vmax, 
     // rows_epilogue clears fp words as it goes: every CTA stages first
     cg::this_grid().sync();
     hot.k = a.hot_k;
+  }
+  if (a.world > 1) {
+    // vertices of other ranks that changed in step k-1: this replica of x_k
+    // still holds x_{k-2} for them; bring it up to x_{k-1} (their owners store
+    // x_k over it if they change again -- atomicMax makes either order right)
+    // and consume the word (the buffer is written again in step k+1)
+    const uint32_t w0 = a.row_lo / 32u, w1 = a.row_hi / 32u;
+    for (uint32_t wi = gw; wi < a.nwords_pad; wi += nw) {
+      if (wi >= w0 && wi < w1) continue;  // own words: rows_epilogue consumes them
+      const uint32_t word = __ldcg(fp + wi);
+      if (!word) continue;
+      const uint32_t v = wi * 32u + lane;
+      if ((word >> lane) & 1u) atomicMax(Q + v, __ldcg(P + v));
+      __syncwarp();
+      if (lane == 0) fp[wi] = 0u;
+    }
   }
   // many chunks per warp (R-MAT hubs): four in flight, and reads before the
   // contended atomics; few (config 2's connectors): one per warp, spread over
@@ -829,8 +852,8 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t* wlp = a.WL[(g - 1u) & 1u];
   const uint4* bp = a.BC[(g - 1u) & 1u];
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   StepAcc acc;
   // big frontier vertices first: one warp per kChunk-edge chunk, each lane
   // raising kChunk/32 targets as one batch
@@ -855,7 +878,8 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   // a scan of the whole bitmap when that list overflowed. Lane i owns bit i of
   // each word; each word is cleared by the warp that consumes it.
   const uint32_t wlc = __ldca(&pl->wl_count);
-  const bool scan = __ldca(&pl->wl_over) != 0u;
+  // sharded: the word lists only know this rank's raises; scan the replicated bitmap
+  const bool scan = a.world > 1 || __ldca(&pl->wl_over) != 0u;
   const uint32_t groups = scan ? (a.nwords + 3u) / 4u : (wlc + 3u) / 4u;
   for (uint32_t it = gw; it < groups; it += nw) {
     uint32_t wi[kBatch], wd[kBatch];
@@ -920,8 +944,8 @@ __device__ void finish_pass(const RunArgs& a, int cur, uint64_t t, bool mark_use
   const uint32_t* P = a.P[cur];
   RunCtl* ctl = a.ctl;
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   unsigned long long h = 0;
   uint32_t fw = kNone;
   for (uint32_t base = gw * 32u; base < a.n; base += nw * 32u) {
@@ -949,7 +973,7 @@ __device__ void finish_pass(const RunArgs& a, int cur, uint64_t t, bool mark_use
     if (h) atomicAdd(&ctl->it_hash[t & 1u], h);
     if (fw != kNone) atomicMin(&ctl->it_finwit[t & 1u], fw);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (vblk(a) == 0 && threadIdx.x == 0) {
     const uint32_t nt = (uint32_t)((t + 1u) & 1u);
     ctl->it_hash[nt] = 0;
     ctl->it_finwit[nt] = kNone;
@@ -964,8 +988,8 @@ __device__ void finish_pass(const RunArgs& a, int cur, uint64_t t, bool mark_use
 __device__ void demote_pass(const RunArgs& a, unsigned int* dcount, unsigned long long* fsize,
                             BlockSh* sh) {
   unsigned long long dc = 0, fs = 0;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.nwords; i += stride) {
+  const uint32_t stride = a.nblk * blockDim.x;
+  for (uint32_t i = vblk(a) * blockDim.x + threadIdx.x; i < a.nwords; i += stride) {
     const uint32_t f = __ldcg(a.F + i), u = __ldcg(a.used + i);
     const uint32_t nf = f & ~u;
     dc += __popc(f & u);
@@ -993,8 +1017,8 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, uint64_t t, BlockSh* sh
   SlotCtl* sl = &a.ctl->slot[g % 3u];
   uint4* bc = a.BC[g & 1u];
   const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = gwarp(a);
+  const uint32_t nw = nwarps(a);
   unsigned long long fe = 0;
   uint32_t vm = 0;  // max id+1 over F: no map value of this fixpoint can exceed it
   // 32 words (1024 vertices) per warp iteration
@@ -1030,7 +1054,7 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, uint64_t t, BlockSh* sh
   vm = ~block_min(~vm, sh);
   if (threadIdx.x == 0 && fe) atomicAdd(&sl->fedges, fe);
   if (threadIdx.x == 0 && vm) atomicMax(&a.ctl->it_vmax[t & 1u], vm);
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->it_vmax[(t + 1u) & 1u] = 0u;  // the next fixpoint's
+  if (vblk(a) == 0 && threadIdx.x == 0) a.ctl->it_vmax[(t + 1u) & 1u] = 0u;  // the next fixpoint's
   wl_flush(sh, sl, a.WL[g & 1u], a.wl_cap);
 }
 
@@ -1046,20 +1070,105 @@ __device__ __forceinline__ void reset_slot(RunCtl* c, uint32_t s) {
   sl.wl_over = 0;
 }
 
-template <bool RL>
-__global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
+// ------------------------------------------------------- sharded exchange
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Every rank's writes so far (local and into peers) visible to every rank.
+// Emulated ranks share the grid, so its barrier is the cross-rank barrier;
+// real ranks also meet at system-scope counters in each rank's memory (the
+// lead spins with a 30 s timeout that traps instead of hanging the GPU).
+__device__ void rank_sync(const RunArgs& a, cg::grid_group& grid, unsigned long long& bars) {
+  __threadfence_system();
+  grid.sync();
+  if (a.world > 1 && !a.emulated) {
+    if (vblk(a) == 0 && threadIdx.x == 0) {
+      for (int p = 0; p < a.world; ++p) atomicAdd_system(a.peerBar[p], 1ull);
+      ++bars;
+      const unsigned long long target = bars * (unsigned long long)a.world, t0 = gtimer();
+      while (ld_acquire_sys(a.bar) < target)
+        if (gtimer() - t0 > 30000000000ull) __trap();
+    }
+    grid.sync();
+  }
+}
+
+__device__ __forceinline__ ShardRec ld_rec(const ShardRec* r) {
+  ShardRec x;
+  x.fedges = __ldcg(&r->fedges);
+  x.nraised = __ldcg(&r->nraised);
+  x.changed = __ldcg(&r->changed);
+  x.wit = __ldcg(&r->wit);
+  x.pad = 0;
+  return x;
+}
+
+// End of a sharded step (or setup, publish = false): this rank's record goes
+// to every rank, the rows it changed (its frontier words of tag g) are stored
+// into every peer's buffers, then the records of all ranks are reduced.
+__device__ ShardRec exchange_step(const RunArgs& a, cg::grid_group& grid, uint32_t g, int cur_new,
+                                  const SlotCtl* sl, uint32_t wit, bool publish, unsigned long long& bars) {
+  const uint32_t par = g & 1u;
+  if (vblk(a) == 0 && threadIdx.x == 0) {
+    ShardRec r;
+    r.fedges = __ldcg(&sl->fedges);
+    r.nraised = __ldcg(&sl->nraised);
+    r.changed = __ldcg(&sl->changed);
+    r.wit = wit;
+    r.pad = 0;
+    for (int p = 0; p < a.world; ++p) a.peerRec[p][par * kMaxWorld + a.rank] = r;
+  }
+  if (publish) {
+    const uint32_t lane = lane_id(), gw = gwarp(a), nw = nwarps(a);
+    const uint32_t* fbw = a.FB[par];
+    const uint32_t* Pn = a.P[cur_new];
+    for (uint32_t wi = a.row_lo / 32u + gw; wi < a.row_hi / 32u; wi += nw) {
+      const uint32_t word = __ldcg(fbw + wi);
+      if (!word) continue;
+      const uint32_t v = wi * 32u + lane;
+      const bool on = (word >> lane) & 1u;
+      const uint32_t x = on ? __ldcg(Pn + v) : 0u;
+      for (int p = 0; p < a.world; ++p) {
+        if (p == a.rank) continue;
+        if (on) a.peerP[p][cur_new][v] = x;
+        if (lane == 0) a.peerFB[p][par][wi] = word;
+      }
+    }
+  }
+  rank_sync(a, grid, bars);
+  ShardRec t;
+  t.fedges = 0;
+  t.nraised = 0;
+  t.changed = 0;
+  t.wit = kNone;
+  t.pad = 0;
+  for (int p = 0; p < a.world; ++p) {
+    const ShardRec r = ld_rec(a.rec + par * kMaxWorld + p);
+    t.fedges += r.fedges;
+    t.nraised += r.nraised;
+    t.changed |= r.changed;
+    t.wit = min(t.wit, r.wit);
+  }
+  return t;
+}
+
+template <bool RL, bool SH>
+__device__ __forceinline__ void map_run_body(const RunArgs& a) {
   __shared__ BlockSh sh;
   // run statistics live in shared memory of block 0 (kept out of registers)
-  __shared__ unsigned long long stat[kResTag + 1];
+  __shared__ unsigned long long stat[kResBars + 1];
   cg::grid_group grid = cg::this_grid();
   RunCtl* ctl = a.ctl;
   uint32_t g = 1;
   int cur = 0;
   int cycle = 0;
   uint32_t witness = kNone;
-  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const bool lead = vblk(a) == 0 && threadIdx.x == 0;
   if (lead)
-    for (int k = 0; k <= kResTag; ++k) stat[k] = 0;
+    for (int k = 0; k <= kResBars; ++k) stat[k] = 0;
   if (threadIdx.x == 0) {
     sh.wl_n = 0;
     sh.big_n = 0;
@@ -1075,6 +1184,10 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
   if (lead) reset_slot(ctl, (g + 1u) % 3u);
   reset_pass<RL>(a, g, 0, &sh);
   grid.sync();
+  unsigned long long bars = a.bar_base;
+  // sharded: global push degree of F (each rank counts its own push rows)
+  unsigned long long g_fe = 0, g_nr = 0;
+  if constexpr (SH) g_fe = exchange_step(a, grid, g, 0, &ctl->slot[g % 3u], kNone, false, bars).fedges;
   uint64_t t = 0;
   uint32_t vmax = __ldcg(&ctl->it_vmax[0]);
   bool truncated = false;
@@ -1088,13 +1201,15 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
         const uint32_t slot = g % 3u, pslot = (g - 1u) % 3u;
         if (lead) reset_slot(ctl, (g + 1u) % 3u);
         int mode = a.mode;
+        // the previous step's (global) frontier size
+        const unsigned long long p_fe = SH ? g_fe : __ldca(&ctl->slot[pslot].fedges);
+        const unsigned long long p_nr = SH ? g_nr : __ldca(&ctl->slot[pslot].nraised);
         if (mode != kModePull && mode != kModePush) {
           unsigned long long est;
           if (prev_push) {
-            est = __ldca(&ctl->slot[pslot].fedges);
+            est = p_fe;
           } else {  // pull steps count big-vertex degrees exactly, the rest by average
-            const unsigned long long nr = __ldca(&ctl->slot[pslot].nraised);
-            est = __ldca(&ctl->slot[pslot].fedges) + (a.n ? nr * a.m / a.n : 0);
+            est = p_fe + (a.n ? p_nr * a.m / a.n : 0);
           }
           mode = (est * a.alpha < a.m) ? kModePush : kModePull;
         }
@@ -1103,11 +1218,9 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
         if (a.trace && lead && tkk < a.trace_cap) a.trace[64u * tkk + 3u] = gtimer();
         if (mode == kModePush) {
           if (lead) {
-            const unsigned long long fe = __ldca(&ctl->slot[pslot].fedges);
-            const unsigned long long nr = __ldca(&ctl->slot[pslot].nraised);
-            stat[kResEdges] += fe;
-            stat[kResRows] += nr;
-            stat[kResBytes] += 8ull * fe + 12ull * nr;
+            stat[kResEdges] += p_fe;
+            stat[kResRows] += p_nr;
+            stat[kResBytes] += 8ull * p_fe + 12ull * p_nr;
             stat[kResPushSteps] += 1;
           }
           push_step<RL>(a, g, cur, &sh, a.trace ? tkk : ~0ull);
@@ -1122,7 +1235,7 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
         cur ^= 1;
         prev_push = mode == kModePush;
         const SlotCtl* sl = &ctl->slot[slot];
-        const uint32_t changed = __ldca(&sl->changed);
+        uint32_t changed = __ldca(&sl->changed);
         uint32_t w = __ldca(&sl->wit);
         const uint32_t nc = __ldca(&sl->cand_cnt);
         if (lead && a.trace && tkk < a.trace_cap) {
@@ -1152,6 +1265,13 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
             if ((__ldcg(Pn + c) & kCode) == id + 1u) mine = min(mine, id);
           }
           w = min(w, block_min(mine, &sh));
+        }
+        if constexpr (SH) {  // every rank gets the others' changed rows and the global record
+          const ShardRec gr = exchange_step(a, grid, g, cur, sl, w, true, bars);
+          changed = gr.changed;
+          w = gr.wit;
+          g_fe = gr.fedges;
+          g_nr = gr.nraised;
         }
         if (a.early_exit && w != kNone) {
           cycle = 1;
@@ -1199,6 +1319,7 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
       reset_pass<RL>(a, g, t, &sh);
       cur = 0;
       grid.sync();
+      if constexpr (SH) g_fe = exchange_step(a, grid, g, 0, &ctl->slot[g % 3u], kNone, false, bars).fedges;
       vmax = __ldcg(&ctl->it_vmax[t & 1u]);
     }
   }
@@ -1207,9 +1328,24 @@ __global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
     stat[kResWitness] = witness;
     stat[kResCur] = (unsigned long long)cur;
     stat[kResTag] = g;
-    for (int k = 0; k <= kResTag; ++k) ctl->res[k] = stat[k];
+    stat[kResBars] = bars;
+    for (int k = 0; k <= kResBars; ++k) ctl->res[k] = stat[k];
   }
 #undef CYC_STAT
+}
+
+template <bool RL, bool SH>
+__global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run(RunArgs a) {
+  map_run_body<RL, SH>(a);
+}
+
+// Tests on one GPU: every rank of a sharded run in ONE cooperative grid (rank
+// r = blocks [r*nblk, (r+1)*nblk)), each with its own arguments; the grid
+// barrier doubles as the cross-rank barrier (B200_PROFILING.md: ranks that
+// wait on one another must not be separate launches on one GPU).
+template <bool RL>
+__global__ void __launch_bounds__(run_threads<RL>(), 1) k_map_run_emul(const RunArgs* __restrict__ ranks, int world) {
+  map_run_body<RL, true>(ranks[blockIdx.x / (gridDim.x / (uint32_t)world)]);
 }
 
 __global__ void k_big_mask(uint32_t n, const uint32_t* __restrict__ poff, uint32_t* __restrict__ bigm) {
@@ -1628,13 +1764,14 @@ void RunWs::ensure(uint32_t nn, uint32_t mm, const uint32_t* poff, cudaStream_t 
   ctl.alloc(sizeof(RunCtl), s);
 }
 
-void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig, const uint32_t* perm,
-                    const uint4* sdesc, const uint32_t* sell, const uint32_t* hcol, const uint32_t* hrow,
-                    uint32_t n_hchunks, RunWs& ws, int early_exit, int mode,
-                    unsigned long long max_iterations, unsigned long long max_steps,
-                    uint32_t alpha, unsigned long long cap, uint32_t trace_cap, cudaStream_t s,
-                    cudaEvent_t e0, cudaEvent_t e1, RunOut& out) {
-  const uint32_t n = gath.n;
+namespace {
+
+// The arguments every run shares (workspace, CSRs, layout, options); resets
+// the control block and the demotion scratch on s.
+RunArgs base_args(const DevCsr& snap, const DevCsr& gath, uint32_t n, const uint32_t* orig, const uint32_t* perm,
+                  const uint4* sdesc, const uint32_t* sell, const uint32_t* hcol, const uint32_t* hrow,
+                  uint32_t n_hchunks, RunWs& ws, int early_exit, int mode, unsigned long long max_iterations,
+                  unsigned long long max_steps, uint32_t alpha, unsigned long long cap, cudaStream_t s) {
   RunCtl init;
   std::memset(&init, 0, sizeof init);
   for (int k = 0; k < 3; ++k) init.slot[k].wit = kNone;
@@ -1648,6 +1785,9 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig
   std::memset(&a, 0, sizeof a);
   a.n = n;
   a.m = gath.m;
+  a.world = 1;  // single device: the whole grid, all rows
+  a.row_lo = 0;
+  a.row_hi = ws.n_pad;
   a.goff = gath.o();
   a.gcol = gath.c();
   a.ell = gath.ell.as<uint32_t>();
@@ -1677,26 +1817,6 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig
   a.hcol = hcol;
   a.hrow = hrow;
   a.n_hchunks = n_hchunks;
-  // shared-memory staging of the hottest map words (degree-ordered plans only)
-  static const size_t hot_cap = [] {  // thread-safe one-time init
-    int dev = 0, optin = 0;
-    CYC_CUDA(cudaGetDevice(&dev));
-    CYC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes fa;
-    CYC_CUDA(cudaFuncGetAttributes(&fa, k_map_run<true>));
-    // measured (scripts/micro/gather_mix.cu): random L2 gathers hold ~283 G/s
-    // per GPU with up to 128 KB of shared memory per SM and halve at 200 KB
-    // (the L1 carve-out that tracks in-flight loads shrinks), so stop at 128 KB
-    size_t cap = (size_t)optin > fa.sharedSizeBytes + 1024 ? (size_t)optin - fa.sharedSizeBytes - 1024 : 0;
-    cap = std::min<size_t>(cap, 128u << 10);
-    CYC_CUDA(cudaFuncSetAttribute(k_map_run<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
-    return cap;
-  }();
-  // frontier bits of the first CYC_HOT_POS positions (tested at 2^19 = 64 KB)
-  const char* hk = std::getenv("CYC_HOT_POS");
-  uint64_t hot_pos = hk ? std::strtoull(hk, nullptr, 10) : 0ull;  // off by default: no gain measured on C3
-  hot_pos = orig ? std::min<uint64_t>({hot_pos, (uint64_t)hot_cap * 8, (uint64_t)ws.n_pad}) : 0;
-  a.hot_k = (uint32_t)(hot_pos / 32u * 32u);
   ws.orig = orig;
   a.nwords = (uint32_t)(((uint64_t)n + 31) / 32);
   a.nwords_pad = ws.n_pad / 32u;
@@ -1711,6 +1831,41 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig
   a.alpha = alpha ? alpha : 16u;  // swept on config 2: 4 81.2, 8 70.4, 16 69.4, 24 70.3, 64 71.4 ms
   a.early_exit = early_exit;
   a.mode = mode;
+  return a;
+}
+
+}  // namespace
+
+void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig, const uint32_t* perm,
+                    const uint4* sdesc, const uint32_t* sell, const uint32_t* hcol, const uint32_t* hrow,
+                    uint32_t n_hchunks, RunWs& ws, int early_exit, int mode,
+                    unsigned long long max_iterations, unsigned long long max_steps,
+                    uint32_t alpha, unsigned long long cap, uint32_t trace_cap, cudaStream_t s,
+                    cudaEvent_t e0, cudaEvent_t e1, RunOut& out) {
+  RunArgs a = base_args(snap, gath, gath.n, orig, perm, sdesc, sell, hcol, hrow, n_hchunks, ws, early_exit, mode,
+                        max_iterations, max_steps, alpha, cap, s);
+  // shared-memory staging of the hottest map words (degree-ordered plans only)
+  static const size_t hot_cap = [] {  // thread-safe one-time init
+    int dev = 0, optin = 0;
+    CYC_CUDA(cudaGetDevice(&dev));
+    CYC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    CYC_CUDA(cudaFuncGetAttributes(&fa, k_map_run<true, false>));
+    // measured (scripts/micro/gather_mix.cu): random L2 gathers hold ~283 G/s
+    // per GPU with up to 128 KB of shared memory per SM and halve at 200 KB
+    // (the L1 carve-out that tracks in-flight loads shrinks), so stop at 128 KB
+    size_t cap = (size_t)optin > fa.sharedSizeBytes + 1024 ? (size_t)optin - fa.sharedSizeBytes - 1024 : 0;
+    cap = std::min<size_t>(cap, 128u << 10);
+    for (const void* f : {(const void*)k_map_run<true, false>, (const void*)k_map_run<true, true>,
+                          (const void*)k_map_run<false, true>})
+      CYC_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+    return cap;
+  }();
+  // frontier bits of the first CYC_HOT_POS positions (tested at 2^19 = 64 KB)
+  const char* hk = std::getenv("CYC_HOT_POS");
+  uint64_t hot_pos = hk ? std::strtoull(hk, nullptr, 10) : 0ull;  // off by default: no gain measured on C3
+  hot_pos = orig ? std::min<uint64_t>({hot_pos, (uint64_t)hot_cap * 8, (uint64_t)ws.n_pad}) : 0;
+  a.hot_k = (uint32_t)(hot_pos / 32u * 32u);
   if (trace_cap) {
     if (ws.trace.bytes < (size_t)trace_cap * 512) ws.trace.alloc((size_t)trace_cap * 512, s);
     CYC_CUDA(cudaMemsetAsync(ws.trace.p, 0, (size_t)trace_cap * 512, s));
@@ -1720,19 +1875,22 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig
 
   static const int blocks_per_sm = [] {  // thread-safe one-time init
     int b = 0;
-    CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_map_run<false>, kRunThreads, 0));
+    CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_map_run<false, false>, kRunThreads, 0));
     return b > 0 ? b : 1;
   }();
   const size_t dyn = (size_t)a.hot_k / 8;
   int bps = blocks_per_sm;
   if (orig) {
-    CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_map_run<true>, kRunThreadsRL, dyn));
+    CYC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_map_run<true, false>, kRunThreadsRL, dyn));
     if (bps < 1) bps = 1;
   }
   dim3 grid((unsigned)(sm_count() * bps)), block(orig ? kRunThreadsRL : kRunThreads);
+  a.blk0 = 0;
+  a.nblk = grid.x;
   void* args[] = {&a};
   CYC_CUDA(cudaEventRecord(e0, s));
-  coop_launch(orig ? (const void*)k_map_run<true> : (const void*)k_map_run<false>, grid, block, args, dyn, s);
+  coop_launch(orig ? (const void*)k_map_run<true, false> : (const void*)k_map_run<false, false>, grid, block, args,
+              dyn, s);
   CYC_LAUNCHED();
   CYC_CUDA(cudaEventRecord(e1, s));
   RunCtl host;
@@ -1744,6 +1902,98 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig
   out.block = block.x;
   const unsigned long long k = host.res[kResTag];  // trace slots are indexed by step tag
   ws.trace_len = (uint32_t)(k < trace_cap ? k : trace_cap);
+}
+
+void launch_map_run_shards(ShardRunIn* in, int k, bool emulated, int early_exit, int mode,
+                           unsigned long long max_iterations, unsigned long long max_steps, uint32_t alpha,
+                           unsigned long long cap, RunOut* outs) {
+  std::vector<RunArgs> args(k);
+  const bool rl = in[0].orig != nullptr;
+  for (int i = 0; i < k; ++i) {
+    ShardRunIn& r = in[i];
+    CYC_CUDA(cudaSetDevice(r.device));
+    if (cap && r.ws->hist.bytes < cap * 16) r.ws->hist.alloc(cap * 16, r.s);
+    RunArgs& a = args[i];
+    a = base_args(*r.push, *r.gath, r.n, r.orig, r.perm, r.sdesc, r.sell, r.hcol, r.hrow, r.n_hchunks, *r.ws,
+                  early_exit, mode, max_iterations, max_steps, alpha, cap, r.s);
+    a.m = (uint32_t)r.m_global;  // decisions and MapStats are about the whole graph
+    a.bigm = r.bigm;
+    for (int b = 0; b < 2; ++b) {
+      a.P[b] = r.P[b];
+      a.FB[b] = r.FB[b];
+    }
+    a.world = r.world;
+    a.rank = r.rank;
+    a.emulated = emulated;
+    a.row_lo = r.row_lo;
+    a.row_hi = r.row_hi;
+    std::memcpy(a.peerP, r.peerP, sizeof a.peerP);
+    std::memcpy(a.peerFB, r.peerFB, sizeof a.peerFB);
+    a.rec = r.rec;
+    std::memcpy(a.peerRec, r.peerRec, sizeof a.peerRec);
+    a.bar = r.bar;
+    std::memcpy(a.peerBar, r.peerBar, sizeof a.peerBar);
+    a.bar_base = r.bar_base;
+  }
+  const dim3 block(rl ? kRunThreadsRL : kRunThreads);
+  std::vector<cudaEvent_t> ev(2 * k);
+  for (int i = 0; i < k; ++i) {
+    CYC_CUDA(cudaSetDevice(in[i].device));
+    CYC_CUDA(cudaEventCreate(&ev[2 * i]));
+    CYC_CUDA(cudaEventCreate(&ev[2 * i + 1]));
+  }
+  if (emulated) {  // one grid, rank i = blocks [i*nblk, (i+1)*nblk)
+    const uint32_t nblk = (uint32_t)sm_count() / (uint32_t)k;
+    for (int i = 0; i < k; ++i) {
+      args[i].blk0 = (uint32_t)i * nblk;
+      args[i].nblk = nblk;
+    }
+    DevBuf dargs(sizeof(RunArgs) * k, in[0].s);
+    CYC_CUDA(cudaMemcpyAsync(dargs.p, args.data(), sizeof(RunArgs) * k, cudaMemcpyHostToDevice, in[0].s));
+    const RunArgs* pa = dargs.as<RunArgs>();
+    int world = k;
+    void* kargs[] = {&pa, &world};
+    CYC_CUDA(cudaEventRecord(ev[0], in[0].s));
+    coop_launch(rl ? (const void*)k_map_run_emul<true> : (const void*)k_map_run_emul<false>, dim3(nblk * k), block,
+                kargs, 0, in[0].s);
+    CYC_LAUNCHED();
+    CYC_CUDA(cudaEventRecord(ev[1], in[0].s));
+    for (int i = 1; i < k; ++i) {
+      ev[2 * i] = ev[0];
+      ev[2 * i + 1] = ev[1];
+    }
+    CYC_CUDA(cudaStreamSynchronize(in[0].s));
+  } else {  // one cooperative grid per device, all in flight together
+    const dim3 grid((unsigned)sm_count());
+    for (int i = 0; i < k; ++i) {
+      CYC_CUDA(cudaSetDevice(in[i].device));
+      args[i].blk0 = 0;
+      args[i].nblk = grid.x;
+      void* kargs[] = {&args[i]};
+      CYC_CUDA(cudaEventRecord(ev[2 * i], in[i].s));
+      coop_launch(rl ? (const void*)k_map_run<true, true> : (const void*)k_map_run<false, true>, grid, block, kargs,
+                  0, in[i].s);
+      CYC_LAUNCHED();
+      CYC_CUDA(cudaEventRecord(ev[2 * i + 1], in[i].s));
+    }
+  }
+  for (int i = 0; i < k; ++i) {
+    CYC_CUDA(cudaSetDevice(in[i].device));
+    RunCtl host;
+    CYC_CUDA(cudaMemcpyAsync(&host, in[i].ws->ctl.p, sizeof host, cudaMemcpyDeviceToHost, in[i].s));
+    CYC_CUDA(cudaStreamSynchronize(in[i].s));
+    std::memcpy(outs[i].res, host.res, sizeof outs[i].res);
+    CYC_CUDA(cudaEventElapsedTime(&outs[i].ms, ev[2 * i], ev[2 * i + 1]));
+    outs[i].grid = emulated ? (uint32_t)sm_count() / (uint32_t)k : (uint32_t)sm_count();
+    outs[i].block = block.x;
+    in[i].ws->orig = in[i].orig;
+  }
+  for (int i = 0; i < (emulated ? 1 : k); ++i) {
+    CYC_CUDA(cudaSetDevice(in[i].device));
+    cudaEventDestroy(ev[2 * i]);
+    cudaEventDestroy(ev[2 * i + 1]);
+  }
+  CYC_CUDA(cudaSetDevice(in[0].device));
 }
 
 void strip_codes(const RunWs& ws, int cur, uint32_t n, uint32_t* dst, cudaStream_t s) {

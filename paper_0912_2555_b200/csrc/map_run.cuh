@@ -37,7 +37,19 @@ struct RunCtl {
 
 enum RunRes {
   kResCycle = 0, kResWitness, kResIterations, kResKernelCalls, kResDemoted, kResStepsLast,
-  kResPullSteps, kResPushSteps, kResEdges, kResRows, kResBytes, kResCur, kResTag
+  kResPullSteps, kResPushSteps, kResEdges, kResRows, kResBytes, kResCur, kResTag, kResBars
+};
+
+// Row-sharded runs (world > 1, shard.cu): every rank keeps the whole map vector
+// and frontier bitmaps replicated, computes the rows [row_lo, row_hi) of each
+// step and stores the changed ones straight into every peer's buffers (NVLink
+// peer pointers); per-step records are reduced by every rank after a
+// cross-rank barrier, so all ranks take the same decisions.
+constexpr int kMaxWorld = 8;
+
+struct alignas(32) ShardRec {
+  unsigned long long fedges;  // push degrees of the rank's newly raised vertices (local push rows)
+  unsigned int nraised, changed, wit, pad;
 };
 
 struct RunArgs {
@@ -81,6 +93,17 @@ struct RunArgs {
   uint32_t trace_cap;
   uint32_t alpha;
   int early_exit, mode;
+  // -- this rank's part of the grid and of the rows (single GPU: the whole grid, all rows)
+  uint32_t blk0, nblk;
+  int world, rank, emulated;       // emulated: all ranks share one grid on one GPU (tests)
+  uint32_t row_lo, row_hi;
+  uint32_t* peerP[kMaxWorld][2];
+  uint32_t* peerFB[kMaxWorld][2];
+  ShardRec* rec;                   // [2][kMaxWorld]: step records written by every rank
+  ShardRec* peerRec[kMaxWorld];
+  unsigned long long* bar;         // cross-rank barrier counter, incremented by every rank
+  unsigned long long* peerBar[kMaxWorld];
+  unsigned long long bar_base;     // barriers completed by earlier runs
 };
 
 struct RunWs {
@@ -110,6 +133,43 @@ void launch_map_run(const DevCsr& snap, const DevCsr& gath, const uint32_t* orig
                     unsigned long long max_iterations, unsigned long long max_steps,
                     uint32_t alpha, unsigned long long cap, uint32_t trace_cap, cudaStream_t s,
                     cudaEvent_t e0, cudaEvent_t e1, RunOut& out);
+
+// One rank of a sharded run as seen by the launcher (shard.cu fills it).
+struct ShardRunIn {
+  int device;
+  cudaStream_t s;
+  const DevCsr* push;  // push rows restricted to this rank's targets
+  const DevCsr* gath;  // this rank's gather rows
+  const uint32_t* orig;
+  const uint32_t* perm;
+  const uint4* sdesc;
+  const uint32_t* sell;
+  const uint32_t* hcol;
+  const uint32_t* hrow;
+  uint32_t n_hchunks;
+  RunWs* ws;
+  uint32_t* P[2];
+  uint32_t* FB[2];
+  const uint32_t* bigm;  // all-zero: no big-vertex chunk lists in sharded runs
+  uint32_t n;
+  uint64_t m_global;
+  int world, rank;
+  uint32_t row_lo, row_hi;
+  uint32_t* peerP[kMaxWorld][2];
+  uint32_t* peerFB[kMaxWorld][2];
+  ShardRec* rec;
+  ShardRec* peerRec[kMaxWorld];
+  unsigned long long* bar;
+  unsigned long long* peerBar[kMaxWorld];
+  unsigned long long bar_base;
+};
+
+// Runs the k ranks of this process: one cooperative grid per device (they
+// meet at system-scope barriers), or, emulated, all k ranks in one grid on one
+// device (tests). outs[i].res[kResBars] = barriers completed (next bar_base).
+void launch_map_run_shards(ShardRunIn* in, int k, bool emulated, int early_exit, int mode,
+                           unsigned long long max_iterations, unsigned long long max_steps, uint32_t alpha,
+                           unsigned long long cap, RunOut* outs);
 
 // Writes the codes (flag bit stripped) of workspace buffer `cur` into dst,
 // in vertex-id order (ws.orig set: dst[orig[p]] = code of position p).

@@ -190,12 +190,12 @@ __global__ void k_plan_chunks(const uint4* __restrict__ chunks, uint32_t nch, co
 }
 
 // per slice of 32 rows: widest light row and the mask of heavy rows
-__global__ void k_sell_width(uint32_t n, uint32_t nsl, const uint32_t* __restrict__ off, uint32_t heavy,
-                             uint32_t* __restrict__ width, uint32_t* __restrict__ hmask) {
+__global__ void k_sell_width(uint32_t n, uint32_t row0, uint32_t nsl, const uint32_t* __restrict__ off,
+                             uint32_t heavy, uint32_t* __restrict__ width, uint32_t* __restrict__ hmask) {
   const uint32_t lane = lane_of();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t sI = gw; sI < nsl; sI += nw) {
-    const uint32_t v = sI * 32u + lane;
+    const uint32_t v = row0 + sI * 32u + lane;
     const uint32_t d = v < n ? __ldg(off + v + 1) - __ldg(off + v) : 0u;
     const bool hv = d > heavy;
     const uint32_t w = __reduce_max_sync(kFull, hv ? 0u : d);
@@ -207,14 +207,14 @@ __global__ void k_sell_width(uint32_t n, uint32_t nsl, const uint32_t* __restric
   }
 }
 
-__global__ void k_sell_fill(uint32_t n, uint32_t nsl, uint32_t np, const uint32_t* __restrict__ off,
+__global__ void k_sell_fill(uint32_t n, uint32_t row0, uint32_t nsl, uint32_t np, const uint32_t* __restrict__ off,
                             const uint32_t* __restrict__ col, const uint32_t* __restrict__ width,
                             const uint32_t* __restrict__ soff, const uint32_t* __restrict__ hmask,
                             uint32_t* __restrict__ sell, uint4* __restrict__ sdesc) {
   const uint32_t lane = lane_of();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t sI = gw; sI < nsl; sI += nw) {
-    const uint32_t v = sI * 32u + lane;
+    const uint32_t v = row0 + sI * 32u + lane;
     const uint32_t hm = hmask[sI], w = width[sI], o = soff[sI];
     uint32_t b = 0, d = 0;
     if (v < n && !((hm >> lane) & 1u)) {
@@ -281,6 +281,55 @@ void relayout(const DevCsr& in, const uint32_t* orig, const uint32_t* perm, DevC
 
 }  // namespace
 
+void degree_order(const uint32_t* key_off, uint32_t n, uint32_t* orig, uint32_t* perm, cudaStream_t s) {
+  const uint32_t nw = (uint32_t)sm_count() * kPlanWarps;
+  const uint32_t per_warp = div_up(div_up(n, nw), 32) * 32;
+  const uint32_t blocks = div_up(nw, kPlanWarps);
+  const uint32_t np = (uint32_t)(((uint64_t)n + kRowPad - 1) / kRowPad * kRowPad);
+  DevBuf T((size_t)kBuckets * nw * 4, s), base((size_t)kBuckets * nw * 4 + 4, s), scratch;
+  k_plan_hist<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, key_off, T.as<uint32_t>(), nw);
+  CYC_LAUNCHED();
+  exclusive_scan(T.as<uint32_t>(), base.as<uint32_t>(), kBuckets * nw, nullptr, s, scratch);
+  k_plan_place<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, key_off, base.as<uint32_t>(), nw, orig, perm);
+  CYC_LAUNCHED();
+  k_plan_pad<<<grid_for(np + 1 - n, 256, 1), 256, 0, s>>>(n, np + 1, orig);
+  CYC_LAUNCHED();
+}
+
+void build_hslab(DevCsr& g, uint32_t np, DevBuf& hcol, DevBuf& hrow, uint32_t& n_hchunks, cudaStream_t s) {
+  build_heavy(g, kHeavyDeg, kHeavyChunk, s, 1u);
+  n_hchunks = g.n_heavy_chunks;
+  hcol.alloc(((size_t)n_hchunks * kHeavyChunk + 1) * 4, s);
+  hrow.alloc(((size_t)n_hchunks + 1) * 4, s);
+  if (n_hchunks) {
+    k_hslab_fill<<<grid_for((uint64_t)n_hchunks * 32, 256, 8), 256, 0, s>>>(
+        g.heavy.as<uint4>(), n_hchunks, g.c(), np, hcol.as<uint32_t>(), hrow.as<uint32_t>());
+    CYC_LAUNCHED();
+  }
+}
+
+uint64_t build_sell(const DevCsr& g, uint32_t row_lo, uint32_t row_hi, uint32_t np, DevBuf& sell, DevBuf& sdesc,
+                    cudaStream_t s) {
+  const uint32_t nsl = (row_hi - row_lo) / 32u;
+  DevBuf width(((size_t)nsl + 1) * 4, s), soff(((size_t)nsl + 1) * 4, s), hmask(((size_t)nsl + 1) * 4, s), scratch;
+  k_sell_width<<<grid_for((uint64_t)nsl * 32, 256, 8), 256, 0, s>>>(g.n, row_lo, nsl, g.o(), kHeavyDeg,
+                                                                   width.as<uint32_t>(), hmask.as<uint32_t>());
+  CYC_LAUNCHED();
+  exclusive_scan(width.as<uint32_t>(), soff.as<uint32_t>(), nsl, nullptr, s, scratch);
+  uint32_t tot = 0;
+  CYC_CUDA(cudaMemcpyAsync(&tot, soff.as<uint32_t>() + nsl, 4, cudaMemcpyDeviceToHost, s));
+  CYC_CUDA(cudaStreamSynchronize(s));
+  const uint64_t words = (uint64_t)tot * 32u;
+  sell.alloc((words ? words : 1) * 4, s);
+  sdesc.alloc(((size_t)nsl + 1) * sizeof(uint4), s);
+  k_sell_fill<<<grid_for((uint64_t)nsl * 32, 256, 8), 256, 0, s>>>(g.n, row_lo, nsl, np, g.o(), g.c(),
+                                                                  width.as<uint32_t>(), soff.as<uint32_t>(),
+                                                                  hmask.as<uint32_t>(), sell.as<uint32_t>(),
+                                                                  sdesc.as<uint4>());
+  CYC_LAUNCHED();
+  return words;
+}
+
 void permute_bits(const uint32_t* src, const uint32_t* orig, uint32_t n, uint32_t* dst, cudaStream_t s) {
   if (!n) return;
   k_permute_bits<<<grid_for((uint64_t)n, 256, 8), 256, 0, s>>>(src, orig, n, dst);
@@ -338,47 +387,15 @@ bool build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& pla
   plan.orig.alloc(((size_t)np + 1) * 4, s);
   plan.perm.alloc((size_t)n * 4, s);
   DevBuf scratch;
-  exclusive_scan(T.as<uint32_t>(), base.as<uint32_t>(), kBuckets * nw, nullptr, s, scratch);
-  k_plan_place<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, snap.o(), base.as<uint32_t>(), nw,
-                                                  plan.orig.as<uint32_t>(), plan.perm.as<uint32_t>());
-  CYC_LAUNCHED();
-  k_plan_pad<<<grid_for(np + 1 - n, 256, 1), 256, 0, s>>>(n, np + 1, plan.orig.as<uint32_t>());
-  CYC_LAUNCHED();
+  degree_order(snap.o(), n, plan.orig.as<uint32_t>(), plan.perm.as<uint32_t>(), s);
   mark("place");
   relayout(gath, plan.orig.as<uint32_t>(), plan.perm.as<uint32_t>(), plan.gath, scratch, s);
   mark("gath");
   relayout(snap, plan.orig.as<uint32_t>(), plan.perm.as<uint32_t>(), plan.snap, scratch, s);
   mark("snap");
-  const char* cb = std::getenv("CYC_PLAN_COLBLOCKS");
-  build_heavy(plan.gath, kHeavyDeg, kHeavyChunk, s, cb ? (uint32_t)std::atoi(cb) : 1u);
-  plan.n_hchunks = plan.gath.n_heavy_chunks;
-  plan.hcol.alloc(((size_t)plan.n_hchunks * kHeavyChunk + 1) * 4, s);
-  plan.hrow.alloc(((size_t)plan.n_hchunks + 1) * 4, s);
-  if (plan.n_hchunks) {
-    k_hslab_fill<<<grid_for((uint64_t)plan.n_hchunks * 32, 256, 8), 256, 0, s>>>(
-        plan.gath.heavy.as<uint4>(), plan.n_hchunks, plan.gath.c(), np, plan.hcol.as<uint32_t>(),
-        plan.hrow.as<uint32_t>());
-    CYC_LAUNCHED();
-  }
+  build_hslab(plan.gath, np, plan.hcol, plan.hrow, plan.n_hchunks, s);
   mark("heavy");
-  {  // sliced ELL of the light rows (map_run.cu pull_sell)
-    const uint32_t nsl = np / 32u;
-    DevBuf width(((size_t)nsl + 1) * 4, s), soff(((size_t)nsl + 1) * 4, s), hmask(((size_t)nsl + 1) * 4, s);
-    k_sell_width<<<grid_for((uint64_t)nsl * 32, 256, 8), 256, 0, s>>>(n, nsl, plan.gath.o(), kHeavyDeg,
-                                                                     width.as<uint32_t>(), hmask.as<uint32_t>());
-    CYC_LAUNCHED();
-    exclusive_scan(width.as<uint32_t>(), soff.as<uint32_t>(), nsl, nullptr, s, scratch);
-    uint32_t tot = 0;
-    CYC_CUDA(cudaMemcpyAsync(&tot, soff.as<uint32_t>() + nsl, 4, cudaMemcpyDeviceToHost, s));
-    CYC_CUDA(cudaStreamSynchronize(s));
-    plan.sell_words = (uint64_t)tot * 32u;
-    plan.sell.alloc((plan.sell_words ? plan.sell_words : 1) * 4, s);
-    plan.sdesc.alloc((size_t)nsl * sizeof(uint4), s);
-    k_sell_fill<<<grid_for((uint64_t)nsl * 32, 256, 8), 256, 0, s>>>(
-        n, nsl, np, plan.gath.o(), plan.gath.c(), width.as<uint32_t>(), soff.as<uint32_t>(), hmask.as<uint32_t>(),
-        plan.sell.as<uint32_t>(), plan.sdesc.as<uint4>());
-    CYC_LAUNCHED();
-  }
+  plan.sell_words = build_sell(plan.gath, 0, np, np, plan.sell, plan.sdesc, s);  // map_run.cu pull_sell
   mark("sell");
   CYC_CUDA(cudaStreamSynchronize(s));
   plan.build_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();

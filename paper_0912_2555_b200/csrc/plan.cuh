@@ -50,6 +50,16 @@ struct MapPlan {
 // Returns false when the graph's plan for this layout was already built.
 bool build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& plan, cudaStream_t s);
 
+// Storage order by descending key (row lengths of key_off, n+1 offsets):
+// orig[p] = vertex at position p (identity on the padding up to n_pad), perm = inverse.
+void degree_order(const uint32_t* key_off, uint32_t n, uint32_t* orig, uint32_t* perm, cudaStream_t s);
+// Rows of g longer than kHeavyDeg as padded kHeavyChunk-column chunks (+ their rows).
+void build_hslab(DevCsr& g, uint32_t np, DevBuf& hcol, DevBuf& hrow, uint32_t& n_hchunks, cudaStream_t s);
+// Sliced ELL of g's rows [row_lo, row_hi) (multiples of 32) of at most
+// kHeavyDeg edges; returns the slab's words.
+uint64_t build_sell(const DevCsr& g, uint32_t row_lo, uint32_t row_hi, uint32_t np, DevBuf& sell, DevBuf& sdesc,
+                    cudaStream_t s);
+
 // dst bit p = src bit orig[p] for p < n (u32 words, dst has n_words words).
 void permute_bits(const uint32_t* src, const uint32_t* orig, uint32_t n, uint32_t* dst, cudaStream_t s);
 

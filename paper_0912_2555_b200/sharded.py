@@ -347,3 +347,84 @@ class FusedShard:
             self.close()
         except Exception:
             pass
+
+
+class MapShard:
+    """One rank's part of a row-sharded graph (cyc_shard_*, csrc/shard.cu).
+
+    From the whole edge log a rank keeps the gather rows of its edge-balanced
+    row range and the push rows that target them (~1/world of the edges);
+    the map vector is replicated. run_map runs ONE persistent kernel per rank
+    that stores the rows it changes straight into every peer's vector (peer
+    memory over NVLink) and meets the other ranks at a system-scope barrier
+    per step — the exchange is fused into the step, no collective per step.
+    Ranks in separate processes connect with `connect(exchange_handles(...))`;
+    ranks of one process with `MapShard.connect_local` (ranks sharing one GPU
+    run as one grid, for tests)."""
+
+    def __init__(self, ctx, edges, m_log: int, n: int, acc_words, world: int, rank: int,
+                 orientation: int = _abi.CYC_TRANSPOSED, layout: str = "auto"):
+        layouts = {"auto": _abi.CYC_LAYOUT_AUTO, "identity": _abi.CYC_LAYOUT_IDENTITY,
+                   "degree": _abi.CYC_LAYOUT_DEGREE}
+        self.ctx, self.n, self.world, self.rank = ctx, int(n), int(world), int(rank)
+        self.h = C.c_void_p()
+        e = edges if not isinstance(edges, np.ndarray) else np.ascontiguousarray(edges, dtype=np.uint32)
+        a = acc_words if not isinstance(acc_words, np.ndarray) else np.ascontiguousarray(acc_words, np.uint64)
+        _abi.check(_abi.lib().cyc_shard_build(ctx.handle, _abi.ptr(e), int(m_log), int(n), _abi.ptr(a),
+                                              int(orientation), layouts[layout], int(world), int(rank),
+                                              C.byref(self.h)))
+        self._keep = (e, a)
+
+    def info(self):
+        lo, hi, me, by = C.c_uint32(), C.c_uint32(), C.c_uint64(), C.c_uint64()
+        _abi.check(_abi.lib().cyc_shard_info(self.h, C.byref(lo), C.byref(hi), C.byref(me), C.byref(by)))
+        return {"row_lo": lo.value, "row_hi": hi.value, "local_edges": me.value, "device_bytes": by.value}
+
+    def handle(self) -> bytes:
+        buf = (C.c_char * _abi.SHARD_HANDLE_BYTES)()
+        _abi.check(_abi.lib().cyc_shard_handle(self.h, buf))
+        return bytes(buf)
+
+    def connect(self, blob: bytes) -> None:
+        assert len(blob) == self.world * _abi.SHARD_HANDLE_BYTES
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        _abi.check(_abi.lib().cyc_shard_connect(self.h, buf))
+
+    @staticmethod
+    def connect_local(shards) -> None:
+        arr = (C.c_void_p * len(shards))(*[s.h.value for s in shards])
+        _abi.check(_abi.lib().cyc_shard_connect_local(arr, len(shards)))
+
+    @staticmethod
+    def run_map(shards, acc_words=None, early_exit: bool = True, mode: str = "auto", hash_cap: int = 4096,
+                want_values: bool = True):
+        """run_map on the given ranks of this process (one, or all after
+        connect_local) -> api.MapRun of the whole graph."""
+        from .api import MapOptions, MapRun, stats_dict
+
+        arr = (C.c_void_p * len(shards))(*[s.h.value for s in shards])
+        n = shards[0].n
+        st = _abi.MapStatsC()
+        vals = np.zeros(max(n, 1), np.uint32) if want_values else None
+        hh = np.zeros(max(hash_cap, 1), np.uint64)
+        hs = np.zeros(max(hash_cap, 1), np.uint64)
+        a = None if acc_words is None else np.ascontiguousarray(acc_words, np.uint64)
+        opt = MapOptions(early_exit=early_exit, mode=mode).to_c()
+        _abi.check(_abi.lib().cyc_shard_run_map(arr, len(shards), _abi.ptr(a), C.byref(opt), C.byref(st),
+                                                _abi.ptr(vals), _abi.ptr(hh), _abi.ptr(hs), C.c_uint64(hash_cap)))
+        k = min(int(st.iterations), hash_cap)
+        verdict = Verdict.cycle(st.witness) if st.cycle_found else Verdict.no_cycle()
+        stats = MapStats(int(st.iterations), int(st.kernel_calls), int(st.demoted_total),
+                         int(st.witness) if st.cycle_found else None, stats_dict(st))
+        return MapRun(verdict, stats, vals[:n] if vals is not None else None, hh[:k], hs[:k])
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            _abi.lib().cyc_shard_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
