@@ -89,7 +89,8 @@ typedef struct cyc_map_stats {
   uint32_t grid_blocks, block_threads;
   double plan_ms;              /* host time building the storage plan in this call (0: cached) */
   int32_t layout;              /* CYC_LAYOUT_IDENTITY or CYC_LAYOUT_DEGREE: the layout that ran */
-  int32_t reserved;
+  int32_t world;               /* ranks of a sharded run (1: one device) */
+  uint64_t exchanged_rows;     /* sharded: rows every rank stored into each peer, over all steps */
 } cyc_map_stats;
 
 /* ---- context ------------------------------------------------------------ */

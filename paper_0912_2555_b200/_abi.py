@@ -88,7 +88,8 @@ class MapStatsC(C.Structure):
         ("block_threads", C.c_uint32),
         ("plan_ms", C.c_double),
         ("layout", C.c_int32),
-        ("reserved", C.c_int32),
+        ("world", C.c_int32),
+        ("exchanged_rows", C.c_uint64),
     ]
 
 

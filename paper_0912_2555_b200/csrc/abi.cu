@@ -443,6 +443,8 @@ void fill_stats(const cyc::RunOut& o, cyc_map_stats* st) {
   st->block_threads = o.block;
   st->plan_ms = o.plan_ms;
   st->layout = o.layout;
+  st->world = 1;
+  st->exchanged_rows = 0;
 }
 
 cyc_map_options default_opts() {
@@ -1136,7 +1138,11 @@ cyc_status cyc_shard_run_map(cyc_shard* const* shards, int count, const uint64_t
                    o.push_alpha, hcap, ss.data(), nullptr, nullptr, outs.data());
     const cyc::RunOut& r = outs[0];
     fill_stats(r, stats);
-    if (stats) stats->layout = gs[0]->relabel ? CYC_LAYOUT_DEGREE : CYC_LAYOUT_IDENTITY;
+    if (stats) {
+      stats->layout = gs[0]->relabel ? CYC_LAYOUT_DEGREE : CYC_LAYOUT_IDENTITY;
+      stats->world = gs[0]->world;
+      stats->exchanged_rows = r.res[cyc::kResRaised];
+    }
     cyc_ctx* ctx = shards[0]->ctx;
     CYC_CUDA(cudaSetDevice(ctx->device));
     const uint32_t n = gs[0]->n;

@@ -391,7 +391,7 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
     acc.raised += go[r];
     acc.first += first[r];
     acc.fedges += e[r] - b[r];
-    if ((bw[r] >> (tgt[r] & 31u)) & 1u) acc.fedges += enlist(a, tgt[r], c.bc, c.nchunk, c.sh);
+    if (a.world == 1 && ((bw[r] >> (tgt[r] & 31u)) & 1u)) acc.fedges += enlist(a, tgt[r], c.bc, c.nchunk, c.sh);
     if (go[r] && (old[r] & kFlag) && val[r] == oid<RL>(a, tgt[r]) + 1u) add_cand(a, c.Cn, c.ccnt, tgt[r]);
   }
 }
@@ -439,7 +439,7 @@ __device__ __forceinline__ void rows_epilogue(const RunArgs& a, uint32_t base, c
   for (int k = 0; k < R; ++k) big[k] = words[k] ? __ldcg(a.bigm + (base >> 5) + k) & words[k] : 0u;
 #pragma unroll
   for (int k = 0; k < R; ++k)
-    if ((big[k] >> lane) & 1u) acc.fedges += enlist(a, base + 32u * k + lane, bc, &sl->nchunk, sh);
+    if (a.world == 1 && ((big[k] >> lane) & 1u)) acc.fedges += enlist(a, base + 32u * k + lane, bc, &sl->nchunk, sh);
 }
 
 // Light rows of a pull step. Each lane owns R rows (32*R consecutive rows per
@@ -640,7 +640,7 @@ __device__ __forceinline__ void pull_heavy(const RunArgs& a, const uint32_t* __r
         ++acc.raised;
         if (mark(fb, sh, v, PRE)) {
           ++acc.first;
-          if (bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
+          if (a.world == 1 && bit_of(a.bigm, v)) acc.fedges += enlist(a, v, bc, &sl->nchunk, sh);
         }
         if ((own & kFlag) && mine == oid<RL>(a, v) + 1u) add_cand(a, Cn, &sl->cand_cnt, v);
       }
@@ -663,7 +663,7 @@ __device__ __forceinline__ void heavy_flush(const RunArgs& a, bool live, uint32_
     ++acc.raised;
     if (mark(fb, sh, pv, true)) {
       ++acc.first;
-      if (bit_of(a.bigm, pv)) acc.fedges += enlist(a, pv, bc, &sl->nchunk, sh);
+      if (a.world == 1 && bit_of(a.bigm, pv)) acc.fedges += enlist(a, pv, bc, &sl->nchunk, sh);
     }
     if ((po & kFlag) && mine == oid<RL>(a, pv) + 1u) add_cand(a, Cn, &sl->cand_cnt, pv);
   }
@@ -855,9 +855,22 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t gw = gwarp(a);
   const uint32_t nw = nwarps(a);
   StepAcc acc;
+  if (a.world > 1) {
+    // sharded: local raises enlist nothing (other ranks raise most of the
+    // frontier); chunk every big vertex of the replicated frontier over this
+    // rank's push rows, then start pushing once every block has listed its part
+    SlotCtl* plw = &a.ctl->slot[(g - 1u) % 3u];
+    uint4* bpw = a.BC[(g - 1u) & 1u];
+    for (uint32_t wi = gw; wi < a.nwords; wi += nw) {
+      const uint32_t word = __ldcg(fp + wi) & __ldcg(a.bigm + wi);
+      if ((word >> lane) & 1u) enlist(a, wi * 32u + lane, bpw, &plw->nchunk, sh);
+    }
+    big_flush(a, sh, bpw, &plw->nchunk);
+    cg::this_grid().sync();
+  }
   // big frontier vertices first: one warp per kChunk-edge chunk, each lane
   // raising kChunk/32 targets as one batch
-  const uint32_t nch = min(__ldca(&pl->nchunk), a.chunk_cap);
+  const uint32_t nch = min(__ldcg(&pl->nchunk), a.chunk_cap);
   for (uint32_t k = gw; k < nch; k += nw) {
     const uint4 ch = bp[k];
     const uint32_t vv = cand_of<RL>(a, __ldca(c.Pc + ch.x), ch.x);
@@ -1040,7 +1053,7 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, uint64_t t, BlockSh* sh
         a.P[1][v] = val;
         if (accv) {
           vm = max(vm, oid<RL>(a, v) + 1u);
-          if (bit_of(a.bigm, v)) {
+          if (a.world == 1 && bit_of(a.bigm, v)) {
             fe += enlist(a, v, bc, &sl->nchunk, sh);
           } else {
             fe += __ldg(a.poff + v + 1) - __ldg(a.poff + v);
@@ -1159,7 +1172,7 @@ template <bool RL, bool SH>
 __device__ __forceinline__ void map_run_body(const RunArgs& a) {
   __shared__ BlockSh sh;
   // run statistics live in shared memory of block 0 (kept out of registers)
-  __shared__ unsigned long long stat[kResBars + 1];
+  __shared__ unsigned long long stat[kResRaised + 1];
   cg::grid_group grid = cg::this_grid();
   RunCtl* ctl = a.ctl;
   uint32_t g = 1;
@@ -1168,7 +1181,7 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
   uint32_t witness = kNone;
   const bool lead = vblk(a) == 0 && threadIdx.x == 0;
   if (lead)
-    for (int k = 0; k <= kResBars; ++k) stat[k] = 0;
+    for (int k = 0; k <= kResRaised; ++k) stat[k] = 0;
   if (threadIdx.x == 0) {
     sh.wl_n = 0;
     sh.big_n = 0;
@@ -1187,7 +1200,7 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
   unsigned long long bars = a.bar_base;
   // sharded: global push degree of F (each rank counts its own push rows)
   unsigned long long g_fe = 0, g_nr = 0;
-  if constexpr (SH) g_fe = exchange_step(a, grid, g, 0, &ctl->slot[g % 3u], kNone, false, bars).fedges;
+  if (SH && a.world > 1) g_fe = exchange_step(a, grid, g, 0, &ctl->slot[g % 3u], kNone, false, bars).fedges;
   uint64_t t = 0;
   uint32_t vmax = __ldcg(&ctl->it_vmax[0]);
   bool truncated = false;
@@ -1202,8 +1215,9 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
         if (lead) reset_slot(ctl, (g + 1u) % 3u);
         int mode = a.mode;
         // the previous step's (global) frontier size
-        const unsigned long long p_fe = SH ? g_fe : __ldca(&ctl->slot[pslot].fedges);
-        const unsigned long long p_nr = SH ? g_nr : __ldca(&ctl->slot[pslot].nraised);
+        const bool xch = SH && a.world > 1;  // records come from the exchange
+        const unsigned long long p_fe = xch ? g_fe : __ldca(&ctl->slot[pslot].fedges);
+        const unsigned long long p_nr = xch ? g_nr : __ldca(&ctl->slot[pslot].nraised);
         if (mode != kModePull && mode != kModePush) {
           unsigned long long est;
           if (prev_push) {
@@ -1266,12 +1280,13 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
           }
           w = min(w, block_min(mine, &sh));
         }
-        if constexpr (SH) {  // every rank gets the others' changed rows and the global record
+        if (SH && a.world > 1) {  // every rank gets the others' changed rows and the global record
           const ShardRec gr = exchange_step(a, grid, g, cur, sl, w, true, bars);
           changed = gr.changed;
           w = gr.wit;
           g_fe = gr.fedges;
           g_nr = gr.nraised;
+          CYC_STAT(kResRaised, g_nr);  // rows stored into every peer this step
         }
         if (a.early_exit && w != kNone) {
           cycle = 1;
@@ -1319,7 +1334,7 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
       reset_pass<RL>(a, g, t, &sh);
       cur = 0;
       grid.sync();
-      if constexpr (SH) g_fe = exchange_step(a, grid, g, 0, &ctl->slot[g % 3u], kNone, false, bars).fedges;
+      if (SH && a.world > 1) g_fe = exchange_step(a, grid, g, 0, &ctl->slot[g % 3u], kNone, false, bars).fedges;
       vmax = __ldcg(&ctl->it_vmax[t & 1u]);
     }
   }
@@ -1329,7 +1344,7 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
     stat[kResCur] = (unsigned long long)cur;
     stat[kResTag] = g;
     stat[kResBars] = bars;
-    for (int k = 0; k <= kResBars; ++k) ctl->res[k] = stat[k];
+    for (int k = 0; k <= kResRaised; ++k) ctl->res[k] = stat[k];
   }
 #undef CYC_STAT
 }

@@ -37,7 +37,7 @@ struct RunCtl {
 
 enum RunRes {
   kResCycle = 0, kResWitness, kResIterations, kResKernelCalls, kResDemoted, kResStepsLast,
-  kResPullSteps, kResPushSteps, kResEdges, kResRows, kResBytes, kResCur, kResTag, kResBars
+  kResPullSteps, kResPushSteps, kResEdges, kResRows, kResBytes, kResCur, kResTag, kResBars, kResRaised
 };
 
 // Row-sharded runs (world > 1, shard.cu): every rank keeps the whole map vector
@@ -150,7 +150,7 @@ struct ShardRunIn {
   RunWs* ws;
   uint32_t* P[2];
   uint32_t* FB[2];
-  const uint32_t* bigm;  // all-zero: no big-vertex chunk lists in sharded runs
+  const uint32_t* bigm;  // push degree > kBigDeg over this rank's push rows
   uint32_t n;
   uint64_t m_global;
   int world, rank;

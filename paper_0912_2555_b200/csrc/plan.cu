@@ -256,7 +256,10 @@ __global__ void k_permute_bits(const uint32_t* __restrict__ src, const uint32_t*
   }
 }
 
-// One CSR in storage order (rows and columns relabelled).
+}  // namespace
+
+// One CSR in storage order (rows and columns relabelled); rows longer than
+// in.heavy_deg come from in's heavy-chunk list.
 void relayout(const DevCsr& in, const uint32_t* orig, const uint32_t* perm, DevCsr& out, DevBuf& scratch,
               cudaStream_t s) {
   const uint32_t n = in.n;
@@ -278,8 +281,6 @@ void relayout(const DevCsr& in, const uint32_t* orig, const uint32_t* perm, DevC
     CYC_LAUNCHED();
   }
 }
-
-}  // namespace
 
 void degree_order(const uint32_t* key_off, uint32_t n, uint32_t* orig, uint32_t* perm, cudaStream_t s) {
   const uint32_t nw = (uint32_t)sm_count() * kPlanWarps;

@@ -17,6 +17,9 @@
 // Per-rank edge memory is ~1/world of the graph; the map vector and frontier
 // bitmaps (O(n)) are replicated.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "plan.cuh"
@@ -63,8 +66,9 @@ __global__ void k_shard_bounds(const uint32_t* __restrict__ pre, uint32_t n, int
   bounds[r] = lo;
 }
 
-// Edges whose gather row (in storage order) is in [lo, hi), relabelled, as
-// (gather row, gather column) pairs. PASS 0 counts, PASS 1 writes.
+// Edges whose gather row (in storage order) is in [lo, hi), as (gather row,
+// gather column) pairs in VERTEX ids (K1's buckets balance on the id order;
+// in degree order the first bucket would hold the hubs). PASS 0 counts, PASS 1 writes.
 template <int PASS>
 __global__ void k_shard_filter(const uint2* __restrict__ e, uint64_t m, int transposed,
                                const uint32_t* __restrict__ perm, uint32_t lo, uint32_t hi,
@@ -78,12 +82,9 @@ __global__ void k_shard_filter(const uint2* __restrict__ e, uint64_t m, int tran
     uint2 y = make_uint2(0u, 0u);
     if (i < m) {
       const uint2 x = e[i];
-      uint32_t r = transposed ? x.x : x.y, c = transposed ? x.y : x.x;
-      if (perm) {
-        r = __ldg(perm + r);
-        c = __ldg(perm + c);
-      }
-      keep = r >= lo && r < hi;
+      const uint32_t r = transposed ? x.x : x.y, c = transposed ? x.y : x.x;
+      const uint32_t pr = perm ? __ldg(perm + r) : r;
+      keep = pr >= lo && pr < hi;
       y = make_uint2(r, c);
     }
     const uint32_t bal = __ballot_sync(kFull, keep);
@@ -137,6 +138,16 @@ void build_shard(const uint32_t* d_edges, uint64_t m_log, uint32_t n, const uint
   if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
     throw Error(CYC_E_CONTRACT, "shard: bad world/rank");
   CYC_CUDA(cudaGetDevice(&sh.device));
+  const bool dbg = std::getenv("CYC_DEBUG_TIMING") != nullptr;
+  auto tm = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {  // CYC_DEBUG_TIMING=1: host-observed phase times
+    if (!dbg) return;
+    CYC_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cyc shard %d/%d] %-10s %8.3f ms\n", rank, world, what,
+                 std::chrono::duration<double, std::milli>(now - tm).count());
+    tm = now;
+  };
   const int transposed = orientation == CYC_TRANSPOSED;
   const uint2* e2 = reinterpret_cast<const uint2*>(d_edges);
   sh.n = n;
@@ -157,6 +168,7 @@ void build_shard(const uint32_t* d_edges, uint64_t m_log, uint32_t n, const uint
   CYC_CUDA(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, s));
   CYC_CUDA(cudaStreamSynchronize(s));
   if (herr) throw Error(CYC_E_CONTRACT, "build_snapshot: edge endpoint >= n (not interned)");
+  mark("counts");
   // storage order (degree layout: descending gather frequency of the log)
   const bool degree = layout == 2 || (layout == 0 && (uint64_t)n * 4 > (40ull << 20));
   sh.relabel = degree && n >= 64;
@@ -188,6 +200,7 @@ void build_shard(const uint32_t* d_edges, uint64_t m_log, uint32_t n, const uint
   }
   sh.row_lo = bounds[rank];
   sh.row_hi = bounds[rank + 1];
+  mark("order");
   // this rank's edges, relabelled
   DevBuf cnt(16, s);
   CYC_CUDA(cudaMemsetAsync(cnt.p, 0, 16, s));
@@ -207,20 +220,35 @@ void build_shard(const uint32_t* d_edges, uint64_t m_log, uint32_t n, const uint
                                                               cnt.as<unsigned long long>(), pairs.as<uint2>());
     CYC_LAUNCHED();
   }
+  mark("filter");
   // gather rows keyed by the pair's first element, push rows by its second
-  build_csr(pairs.as<uint32_t>(), mine, n, 0, s, sh.gath, err.as<uint32_t>(), ar);
-  build_csr(pairs.as<uint32_t>(), mine, n, 1, s, sh.push, err.as<uint32_t>(), ar);
-  pairs = DevBuf();
+  // (vertex ids), then both relabelled to the storage order
+  if (sh.relabel) {
+    DevCsr g0, p0;
+    build_csr(pairs.as<uint32_t>(), mine, n, 0, s, g0, err.as<uint32_t>(), ar);
+    build_csr(pairs.as<uint32_t>(), mine, n, 1, s, p0, err.as<uint32_t>(), ar);
+    mark("csrs");
+    pairs = DevBuf();
+    build_heavy(g0, kHeavyDeg, kHeavyChunk, s, 1u);
+    build_heavy(p0, kHeavyDeg, kHeavyChunk, s, 1u);
+    relayout(g0, sh.orig.as<uint32_t>(), sh.perm.as<uint32_t>(), sh.gath, scratch, s);
+    relayout(p0, sh.orig.as<uint32_t>(), sh.perm.as<uint32_t>(), sh.push, scratch, s);
+    mark("relayout");
+  } else {
+    build_csr(pairs.as<uint32_t>(), mine, n, 0, s, sh.gath, err.as<uint32_t>(), ar);
+    build_csr(pairs.as<uint32_t>(), mine, n, 1, s, sh.push, err.as<uint32_t>(), ar);
+    mark("csrs");
+    pairs = DevBuf();
+  }
   sh.m_local = sh.gath.m;
   build_hslab(sh.gath, np, sh.hcol, sh.hrow, sh.n_hchunks, s);
   sh.sell_words = build_sell(sh.gath, sh.row_lo, sh.row_hi, np, sh.sell, sh.sdesc, s);
+  mark("slabs");
   // accepting words (vertex-id order), the workspace and the exchange buffers
   sh.acc.alloc((((size_t)n + 63) / 64 + 1) * 8, s);
   CYC_CUDA(cudaMemsetAsync(sh.acc.p, 0, sh.acc.bytes, s));
   if (acc_words && n) CYC_CUDA(cudaMemcpyAsync(sh.acc.p, acc_words, ((size_t)n + 63) / 64 * 8, cudaMemcpyDefault, s));
   sh.ws.ensure(n, sh.gath.m, sh.push.o(), s);
-  sh.zero_bigm.alloc(((size_t)np / 32 + 2) * 4, s);
-  CYC_CUDA(cudaMemsetAsync(sh.zero_bigm.p, 0, sh.zero_bigm.bytes, s));
   CYC_CUDA(cudaStreamSynchronize(s));
   for (int b = 0; b < 2; ++b) {
     sh.xP[b] = static_cast<uint32_t*>(xalloc(((size_t)np + 1) * 4));
@@ -228,6 +256,7 @@ void build_shard(const uint32_t* d_edges, uint64_t m_log, uint32_t n, const uint
   }
   sh.rec = static_cast<ShardRec*>(xalloc(sizeof(ShardRec) * 2 * kMaxWorld));
   sh.bar = static_cast<unsigned long long*>(xalloc(64));
+  mark("buffers");
   // the global snapshot edge count: every rank's rows are disjoint, so
   // m_global = sum over ranks; a rank alone knows only its own. Ranks agree
   // on it when connected (shard_connect_*); until then it is the local one.
@@ -356,7 +385,7 @@ void shard_run(ShardGraph* const* shards, int k, const uint64_t* acc_words, int 
       r.P[b] = sh.xP[b];
       r.FB[b] = sh.xFB[b];
     }
-    r.bigm = sh.zero_bigm.as<uint32_t>();
+    r.bigm = sh.ws.bigm.as<uint32_t>();  // push degree > kBigDeg over this rank's push rows
     r.n = sh.n;
     r.m_global = sh.m_global;
     r.world = sh.world;

@@ -28,7 +28,6 @@ struct ShardGraph {
   uint64_t sell_words = 0;
   DevBuf acc;              // accepting words (u64) in vertex-id order
   RunWs ws;
-  DevBuf zero_bigm;        // sharded push steps expand every vertex lane by lane
   // exchange buffers (cudaMalloc): map words [2], frontier bitmaps [2], records, barrier
   uint32_t* xP[2] = {nullptr, nullptr};
   uint32_t* xFB[2] = {nullptr, nullptr};
