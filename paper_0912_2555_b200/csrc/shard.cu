@@ -169,15 +169,33 @@ void build_shard(const uint32_t* d_edges, uint64_t m_log, uint32_t n, const uint
   CYC_CUDA(cudaStreamSynchronize(s));
   if (herr) throw Error(CYC_E_CONTRACT, "build_snapshot: edge endpoint >= n (not interned)");
   mark("counts");
-  // storage order (degree layout: descending gather frequency of the log)
-  const bool degree = layout == 2 || (layout == 0 && (uint64_t)n * 4 > (40ull << 20));
-  sh.relabel = degree && n >= 64;
-  if (sh.relabel) {
+  // storage order (degree layout: descending gather frequency of the log);
+  // auto as plan.cu: a map vector beyond ~40 MB whose n/8 most-gathered
+  // vertices take at least half of the gathers
+  const bool want = n >= 64 && (layout == 2 || (layout == 0 && (uint64_t)n * 4 > (40ull << 20)));
+  if (want) {
     DevBuf koff(((size_t)n + 1) * 4, s);
     exclusive_scan(gcol.as<uint32_t>(), koff.as<uint32_t>(), n, nullptr, s, scratch);
     sh.orig.alloc(((size_t)np + 1) * 4, s);
     sh.perm.alloc((size_t)n * 4, s);
     degree_order(koff.as<uint32_t>(), n, sh.orig.as<uint32_t>(), sh.perm.as<uint32_t>(), s);
+    sh.relabel = true;
+    if (layout == 0) {
+      DevBuf hl(((size_t)n + 1) * 4, s), hp(((size_t)n + 1) * 4, s);
+      k_shard_rowlen<<<grid_for(n, 256, 8), 256, 0, s>>>(n, sh.orig.as<uint32_t>(), gcol.as<uint32_t>(),
+                                                         hl.as<uint32_t>());
+      CYC_LAUNCHED();
+      exclusive_scan(hl.as<uint32_t>(), hp.as<uint32_t>(), n, nullptr, s, scratch);
+      uint32_t hot = 0, all = 0;
+      CYC_CUDA(cudaMemcpyAsync(&hot, hp.as<uint32_t>() + n / 8, 4, cudaMemcpyDeviceToHost, s));
+      CYC_CUDA(cudaMemcpyAsync(&all, hp.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+      CYC_CUDA(cudaStreamSynchronize(s));
+      if ((double)hot < 0.5 * (double)all) {
+        sh.relabel = false;
+        sh.orig = DevBuf();
+        sh.perm = DevBuf();
+      }
+    }
   }
   // edge-balanced row ranges (every rank computes the same ones)
   std::vector<uint32_t> bounds(world + 1);
