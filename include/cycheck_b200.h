@@ -272,6 +272,9 @@ cyc_status cyc_host_alloc(size_t bytes, void** out);      /* pinned */
 void cyc_host_free(void* p);
 cyc_status cyc_device_alloc(cyc_ctx* ctx, size_t bytes, void** out);
 void cyc_device_free(cyc_ctx* ctx, void* p);
+/* Copy ordered on the context's stream, returns without waiting (pair with
+ * cyc_ctx_synchronize); either side may be host (pinned for overlap) or device. */
+cyc_status cyc_memcpy_async(cyc_ctx* ctx, void* dst, const void* src, size_t bytes);
 cyc_status cyc_memcpy(cyc_ctx* ctx, void* dst, const void* src, size_t bytes);
 /* Writes `bytes` of a scratch buffer to evict L2 (timing hygiene). */
 cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes);

@@ -7,20 +7,85 @@
 // from build_snapshot, the same restriction. Runs on a GPU box (the binary is
 // prebuilt into oracle/_ref/ and shipped); exits non-zero on any mismatch.
 #include <algorithm>
-#include <cstdio>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <random>
+#include <thread>
 
 #include "cycheck/graph.hpp"
 #include "cycheck/map_engine.hpp"
 #include "cycheck/oracle.hpp"
 #include "cycheck/owcty.hpp"
 #include "../include/cycheck_b200.hpp"
+#include "../include/cyc_gen.h"
 
 using namespace cycheck;
 
+// `dropin_test time <scale>`: the cycheck_main.cpp:88-97 path (build_snapshot
+// from the reference's EdgeLog + run_map) through the drop-in, timed against
+// cyc_check from a contiguous pinned copy of the same log (R-MAT, config 3's
+// generator at the given scale). Prints one JSON line.
+static int time_dropin(int scale) {
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
+  cyc_gen_params p;
+  cyc_gen_config(&p, 3);
+  p.scale = (uint32_t)scale;
+  cyc_gen_init(&p);
+  b200::Engine gpu(0);
+  EdgeLog log({p.n, p.m});
+  auto t0 = clk::now();
+  for (uint32_t v = 0; v < p.n; ++v) log.add_vertex(cyc_gen_accepting(&p, v) != 0);
+  for (uint64_t i = 0; i < p.m; ++i) {
+    uint32_t s, d;
+    cyc_gen_edge(&p, i, &s, &d);
+    log.append_edge(s, d);
+  }
+  const double fill_ms = ms(t0);
+  // contiguous pinned copy of the same edges
+  void* pin = nullptr;
+  b200::check(cyc_host_alloc(p.m * 8, &pin));
+  for (uint64_t i = 0; i < p.m; ++i) {
+    auto e = log.edge(i);
+    static_cast<uint32_t*>(pin)[2 * i] = e.first;
+    static_cast<uint32_t*>(pin)[2 * i + 1] = e.second;
+  }
+  const Bitset acc = log.accepting_prefix(p.n);
+  double best_drop = 1e30, best_pin = 1e30, csr_ms = 0, kernel_ms = 0;
+  bool same = true;
+  for (int rep = 0; rep < 3; ++rep) {
+    auto tb = clk::now();
+    auto snap = b200::build_snapshot(gpu, log, Orientation::transposed);
+    const double c = ms(tb);
+    auto tk = clk::now();
+    auto [v, st] = b200::run_map<Verdict, MapStats>(snap, log.accepting_prefix(snap.n()), MapOptions{});
+    const double k = ms(tk);
+    if (c + k < best_drop) {
+      best_drop = c + k;
+      csr_ms = c;
+      kernel_ms = k;
+    }
+    cyc_map_options o{};
+    o.early_exit = 1;
+    cyc_map_stats cs{};
+    auto tp = clk::now();
+    b200::check(cyc_check(gpu.get(), static_cast<const uint32_t*>(pin), p.m, p.n, acc.words().data(),
+                          CYC_TRANSPOSED, 0, &o, &cs, nullptr));
+    best_pin = std::min(best_pin, ms(tp));
+    same = same && cs.cycle_found == (int)v.cycle_found() && cs.kernel_calls == st.kernel_calls;
+  }
+  cyc_host_free(pin);
+  std::printf("{\"scale\": %d, \"m_log\": %llu, \"log_fill_ms\": %.1f, \"dropin_ms\": %.2f, \"csr_ms\": %.2f, "
+              "\"kernel_ms\": %.2f, \"pinned_cyc_check_ms\": %.2f, \"ratio\": %.3f, \"same_verdict\": %s}\n",
+              scale, (unsigned long long)p.m, fill_ms, best_drop, csr_ms, kernel_ms, best_pin, best_drop / best_pin,
+              same ? "true" : "false");
+  return same ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 2 && std::strcmp(argv[1], "time") == 0) return time_dropin(std::atoi(argv[2]));
   const int trials = argc > 1 ? std::atoi(argv[1]) : 200;
   b200::Engine gpu(0);
   std::mt19937_64 rng(0x0912255);

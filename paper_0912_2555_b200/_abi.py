@@ -167,6 +167,7 @@ _SIGS = {
     "cyc_device_alloc": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
     "cyc_device_free": (None, [_P, _P]),
     "cyc_memcpy": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "cyc_memcpy_async": (C.c_int, [_P, _P, _P, C.c_size_t]),
     "cyc_flush_l2": (C.c_int, [_P, C.c_size_t]),
     "cyc_shard_bounds": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
     "cyc_map_trace": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),

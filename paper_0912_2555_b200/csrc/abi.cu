@@ -1258,6 +1258,13 @@ cyc_status cyc_memcpy(cyc_ctx* ctx, void* dst, const void* src, size_t bytes) {
   });
 }
 
+cyc_status cyc_memcpy_async(cyc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    require(ctx, CYC_E_CONTRACT, "null ctx");
+    CYC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->s));
+  });
+}
+
 cyc_status cyc_flush_l2(cyc_ctx* ctx, size_t bytes) {
   return guard([&] {
     require(ctx, CYC_E_CONTRACT, "null ctx");

@@ -71,8 +71,24 @@ constexpr int kHeavyBatch = 4;                     // heavy chunks in flight per
 // than L2 and read once per step: load them evict-first so they do not push
 // the hot map words out (ld.global.cs). The identity layout's HYB slab is not
 // hinted: on L2-resident graphs (config 2) it is re-read by every step.
-__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+#ifdef CYC_STREAM_NA  // no L1 allocation, L2 evict-first policy
+  uint32_t v;
+  asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+               "ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], pol;\n\t}"
+               : "=r"(v) : "l"(p));
+  return v;
+#else
+  return __ldcs(p);
+#endif
+}
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
+
+// A map word of the frozen buffer at a gathered position, L1-allocating:
+// measured on config 3, letting the colder positions bypass L1
+// (ld.global.nc.L1::no_allocate) doubles a run (21.2 -> 45.1 ms) — random
+// gathers need the L1 allocation path.
+__device__ __forceinline__ uint32_t ld_gather(const uint32_t* __restrict__ P, uint32_t u) { return __ldca(P + u); }
 
 // Frontier filter of a pull step on a degree-ordered plan. Step k's pull
 // only needs the sources that changed in step k-1: x_{k-1}[v] already
@@ -98,7 +114,7 @@ __device__ __forceinline__ uint32_t ld_word(const Hot& h, const uint32_t* __rest
   bool need = true;
   if (u < h.k) need = (hot_sh[u >> 5] >> (u & 31u)) & 1u;
   uint32_t w = 0;  // NIL: contributes nothing to the maximum
-  if (need) w = __ldca(P + u);
+  if (need) w = ld_gather(P, u);
   return w;
 }
 

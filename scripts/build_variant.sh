@@ -5,7 +5,7 @@ set -e
 cd "$(dirname "$0")/../paper_0912_2555_b200/csrc"
 name=$1; shift
 out=../_lib/variants/$name; mkdir -p $out
-for f in abi build map_run plan scc owcty gen extend ingest fused; do
+for f in $(sed -n "s/^SRCS := //p" Makefile | sed "s/\.cu//g"); do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr "$@" -c $f.cu -o $out/$f.o &
 done
 wait
