@@ -252,6 +252,65 @@ std::pair<VerdictT, StatsT> run_map(const Snapshot& s, const BitsetT& accepting,
   return {VerdictT::no_cycle(), stats};
 }
 
+// Row-sharded run_map over several GPUs of this process: one
+// Engine per device, each rank keeps ~1/N of the snapshot's edges; results
+// equal run_map on one device. Engines on the same device run their ranks as
+// one grid (tests on one GPU).
+class ShardedGraph {
+ public:
+  template <class EdgeLogT, class OrientationT>
+  ShardedGraph(const std::vector<Engine>& engines, const EdgeLogT& log, OrientationT orientation, uint64_t m,
+               uint32_t n, int layout = CYC_LAYOUT_AUTO)
+      : n_(n) {
+    const int world = static_cast<int>(engines.size());
+    if (world < 1) throw DefaultContractError("ShardedGraph: no engines");
+    auto acc = log.accepting_prefix(n);
+    for (int r = 0; r < world; ++r) {
+      DeviceLog dl(engines[r], log, 0, m);
+      cyc_shard* s = nullptr;
+      check(cyc_shard_build(engines[r].get(), dl.data(), m, n, acc.words().data(), orientation_code(orientation),
+                            layout, world, r, &s));
+      shards_.emplace_back(s, &cyc_shard_destroy);
+      engines_.push_back(engines[r]);
+    }
+    std::vector<cyc_shard*> raw;
+    for (auto& s : shards_) raw.push_back(s.get());
+    check(cyc_shard_connect_local(raw.data(), world));
+  }
+  uint32_t n() const { return n_; }
+  // edges held by rank r
+  uint64_t local_edges(int r) const {
+    uint64_t e = 0;
+    check(cyc_shard_info(shards_.at(r).get(), nullptr, nullptr, &e, nullptr));
+    return e;
+  }
+  template <class VerdictT, class StatsT, class BitsetT, class OptionsT>
+  std::pair<VerdictT, StatsT> run_map(const BitsetT& accepting, const OptionsT& opt) const {
+    if (accepting.size() != n_) throw DefaultContractError("run_map: accepting set size mismatch");
+    std::vector<cyc_shard*> raw;
+    for (auto& s : shards_) raw.push_back(s.get());
+    cyc_map_options o{};
+    o.early_exit = opt.early_exit ? 1 : 0;
+    cyc_map_stats st{};
+    check(cyc_shard_run_map(raw.data(), static_cast<int>(raw.size()), accepting.words().data(), &o, &st, nullptr,
+                            nullptr, nullptr, 0));
+    StatsT stats;
+    stats.iterations = st.iterations;
+    stats.kernel_calls = st.kernel_calls;
+    stats.demoted_total = st.demoted_total;
+    if (st.cycle_found) {
+      stats.cycle_witness = st.witness;
+      return {VerdictT::cycle(st.witness), stats};
+    }
+    return {VerdictT::no_cycle(), stats};
+  }
+
+ private:
+  uint32_t n_ = 0;
+  std::vector<Engine> engines_;
+  std::vector<std::shared_ptr<cyc_shard>> shards_;
+};
+
 // fixpoint — map_engine.hpp:86-87; fills values with map codes (id+1, 0 NIL).
 template <class BitsetT, class OptionsT>
 uint64_t fixpoint(const Snapshot& s, const BitsetT& accepting, const OptionsT& opt,

@@ -151,6 +151,22 @@ int main(int argc, char** argv) {
         }
       }
       if (std::getenv("DROPIN_TRACE")) std::fprintf(stderr, "  run_map done\n");
+      // explore.cpp-style caller on a row-sharded graph (ranks emulated on this GPU)
+      if (t % 8 == 0) {
+        std::vector<b200::Engine> engines = {gpu, gpu, gpu};
+        b200::ShardedGraph sg(engines, log, o, m, n);
+        for (bool early : {true, false}) {
+          MapOptions mo;
+          mo.early_exit = early;
+          auto [rv, rs] = run_map(ref, ref.accepting, mo);
+          auto [sv, ss] = sg.run_map<Verdict, MapStats>(ref.accepting, mo);
+          if (!(sv == rv) || ss.iterations != rs.iterations || ss.kernel_calls != rs.kernel_calls ||
+              ss.demoted_total != rs.demoted_total) {
+            std::printf("trial %d: sharded run_map differs\n", t);
+            ++bad;
+          }
+        }
+      }
       // OWCTY and the SCC verdict through the drop-in (owcty.hpp, oracle.hpp)
       auto [ov, os] = run_owcty(ref, ref.accepting);
       auto [gov, gos] = b200::run_owcty<Verdict, OwctyStats>(dev, ref.accepting);

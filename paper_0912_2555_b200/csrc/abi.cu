@@ -229,17 +229,22 @@ struct CallTrace {
   }
 };
 
-// One library call at a time per process. Threads with their own contexts
-// (the explorer's detector and final round) each run persistent grids that
-// spin at grid barriers; interleaved with each other's kernels they hung
-// about one run in ten of tests/test_gpu_concurrency.py even with the grids
-// ordered by coop_launch. Calls stay re-entrant per context and results are
-// unchanged; concurrent callers queue on the host instead.
+// Calls from different contexts run concurrently (one call in flight per
+// context is the contract). Round 1 serialised every call behind one
+// process-wide lock to stop an intermittent hang of threads with their own
+// contexts; its cause was a race in the frontier engine's solo mode (a block
+// could read a level length that CTA 0 had already rewritten, frontier.cuh),
+// fixed in round 2. CYC_SERIALIZE=1 restores the lock (diagnostics).
 std::recursive_mutex g_api_mu;
+const bool g_serialize = [] {
+  const char* e = std::getenv("CYC_SERIALIZE");
+  return e && e[0] == '1';
+}();
 
 template <class F>
 cyc_status guard(F&& f) {
-  std::lock_guard<std::recursive_mutex> api_lock(g_api_mu);
+  std::unique_lock<std::recursive_mutex> api_lock(g_api_mu, std::defer_lock);
+  if (g_serialize) api_lock.lock();
   try {
     f();
     return CYC_OK;

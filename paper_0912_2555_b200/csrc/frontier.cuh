@@ -202,6 +202,12 @@ __global__ void __launch_bounds__(kFrontierThreads) k_frontier(const uint32_t* _
       return;
     }
     if (len <= kSoloEnter && solo_ok) {
+      // every block has read this level's length before CTA 0 rewrites the
+      // counters: without this barrier a block still on its way here could
+      // read the count solo left behind (a later level's, same slot mod 3)
+      // and take the grid branch alone — the intermittent hang of round 1
+      // (~1 in 1800 restrictions; dropin_test, test_gpu_concurrency)
+      grid.sync();
       if (blockIdx.x == 0) solo_levels(off, col, fb, op, L, len);
       grid.sync();
       const uint32_t L2 = __ldcg(fb.cnt + 7);
