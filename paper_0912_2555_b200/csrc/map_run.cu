@@ -259,12 +259,12 @@ struct StepAcc {
 
 // One fused 3-value reduction, one flag store and two atomics per CTA, then
 // the CTA's frontier-word list is flushed.
-__device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc,
-                                        unsigned int* nchunk);
+__device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc, SlotCtl* sl,
+                                        bool flag_overflow);
 __device__ void step_flags(const RunArgs& a, const StepAcc& acc, SlotCtl* sl, BlockSh* sh,
                            uint32_t* wl, uint32_t wl_cap, uint4* bc) {
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const unsigned long long bigdeg = big_flush(a, sh, bc, &sl->nchunk);
+  const unsigned long long bigdeg = big_flush(a, sh, bc, sl, true);
   const unsigned long long r = warp_sum64(acc.raised), f = warp_sum64(acc.first),
                            e = warp_sum64(acc.fedges) + (threadIdx.x == 0 ? bigdeg : 0ull);
   if (lane == 0) {
@@ -305,7 +305,7 @@ __device__ __forceinline__ bool mark(uint32_t* fb, BlockSh* sh, uint32_t v, bool
 __device__ uint32_t enlist_now(const RunArgs& a, uint32_t v, uint4* bc, unsigned int* nchunk) {
   const uint32_t b = __ldg(a.poff + v), e = __ldg(a.poff + v + 1);
   const uint32_t nc = (e - b + kChunk - 1) / kChunk;
-  const uint32_t base = atomicAdd(nchunk, nc);
+  const uint32_t base = atomicAdd(nchunk, nc) & ~kChunkOver;
   for (uint32_t c = 0; c < nc && base + c < a.chunk_cap; ++c)
     bc[base + c] = make_uint4(v, b + c * kChunk, min(e, b + (c + 1) * kChunk), 0u);
   return e - b;
@@ -313,10 +313,25 @@ __device__ uint32_t enlist_now(const RunArgs& a, uint32_t v, uint4* bc, unsigned
 
 // A big-degree vertex entered the next frontier: note it in the CTA's list;
 // the whole CTA writes its chunk descriptors at step end (big_flush), so no
-// single lane serialises hundreds of stores. Returns the degree if it had to
-// be expanded here (list full), else 0 (big_flush accounts it).
+// single lane serialises hundreds of stores. When the list is full the
+// vertex is left out and big_flush flags the step (chunk_over): a following
+// push step re-chunks the whole frontier, and a following pull step — what
+// large frontiers lead to — needs no chunks at all (config 3's first push
+// step spent most of its 2.7 ms in one-lane fallback expansions). Returns the
+// degree if it was not queued, else 0 (big_flush accounts it).
 __device__ __forceinline__ uint32_t enlist(const RunArgs& a, uint32_t v, uint4* bc,
                                            unsigned int* nchunk, BlockSh* sh) {
+  const uint32_t pos = atomicAdd(&sh->big_n, 1u);
+  if (pos < kBigCap) {
+    sh->bigv[pos] = v;
+    return 0u;
+  }
+  return __ldg(a.poff + v + 1) - __ldg(a.poff + v);
+}
+
+// Same, expanding here when the list is full (re-chunking passes).
+__device__ __forceinline__ uint32_t enlist_all(const RunArgs& a, uint32_t v, uint4* bc,
+                                               unsigned int* nchunk, BlockSh* sh) {
   const uint32_t pos = atomicAdd(&sh->big_n, 1u);
   if (pos < kBigCap) {
     sh->bigv[pos] = v;
@@ -327,9 +342,13 @@ __device__ __forceinline__ uint32_t enlist(const RunArgs& a, uint32_t v, uint4* 
 
 // Expands the CTA's noted big vertices into chunks (whole CTA); returns the
 // sum of their degrees in thread 0.
-__device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc,
-                                        unsigned int* nchunk) {
+__device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc, SlotCtl* sl,
+                                        bool flag_overflow = true) {
+  unsigned int* nchunk = &sl->nchunk;
   __syncthreads();
+  // the list overflowed (enlist left vertices out): flag the step in the
+  // count's top bit, so the next step learns it from the load it makes anyway
+  if (flag_overflow && sh->big_n > kBigCap && threadIdx.x == 0) atomicOr(nchunk, kChunkOver);
   const uint32_t nb = min(sh->big_n, kBigCap);
   unsigned long long deg = 0;
   if (nb == 0) return 0;
@@ -346,7 +365,7 @@ __device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc
       total += (sh->bige[i] - sh->bigb[i] + kChunk - 1) / kChunk;
       deg += sh->bige[i] - sh->bigb[i];
     }
-    const uint32_t base = atomicAdd(nchunk, total);
+    const uint32_t base = atomicAdd(nchunk, total) & ~kChunkOver;
     for (uint32_t i = 0; i < nb; ++i) sh->bigc[i] += base;
   }
   __syncthreads();
@@ -848,8 +867,30 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, uint32_t vmax, 
 }
 
 // ------------------------------------------------------------------ push
+// Chunks of every big vertex of the frontier of step g-1, over this rank's
+// push rows, replacing the list step g-1 built: sharded runs (local raises
+// enlist nothing; other ranks raise most of the frontier) and steps whose
+// big-vertex lists overflowed (enlist). Between steps, not inside push_step:
+// barriers there keep the push step's loads from being scheduled early.
+__device__ void rechunk_pass(const RunArgs& a, uint32_t g, BlockSh* sh, cg::grid_group& grid) {
+  SlotCtl* plw = &a.ctl->slot[(g - 1u) % 3u];
+  uint4* bpw = a.BC[(g - 1u) & 1u];
+  const uint32_t* fp = a.FB[(g - 1u) & 1u];
+  const uint32_t lane = lane_id(), gw = gwarp(a), nw = nwarps(a);
+  grid.sync();  // every block has read the count before it is reset
+  if (vblk(a) == 0 && threadIdx.x == 0) plw->nchunk = 0;
+  grid.sync();
+  for (uint32_t wi = gw; wi < a.nwords; wi += nw) {
+    const uint32_t word = __ldcg(fp + wi) & __ldcg(a.bigm + wi);
+    if ((word >> lane) & 1u) enlist_all(a, wi * 32u + lane, bpw, &plw->nchunk, sh);
+  }
+  big_flush(a, sh, bpw, plw, false);
+  grid.sync();
+}
+
 template <bool RL>
-__device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, unsigned long long tk) {
+__device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk, BlockSh* sh,
+                          unsigned long long tk) {
   SlotCtl* sl = &a.ctl->slot[g % 3u];
   const SlotCtl* pl = &a.ctl->slot[(g - 1u) % 3u];
   PushCtx c;
@@ -871,22 +912,11 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   const uint32_t gw = gwarp(a);
   const uint32_t nw = nwarps(a);
   StepAcc acc;
-  if (a.world > 1) {
-    // sharded: local raises enlist nothing (other ranks raise most of the
-    // frontier); chunk every big vertex of the replicated frontier over this
-    // rank's push rows, then start pushing once every block has listed its part
-    SlotCtl* plw = &a.ctl->slot[(g - 1u) % 3u];
-    uint4* bpw = a.BC[(g - 1u) & 1u];
-    for (uint32_t wi = gw; wi < a.nwords; wi += nw) {
-      const uint32_t word = __ldcg(fp + wi) & __ldcg(a.bigm + wi);
-      if ((word >> lane) & 1u) enlist(a, wi * 32u + lane, bpw, &plw->nchunk, sh);
-    }
-    big_flush(a, sh, bpw, &plw->nchunk);
-    cg::this_grid().sync();
-  }
+  const uint32_t wlc = __ldca(&pl->wl_count);
+  const uint32_t wl_over = __ldca(&pl->wl_over);
   // big frontier vertices first: one warp per kChunk-edge chunk, each lane
   // raising kChunk/32 targets as one batch
-  const uint32_t nch = min(__ldcg(&pl->nchunk), a.chunk_cap);
+  const uint32_t nch = min(nchunk & ~kChunkOver, a.chunk_cap);
   for (uint32_t k = gw; k < nch; k += nw) {
     const uint4 ch = bp[k];
     const uint32_t vv = cand_of<RL>(a, __ldca(c.Pc + ch.x), ch.x);
@@ -906,9 +936,8 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, BlockSh* sh, un
   // grid, so a contiguous wave of raised ids spreads over many warps), or from
   // a scan of the whole bitmap when that list overflowed. Lane i owns bit i of
   // each word; each word is cleared by the warp that consumes it.
-  const uint32_t wlc = __ldca(&pl->wl_count);
   // sharded: the word lists only know this rank's raises; scan the replicated bitmap
-  const bool scan = a.world > 1 || __ldca(&pl->wl_over) != 0u;
+  const bool scan = a.world > 1 || wl_over != 0u;
   const uint32_t groups = scan ? (a.nwords + 3u) / 4u : (wlc + 3u) / 4u;
   for (uint32_t it = gw; it < groups; it += nw) {
     uint32_t wi[kBatch], wd[kBatch];
@@ -1078,7 +1107,7 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, uint64_t t, BlockSh* sh
       }
     }
   }
-  const unsigned long long bigdeg = big_flush(a, sh, bc, &sl->nchunk);
+  const unsigned long long bigdeg = big_flush(a, sh, bc, sl, true);
   fe = block_sum(fe, sh) + bigdeg;
   vm = ~block_min(~vm, sh);
   if (threadIdx.x == 0 && fe) atomicAdd(&sl->fedges, fe);
@@ -1234,6 +1263,7 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
         const bool xch = SH && a.world > 1;  // records come from the exchange
         const unsigned long long p_fe = xch ? g_fe : __ldca(&ctl->slot[pslot].fedges);
         const unsigned long long p_nr = xch ? g_nr : __ldca(&ctl->slot[pslot].nraised);
+        unsigned int p_nchunk = __ldca(&ctl->slot[pslot].nchunk);
         if (mode != kModePull && mode != kModePush) {
           unsigned long long est;
           if (prev_push) {
@@ -1253,7 +1283,12 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
             stat[kResBytes] += 8ull * p_fe + 12ull * p_nr;
             stat[kResPushSteps] += 1;
           }
-          push_step<RL>(a, g, cur, &sh, a.trace ? tkk : ~0ull);
+          // every sharded rank re-chunks (ranks emulated in one grid stay in step)
+          if (xch || (p_nchunk & kChunkOver)) {
+            rechunk_pass(a, g, &sh, grid);
+            p_nchunk = __ldcg(&ctl->slot[pslot].nchunk);
+          }
+          push_step<RL>(a, g, cur, p_nchunk, &sh, a.trace ? tkk : ~0ull);
         } else {
           CYC_STAT(kResEdges, a.m);
           CYC_STAT(kResRows, a.n);

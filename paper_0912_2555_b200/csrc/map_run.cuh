@@ -15,12 +15,14 @@ struct alignas(64) SlotCtl {
   unsigned long long fedges;  // push degrees of the vertices first raised in the step
   unsigned int nraised;       // vertices raised
   unsigned int changed;
-  unsigned int nchunk;        // big-vertex chunks enlisted for the next step
+  unsigned int nchunk;        // big-vertex chunks enlisted for the next step; bit 31: a CTA's list
+                              // overflowed, the next push step re-chunks the frontier (kChunkOver)
   unsigned int cand_cnt;      // self-witness candidates
   unsigned int wit;           // exact min self-witness (pull rows)
   unsigned int wl_count;      // frontier words listed for the next push step
   unsigned int wl_over;       // the list is incomplete: scan the bitmap instead
 };
+constexpr unsigned int kChunkOver = 0x80000000u;
 
 // Control block of one k_map_run launch. Per-step counters rotate over three
 // slots (step g writes slot g%3, reads slot (g-1)%3, and clears slot (g+1)%3),
