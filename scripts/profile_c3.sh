@@ -1,8 +1,10 @@
 #!/bin/bash
-# Round-2 evidence: GPU tests (both layouts), bench launch list, ncu --set full of k_map_run on config 3.
+# Round-2 evidence: bench line (N=1), reference arm, sharded N=1 line, launch
+# list and ncu --set full of k_map_run on config 3 (outputs in gpurun_out/).
 cd "$(dirname "$0")/.."
-timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo GPU_TESTS=$?; tail -2 gpurun_out/gpu_tests.log
-CYC_LAYOUT=2 timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests_l2.log 2>&1; echo GPU_TESTS_L2=$?; tail -2 gpurun_out/gpu_tests_l2.log
+timeout 900 python bench.py > gpurun_out/bench_c3.log 2>&1; echo BENCH=$?
+timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_ref_c3.log 2>&1; echo REF=$?
+timeout 900 python bench.py --sharded --steps 5 --warmup 2 --no-cpu-baseline > gpurun_out/bench_shard1.log 2>&1; echo SHARD=$?
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
