@@ -232,7 +232,25 @@ def cpu_reference_sample(params, seconds: float, workers: int):
                                        "setup_snapshot_s": round(t_snap, 3)}
 
 
-def ref_ttv_summary(args):
+def ref_live(params, args, workers, samples):
+    """The reference's CPU numbers measured in THIS run on this host: the W=1
+    step rate (one bounded sample), the spread of the W=nproc samples, and
+    its run_map part of the time to verdict (gather-index build + the early-
+    exit step count at the measured step time) beside the recorded one."""
+    g1, k1, s1, _, _ = cpu_reference_sample(params, max(1.0, args.ref_seconds / 2), 1)
+    rates = [v[0] for v in samples]
+    step_s = statistics.median(v[2] / max(v[1], 1) for v in samples)
+    out = {"w1_gteps": round(g1, 5), "w1_steps": k1, "wn_gteps_min": round(min(rates), 5),
+           "wn_gteps_max": round(max(rates), 5), "wn_samples": len(rates), "wn_step_s": round(step_s, 4)}
+    rec = recorded_ref_ttv()
+    if rec and rec.get("config") == args.config and (rec.get("n"), rec.get("m_log")) == (int(params.n), int(params.m)):
+        kc = rec["stats"][str(workers)][3] if str(workers) in rec["stats"] else rec["stats"]["1"][3]
+        out["run_map_s_live_estimate"] = round(samples[0][3] + kc * step_s, 3)
+        out["ttv_s_live_estimate"] = round(rec["build_snapshot_s"] + out["run_map_s_live_estimate"], 3)
+    return out
+
+
+def ref_ttv_summary(args, params):
     """CPU time to verdict (early exit) of the reference, phase by phase
     (cycheck_main.cpp:88-97: csr = build_snapshot, kernel = run_map incl. its
     gather-index build) at W=1 and W=nproc. A full config-3 run takes ~10
@@ -240,7 +258,7 @@ def ref_ttv_summary(args):
     scripts/ref_ttv.py on a GPU box host (same oracle/_ref build) and quoted
     from profiles/r02_ref_ttv_c3.json; None for other configs."""
     rec = recorded_ref_ttv()
-    if not rec or rec.get("config") != args.config:
+    if not rec or rec.get("config") != args.config or (rec.get("n"), rec.get("m_log")) != (int(params.n), int(params.m)):
         return None
     return {"recorded": os.path.relpath(REF_TTV_FILE, ROOT), "cpu_model": rec.get("cpu_model"),
             "nproc": rec.get("nproc"), "build_snapshot_s": rec.get("build_snapshot_s"),
@@ -262,8 +280,9 @@ def run_reference_arm(args, rank, world):
     for i in range(args.warmup + args.steps):
         g, k, secs, m, info = cpu_reference_sample(params, args.ref_seconds, workers)
         if i >= args.warmup:
-            vals.append((g, k, secs))
+            vals.append((g, k, secs, info["gather_build_s"]))
     gteps = statistics.median(v[0] for v in vals)
+    live = ref_live(params, args, workers, vals)
     sample = (f"{WORKLOADS.get(args.config)}: reference MaxPropagation::step with WorkerPool({workers}), "
               f"Jacobi steps of the first fixpoint from all-NIL (restarted at the fixpoint), "
               f"~{args.ref_seconds}s per bench step ({vals[0][1]} steps)")
@@ -276,7 +295,7 @@ def run_reference_arm(args, rank, world):
         "config": bench_config(args, params),
         "cpu_baseline": {"value": round(gteps, 5), "unit": "GTEPS", "cores": workers, "kind": "reference",
                          "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count(), **(info or {}),
-                         "time_to_verdict": ref_ttv_summary(args)},
+                         "live": live, "time_to_verdict": ref_ttv_summary(args, params)},
         "e2e": {"value": round(gteps, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     # the reference arm must not have mapped the engine library
@@ -417,15 +436,16 @@ def run_b200(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             workers = os.cpu_count() or 1
-            g_cpu, k, secs, m_ref, info = cpu_reference_sample(gen_params(args, reference=True), args.ref_seconds,
-                                                               workers)
+            rp = gen_params(args, reference=True)
+            g_cpu, k, secs, m_ref, info = cpu_reference_sample(rp, args.ref_seconds, workers)
             assert m_ref == m
+            live = ref_live(rp, args, workers, [(g_cpu, k, secs, info["gather_build_s"])])
             line["cpu_baseline"] = {
                 "value": round(g_cpu, 5), "unit": "GTEPS", "cores": workers, "kind": "reference",
                 "cpu_model": cpu_model(),
                 "sample": f"reference MaxPropagation::step, WorkerPool({workers}), {k} Jacobi steps of the "
-                          f"first fixpoint of the same graph in {secs:.1f}s", **info,
-                "time_to_verdict": ref_ttv_summary(args)}
+                          f"first fixpoint of the same graph in {secs:.1f}s", **info, "live": live,
+                "time_to_verdict": ref_ttv_summary(args, rp)}
         except Exception as ex:  # reference build missing on this box
             line["cpu_baseline"] = {"value": None, "unit": "GTEPS", "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {ex}"}

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <stdexcept>
 #include <sstream>
 #include <string>
@@ -41,6 +42,10 @@ int fail(const std::exception& e, int code) {
 struct Snap {
   CsrSnapshot snap;
   std::vector<VertexId> kept;  // only for restricted snapshots
+  // the reference's MaxPropagation of this snapshot (its gather-index build,
+  // map_engine.cpp:9-19), made once by ref_time_steps and reused
+  std::unique_ptr<MaxPropagation> prop;
+  double prop_s = 0;
 };
 
 Bitset bitset_from(const uint64_t* words, uint32_t n) {
@@ -344,9 +349,12 @@ int ref_time_steps(void* h, int workers, uint64_t max_steps, double max_seconds,
   REF_TRY
   using clk = std::chrono::steady_clock;
   auto* s = static_cast<Snap*>(h);
-  auto t0 = clk::now();
-  MaxPropagation kernel(s->snap);
-  auto t1 = clk::now();
+  if (!s->prop) {
+    auto t0 = clk::now();
+    s->prop = std::make_unique<MaxPropagation>(s->snap);
+    s->prop_s = std::chrono::duration<double>(clk::now() - t0).count();
+  }
+  const MaxPropagation& kernel = *s->prop;
   WorkerPool pool(workers);
   MapVector x(s->snap.n, MapValue::nil()), nx(s->snap.n, MapValue::nil());
   uint64_t k = 0;
@@ -361,7 +369,7 @@ int ref_time_steps(void* h, int workers, uint64_t max_steps, double max_seconds,
     if (std::chrono::duration<double>(clk::now() - t2).count() > max_seconds) break;
   }
   auto t3 = clk::now();
-  times[0] = std::chrono::duration<double>(t1 - t0).count();
+  times[0] = s->prop_s;  // the gather-index build (first call of this snapshot)
   times[1] = std::chrono::duration<double>(t3 - t2).count();
   *steps_done = k;
   return 0;
