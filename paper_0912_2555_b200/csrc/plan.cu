@@ -5,7 +5,11 @@
 //      rows contain it), descending; log-linear buckets above 512.
 //   2. stable counting sort of the vertices by key: per-warp ranges, a
 //      [bucket x warp] count table scanned bucket-major, then each warp places
-//      its vertices in id order (match_any ranks) -> orig[] and perm[].
+//      its vertices in sequence order (match_any ranks) -> orig[] and perm[].
+//      Ties (equally gathered vertices, so equally hot in L2) are broken by
+//      gather-row length through a first stable pass (LSD), which makes the
+//      sliced ELL's 32-row slices near uniform (config 3 family: 2.2x -> 1.01x
+//      padding of the light rows).
 //   3. both CSRs re-laid out in storage order with columns mapped through
 //      perm[]: rows <= kHeavyDeg as 32-row warp groups walking their
 //      concatenated edges, longer rows from the graph's heavy-chunk lists.
@@ -23,6 +27,9 @@ namespace {
 
 constexpr uint32_t kBuckets = 1024;
 constexpr int kPlanWarps = 8;  // warps per CTA in the sort kernels
+// tie-break classes: gather-row lengths 0..64 exact, longer (heavy-slab) rows
+// share one class, so the 32-row slices of the sliced ELL are near uniform
+constexpr uint32_t kTieClamp = 65;
 
 __device__ __forceinline__ uint32_t lane_of() { return threadIdx.x & 31u; }
 
@@ -34,14 +41,20 @@ __device__ __forceinline__ uint32_t deg_bucket(uint32_t d) {
   return b < kBuckets ? b : kBuckets - 1u;
 }
 
-// descending degree first
-__device__ __forceinline__ uint32_t sort_key(const uint32_t* __restrict__ off, uint32_t v) {
-  return kBuckets - 1u - deg_bucket(__ldg(off + v + 1) - __ldg(off + v));
+// descending degree first (degrees above `clamp` share one bucket)
+__device__ __forceinline__ uint32_t sort_key(const uint32_t* __restrict__ off, uint32_t v, uint32_t clamp) {
+  return kBuckets - 1u - min(deg_bucket(__ldg(off + v + 1) - __ldg(off + v)), clamp);
+}
+
+// i-th vertex of the sequence being sorted (ids, or a previous pass's order)
+__device__ __forceinline__ uint32_t seq_at(const uint32_t* __restrict__ src, uint64_t i) {
+  return src ? __ldg(src + i) : (uint32_t)i;
 }
 
 // T[key * nw + w] = vertices of warp range w with that key
 __global__ void k_plan_hist(uint32_t n, uint32_t per_warp, const uint32_t* __restrict__ soff,
-                            uint32_t* __restrict__ T, uint32_t nw) {
+                            const uint32_t* __restrict__ src, uint32_t clamp, uint32_t* __restrict__ T,
+                            uint32_t nw) {
   __shared__ uint32_t h[kPlanWarps][kBuckets];
   const uint32_t wl = threadIdx.x >> 5, lane = lane_of();
   const uint32_t gw = blockIdx.x * kPlanWarps + wl;
@@ -50,7 +63,7 @@ __global__ void k_plan_hist(uint32_t n, uint32_t per_warp, const uint32_t* __res
   if (gw < nw) {
     const uint64_t lo = (uint64_t)gw * per_warp;
     const uint64_t hi = lo + per_warp < n ? lo + per_warp : n;
-    for (uint64_t v = lo + lane; v < hi; v += 32u) atomicAdd(&h[wl][sort_key(soff, (uint32_t)v)], 1u);
+    for (uint64_t v = lo + lane; v < hi; v += 32u) atomicAdd(&h[wl][sort_key(soff, seq_at(src, v), clamp)], 1u);
     __syncwarp();
     for (uint32_t k = lane; k < kBuckets; k += 32u) T[(size_t)k * nw + gw] = h[wl][k];
   }
@@ -66,7 +79,7 @@ __global__ void k_plan_totals(const uint32_t* __restrict__ T, uint32_t nw, unsig
 }
 
 __global__ void k_plan_place(uint32_t n, uint32_t per_warp, const uint32_t* __restrict__ soff,
-                             const uint32_t* __restrict__ base, uint32_t nw, uint32_t* __restrict__ orig,
+                             const uint32_t* __restrict__ src, uint32_t clamp, const uint32_t* __restrict__ base, uint32_t nw, uint32_t* __restrict__ orig,
                              uint32_t* __restrict__ perm) {
   __shared__ uint32_t cur[kPlanWarps][kBuckets];
   const uint32_t wl = threadIdx.x >> 5, lane = lane_of();
@@ -77,15 +90,16 @@ __global__ void k_plan_place(uint32_t n, uint32_t per_warp, const uint32_t* __re
   const uint64_t lo = (uint64_t)gw * per_warp;
   const uint64_t hi = lo + per_warp < n ? lo + per_warp : n;
   const uint32_t below = (1u << lane) - 1u;
-  for (uint64_t v0 = lo; v0 < hi; v0 += 32u) {
-    const uint64_t v = v0 + lane;
-    const bool ok = v < hi;
-    const uint32_t key = ok ? sort_key(soff, (uint32_t)v) : kBuckets + lane;  // unmatched sentinel
+  for (uint64_t i0 = lo; i0 < hi; i0 += 32u) {
+    const uint64_t i = i0 + lane;
+    const bool ok = i < hi;
+    const uint32_t v = ok ? seq_at(src, i) : 0u;
+    const uint32_t key = ok ? sort_key(soff, v, clamp) : kBuckets + lane;  // unmatched sentinel
     const uint32_t peers = __match_any_sync(kFull, key);
     if (ok) {
       const uint32_t pos = cur[wl][key] + __popc(peers & below);
-      orig[pos] = (uint32_t)v;
-      perm[v] = pos;
+      orig[pos] = v;
+      if (perm) perm[v] = pos;
     }
     __syncwarp();
     if (ok && (__ffs(peers) - 1u) == lane) cur[wl][key] += __popc(peers);
@@ -282,17 +296,29 @@ void relayout(const DevCsr& in, const uint32_t* orig, const uint32_t* perm, DevC
   }
 }
 
-void degree_order(const uint32_t* key_off, uint32_t n, uint32_t* orig, uint32_t* perm, cudaStream_t s) {
+void degree_order(const uint32_t* key_off, const uint32_t* tie_off, uint32_t n, uint32_t* orig, uint32_t* perm,
+                  cudaStream_t s) {
   const uint32_t nw = (uint32_t)sm_count() * kPlanWarps;
   const uint32_t per_warp = div_up(div_up(n, nw), 32) * 32;
   const uint32_t blocks = div_up(nw, kPlanWarps);
   const uint32_t np = (uint32_t)(((uint64_t)n + kRowPad - 1) / kRowPad * kRowPad);
-  DevBuf T((size_t)kBuckets * nw * 4, s), base((size_t)kBuckets * nw * 4 + 4, s), scratch;
-  k_plan_hist<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, key_off, T.as<uint32_t>(), nw);
-  CYC_LAUNCHED();
-  exclusive_scan(T.as<uint32_t>(), base.as<uint32_t>(), kBuckets * nw, nullptr, s, scratch);
-  k_plan_place<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, key_off, base.as<uint32_t>(), nw, orig, perm);
-  CYC_LAUNCHED();
+  DevBuf T((size_t)kBuckets * nw * 4, s), base((size_t)kBuckets * nw * 4 + 4, s), scratch, seq;
+  // LSD: the tie-break pass first (stable sorts), then the primary key over its order
+  auto pass = [&](const uint32_t* off, const uint32_t* src, uint32_t clamp, uint32_t* out, uint32_t* pm) {
+    k_plan_hist<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, off, src, clamp, T.as<uint32_t>(), nw);
+    CYC_LAUNCHED();
+    exclusive_scan(T.as<uint32_t>(), base.as<uint32_t>(), kBuckets * nw, nullptr, s, scratch);
+    k_plan_place<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, off, src, clamp, base.as<uint32_t>(), nw, out, pm);
+    CYC_LAUNCHED();
+  };
+  const char* tb = std::getenv("CYC_PLAN_TIE");
+  if (tie_off && !(tb && tb[0] == '0')) {
+    seq.alloc((size_t)n * 4, s);
+    pass(tie_off, nullptr, kTieClamp, seq.as<uint32_t>(), nullptr);
+    pass(key_off, seq.as<uint32_t>(), kBuckets - 1u, orig, perm);
+  } else {
+    pass(key_off, nullptr, kBuckets - 1u, orig, perm);
+  }
   k_plan_pad<<<grid_for(np + 1 - n, 256, 1), 256, 0, s>>>(n, np + 1, orig);
   CYC_LAUNCHED();
 }
@@ -361,7 +387,7 @@ bool build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& pla
   const uint32_t per_warp = div_up(div_up(n, nw), 32) * 32;
   DevBuf T((size_t)kBuckets * nw * 4, s), base((size_t)kBuckets * nw * 4 + 4, s), tot(kBuckets * 8, s);
   const uint32_t blocks = div_up(nw, kPlanWarps);
-  k_plan_hist<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, snap.o(), T.as<uint32_t>(), nw);
+  k_plan_hist<<<blocks, kPlanWarps * 32, 0, s>>>(n, per_warp, snap.o(), nullptr, kBuckets - 1u, T.as<uint32_t>(), nw);
   CYC_LAUNCHED();
   k_plan_totals<<<kBuckets / 256, 256, 0, s>>>(T.as<uint32_t>(), nw, tot.as<unsigned long long>());
   CYC_LAUNCHED();
@@ -388,7 +414,7 @@ bool build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& pla
   plan.orig.alloc(((size_t)np + 1) * 4, s);
   plan.perm.alloc((size_t)n * 4, s);
   DevBuf scratch;
-  degree_order(snap.o(), n, plan.orig.as<uint32_t>(), plan.perm.as<uint32_t>(), s);
+  degree_order(snap.o(), gath.o(), n, plan.orig.as<uint32_t>(), plan.perm.as<uint32_t>(), s);
   mark("place");
   relayout(gath, plan.orig.as<uint32_t>(), plan.perm.as<uint32_t>(), plan.gath, scratch, s);
   mark("gath");

@@ -52,7 +52,8 @@ bool build_plan(const DevCsr& snap, const DevCsr& gath, int layout, MapPlan& pla
 
 // Storage order by descending key (row lengths of key_off, n+1 offsets):
 // orig[p] = vertex at position p (identity on the padding up to n_pad), perm = inverse.
-void degree_order(const uint32_t* key_off, uint32_t n, uint32_t* orig, uint32_t* perm, cudaStream_t s);
+void degree_order(const uint32_t* key_off, const uint32_t* tie_off, uint32_t n, uint32_t* orig, uint32_t* perm,
+                  cudaStream_t s);
 // `in` with rows and columns relabelled to storage order (out[perm[v]] = in[v]
 // with columns mapped through perm); needs in's heavy-chunk list.
 void relayout(const DevCsr& in, const uint32_t* orig, const uint32_t* perm, DevCsr& out, DevBuf& scratch,

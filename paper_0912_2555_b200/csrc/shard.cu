@@ -174,11 +174,12 @@ void build_shard(const uint32_t* d_edges, uint64_t m_log, uint32_t n, const uint
   // vertices take at least half of the gathers
   const bool want = n >= 64 && (layout == 2 || (layout == 0 && (uint64_t)n * 4 > (40ull << 20)));
   if (want) {
-    DevBuf koff(((size_t)n + 1) * 4, s);
+    DevBuf koff(((size_t)n + 1) * 4, s), toff(((size_t)n + 1) * 4, s);
     exclusive_scan(gcol.as<uint32_t>(), koff.as<uint32_t>(), n, nullptr, s, scratch);
+    exclusive_scan(grow.as<uint32_t>(), toff.as<uint32_t>(), n, nullptr, s, scratch);
     sh.orig.alloc(((size_t)np + 1) * 4, s);
     sh.perm.alloc((size_t)n * 4, s);
-    degree_order(koff.as<uint32_t>(), n, sh.orig.as<uint32_t>(), sh.perm.as<uint32_t>(), s);
+    degree_order(koff.as<uint32_t>(), toff.as<uint32_t>(), n, sh.orig.as<uint32_t>(), sh.perm.as<uint32_t>(), s);
     sh.relabel = true;
     if (layout == 0) {
       DevBuf hl(((size_t)n + 1) * 4, s), hp(((size_t)n + 1) * 4, s);
