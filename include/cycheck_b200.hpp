@@ -59,6 +59,12 @@ class Engine {
     ctx_.reset(c, &cyc_ctx_destroy);
   }
   cyc_ctx* get() const { return ctx_.get(); }
+  // Allocates a build's device memory for logs up to m_log edges / n vertices
+  // ahead of the first build (cyc_ctx_reserve), by default on a library
+  // thread while the caller fills its EdgeLog.
+  void reserve(uint64_t m_log, uint32_t n, bool background = true) const {
+    check(cyc_ctx_reserve(ctx_.get(), m_log, n, background ? 1 : 0));
+  }
 
  private:
   std::shared_ptr<cyc_ctx> ctx_;

@@ -134,6 +134,7 @@ _SIGS = {
     "cyc_ctx_synchronize": (C.c_int, [_P]),
     "cyc_ctx_stream": (_P, [_P]),
     "cyc_ctx_set_stream": (C.c_int, [_P, _P, C.c_int]),
+    "cyc_ctx_reserve": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_int]),
     "cyc_graph_build": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.c_int, C.POINTER(_P)]),
     "cyc_graph_from_csr": (C.c_int, [_P, _P, _P, C.c_uint32, C.c_uint64, _P, C.c_int, C.POINTER(_P)]),
     "cyc_graph_extend": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, _P, C.POINTER(_P)]),

@@ -184,6 +184,12 @@ class Context:
     def synchronize(self) -> None:
         check(_abi.lib().cyc_ctx_synchronize(self._h))
 
+    def reserve(self, m_log: int, n: int, background: bool = True) -> None:
+        """Allocate what a build of an m_log-edge log over n vertices uses
+        ahead of the first call (cyc_ctx_reserve); (0, 0) waits for a
+        background reserve."""
+        check(_abi.lib().cyc_ctx_reserve(self._h, int(m_log), int(n), int(background)))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             _abi.lib().cyc_ctx_destroy(self._h)

@@ -154,13 +154,19 @@ struct cyc_ctx {
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cyc::BuildArena arena2;
+  std::thread reserver;  // cyc_ctx_reserve(background): maps pool memory off the caller's thread
   std::atomic<int> refs{1};
 };
 
 namespace {
 void big_trim(int device, cudaStream_t st);
+// builds wait for a background cyc_ctx_reserve (it owns the arenas meanwhile)
+void join_reserve(cyc_ctx* ctx) {
+  if (ctx->reserver.joinable()) ctx->reserver.join();
+}
 void ctx_release(cyc_ctx* ctx) {
   if (ctx->refs.fetch_sub(1) != 1) return;
+  join_reserve(ctx);
   cudaSetDevice(ctx->device);
   ctx->flush.release();
   ctx->arena = cyc::BuildArena();
@@ -360,6 +366,7 @@ void build_graph(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, uint32_t n
   require(n < 0x80000000u, CYC_E_RESOURCE, "vertex count must be < 2^31");
   require(m_log < 0xFFFFFFFFull, CYC_E_RESOURCE, "edge log prefix must be < 2^32");
   require(m_log == 0 || edges, CYC_E_CONTRACT, "build_snapshot: null edge array");
+  join_reserve(ctx);
   cudaStream_t s = ctx->s;
   DevBuf tmp_edges, err(16, s);
   CYC_CUDA(cudaMemsetAsync(err.p, 0, 16, s));
@@ -538,6 +545,51 @@ cyc_status cyc_ctx_create(int device, cyc_ctx** out) {
 
 void cyc_ctx_destroy(cyc_ctx* ctx) {
   if (ctx) ctx_release(ctx);
+}
+
+// First touch of device memory costs ~150 GB/s on a B200
+// (scripts/micro/map_rate.cu): config 3's first call maps ~60 GB of build
+// temporaries and outputs (~0.4 s of a ~0.7 s first call). cyc_ctx_reserve
+// allocates them ahead, sized for a log of m_log edges over n vertices: the
+// two build arenas at the sizes build_csr asks for, and blocks of the staged
+// log / CSR columns / offsets parked in the big-block cache, where the
+// build's own requests pick them up.
+cyc_status cyc_ctx_reserve(cyc_ctx* ctx, uint64_t m_log, uint32_t n, int background) {
+  return guard([&] {
+    require(ctx, CYC_E_CONTRACT, "null ctx");
+    join_reserve(ctx);
+    if (!m_log) return;
+    auto work = [ctx, m_log, n] {
+      try {
+        CYC_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->own;
+        const size_t nn = (size_t)n + 1;
+        for (cyc::BuildArena* a : {&ctx->arena, &ctx->arena2}) {
+          a->get<uint8_t>(a->tmp, m_log * 8, s);
+          a->get<uint8_t>(a->tmp2, m_log * 8, s);
+          a->get<uint8_t>(a->raw, m_log * 4, s);
+          a->get<uint8_t>(a->roff, nn * 4, s);
+          a->get<uint8_t>(a->ucnt, nn * 4, s);
+          a->get<uint8_t>(a->lists, nn * 12, s);
+        }
+        // staged log, snapshot / gather / plan columns and offsets
+        const size_t sizes[] = {m_log * 8, m_log * 4, m_log * 4, m_log * 4, m_log * 4, nn * 4, nn * 4, nn * 4, nn * 4};
+        std::vector<std::pair<void*, size_t>> got;
+        for (size_t b : sizes) {
+          if (b < cyc::kBigBlock) continue;
+          size_t cap = 0;
+          void* p = cyc::big_alloc(b, s, &cap);
+          got.emplace_back(p, cap);
+        }
+        for (auto& pc : got) cyc::big_free(pc.first, pc.second, s);
+        CYC_CUDA(cudaStreamSynchronize(s));
+      } catch (...) {
+        cudaGetLastError();  // out of memory: the builds allocate as they go
+      }
+    };
+    if (background) ctx->reserver = std::thread(work);
+    else work();
+  });
 }
 
 cyc_status cyc_ctx_synchronize(cyc_ctx* ctx) {
@@ -1058,6 +1110,7 @@ cyc_status cyc_shard_build(cyc_ctx* ctx, const uint32_t* edges, uint64_t m_log, 
     require(m_log < 0xFFFFFFFFull, CYC_E_RESOURCE, "edge log prefix must be < 2^32");
     require(m_log == 0 || edges, CYC_E_CONTRACT, "build_snapshot: null edge array");
     CYC_CUDA(cudaSetDevice(ctx->device));
+    join_reserve(ctx);
     DevBuf tmp, tacc;
     const uint32_t* de = stage_in(edges, (size_t)m_log * 2, tmp, ctx->s);
     const uint64_t* da = stage_in(acc_words, acc_words64(n), tacc, ctx->s);

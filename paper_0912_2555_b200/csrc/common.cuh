@@ -78,14 +78,15 @@ struct DevBuf {
     return *this;
   }
   ~DevBuf() { release(); }
+  // On failure the buffer is left empty (bytes == 0), never sized but null.
   void alloc(size_t n, cudaStream_t st) {
     release();
     s = st;
-    bytes = n;
     if (n == 0) return;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (n >= kBigBlock && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
       p = big_alloc(n, st, &cap);
+      bytes = n;
       return;
     }
     cudaError_t e = cudaMallocAsync(&p, n, st);
@@ -95,6 +96,7 @@ struct DevBuf {
       throw Error(CYC_E_RESOURCE, "device memory exhausted allocating " + std::to_string(n) + " bytes");
     }
     CYC_CUDA(e);
+    bytes = n;
   }
   void release() {
     if (p && cap) big_free(p, cap, s);
