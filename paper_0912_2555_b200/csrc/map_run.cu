@@ -138,6 +138,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ uint32_t vblk(const RunArgs& a) { return blockIdx.x - a.blk0; }
 __device__ __forceinline__ uint32_t gwarp(const RunArgs& a) { return (vblk(a) * blockDim.x + threadIdx.x) >> 5; }
 __device__ __forceinline__ uint32_t nwarps(const RunArgs& a) { return (a.nblk * blockDim.x) >> 5; }
+// The same warps numbered across the blocks first (warp w of block b ->
+// w * nblk + b): loops over few items (push steps of small frontiers) then
+// spread them over every SM. Numbered block-major, config 5's 128 frontier
+// groups all ran on 4 SMs, whose load units (one divergent-load wavefront per
+// clock) spent ~5 us of each 10 us step on their scattered loads.
+__device__ __forceinline__ uint32_t swarp(const RunArgs& a) { return (threadIdx.x >> 5) * a.nblk + vblk(a); }
 
 // Trace hook: latest time any warp passed phase `ph` of the current step.
 __device__ __forceinline__ void phase_mark(const RunArgs& a, unsigned long long k, int ph) {
@@ -289,6 +295,34 @@ __device__ void step_flags(const RunArgs& a, const StepAcc& acc, SlotCtl* sl, Bl
   wl_flush(sh, sl, wl, wl_cap);
 }
 
+// A step's final counters, read once after the barrier that ends it: the
+// loop's exit tests, the next step's direction choice and the push step's
+// word list all come from this one round trip (small steps are latency
+// bound: config 5 runs 16767 of them).
+struct SlotView {
+  unsigned long long fedges;
+  uint32_t nraised, changed, nchunk, cand_cnt, wit, wl_count, wl_over;
+};
+static_assert(offsetof(SlotCtl, fedges) == 0 && offsetof(SlotCtl, nraised) == 8 && offsetof(SlotCtl, changed) == 12 &&
+                  offsetof(SlotCtl, nchunk) == 16 && offsetof(SlotCtl, cand_cnt) == 20 &&
+                  offsetof(SlotCtl, wit) == 24 && offsetof(SlotCtl, wl_count) == 28 &&
+                  offsetof(SlotCtl, wl_over) == 32,
+              "ld_slot unpacks SlotCtl by offset");
+__device__ __forceinline__ SlotView ld_slot(const SlotCtl* s) {
+  const uint4* q = reinterpret_cast<const uint4*>(s);
+  const uint4 x = __ldcg(q), y = __ldcg(q + 1);
+  SlotView v;
+  v.fedges = ((unsigned long long)x.y << 32) | x.x;
+  v.nraised = x.z;
+  v.changed = x.w;
+  v.nchunk = y.x;
+  v.cand_cnt = y.y;
+  v.wit = y.z;
+  v.wl_count = y.w;
+  v.wl_over = __ldcg(&s->wl_over);
+  return v;
+}
+
 // Sets bit v of the frontier bitmap (and its summary bit); true iff new.
 __device__ __forceinline__ bool mark(uint32_t* fb, BlockSh* sh, uint32_t v, bool precheck = false) {
   const uint32_t w = v >> 5, bit = 1u << (v & 31u);
@@ -401,8 +435,17 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
                                             StepAcc& acc) {
   uint32_t old[R];
   bool go[R];
+  uint32_t bw[R], b[R], e[R];
+  // small frontiers (latency bound): the target's big bit and degree are
+  // loaded with its value, before knowing it is raised (one round trip less)
 #pragma unroll
-  for (int r = 0; r < R; ++r) old[r] = tgt[r] != kNone ? __ldca(c.Pc + tgt[r]) : kCode;
+  for (int r = 0; r < R; ++r) {
+    const bool spec = !c.contend && tgt[r] != kNone;
+    old[r] = tgt[r] != kNone ? __ldca(c.Pc + tgt[r]) : kCode;
+    bw[r] = spec ? __ldcg(a.bigm + (tgt[r] >> 5)) : 0u;
+    b[r] = spec ? __ldg(a.poff + tgt[r]) : 0u;
+    e[r] = spec ? __ldg(a.poff + tgt[r] + 1) : 0u;
+  }
 #pragma unroll
   for (int r = 0; r < R; ++r) go[r] = tgt[r] != kNone && val[r] > (old[r] & kCode);
   uint32_t cur[R];  // hub targets: many sources raise the same word, skip settled atomics
@@ -411,15 +454,34 @@ __device__ __forceinline__ void raise_batch(const RunArgs& a, const PushCtx& c,
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (go[r] && ((old[r] & kFlag) | val[r]) > cur[r]) atomicMax(c.Pn + tgt[r], (old[r] & kFlag) | val[r]);
-  bool first[R];
+  // frontier bits of the raised targets: every atomic of the batch in flight
+  // together (a per-target mark() would wait for each result before the next)
+  bool first[R], need[R];
+  uint32_t prev[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) first[r] = go[r] && mark(c.fb, c.sh, tgt[r], c.contend);
-  uint32_t bw[R], b[R], e[R];
+  for (int r = 0; r < R; ++r) need[r] = go[r];
+  if (c.contend) {  // hub targets: read first, skip bits already set
 #pragma unroll
-  for (int r = 0; r < R; ++r) {  // one round trip for the big bit and the degree
-    bw[r] = first[r] ? __ldcg(a.bigm + (tgt[r] >> 5)) : 0u;
-    b[r] = first[r] ? __ldg(a.poff + tgt[r]) : 0u;
-    e[r] = first[r] ? __ldg(a.poff + tgt[r] + 1) : 0u;
+    for (int r = 0; r < R; ++r) prev[r] = need[r] ? __ldcg(c.fb + (tgt[r] >> 5)) : 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) need[r] = need[r] && !((prev[r] >> (tgt[r] & 31u)) & 1u);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) prev[r] = need[r] ? atomicOr(c.fb + (tgt[r] >> 5), 1u << (tgt[r] & 31u)) : ~0u;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    first[r] = need[r] && !((prev[r] >> (tgt[r] & 31u)) & 1u);
+    if (need[r] && prev[r] == 0u) note_word(c.sh, tgt[r] >> 5);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {  // large frontiers: one round trip for the big bit and degree of new ones
+    if (c.contend) {
+      bw[r] = first[r] ? __ldcg(a.bigm + (tgt[r] >> 5)) : 0u;
+      b[r] = first[r] ? __ldg(a.poff + tgt[r]) : 0u;
+      e[r] = first[r] ? __ldg(a.poff + tgt[r] + 1) : 0u;
+    } else if (!first[r]) {
+      bw[r] = b[r] = e[r] = 0u;
+    }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -889,10 +951,9 @@ __device__ void rechunk_pass(const RunArgs& a, uint32_t g, BlockSh* sh, cg::grid
 }
 
 template <bool RL>
-__device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk, BlockSh* sh,
+__device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk, const SlotView& pv, BlockSh* sh,
                           unsigned long long tk) {
   SlotCtl* sl = &a.ctl->slot[g % 3u];
-  const SlotCtl* pl = &a.ctl->slot[(g - 1u) % 3u];
   PushCtx c;
   c.Pc = a.P[cur];
   c.Pn = a.P[cur ^ 1];
@@ -904,16 +965,16 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk
   c.ccnt = &sl->cand_cnt;
   // previous step's frontier edges: small frontiers are latency-bound (one
   // more round trip costs), large ones meet hub targets (atomics contend)
-  c.contend = __ldca(&pl->fedges) > (1ull << 20);
+  c.contend = pv.fedges > (1ull << 20);
   uint32_t* fp = a.FB[(g - 1u) & 1u];
   const uint32_t* wlp = a.WL[(g - 1u) & 1u];
   const uint4* bp = a.BC[(g - 1u) & 1u];
   const uint32_t lane = lane_id();
-  const uint32_t gw = gwarp(a);
+  const uint32_t gw = swarp(a);
   const uint32_t nw = nwarps(a);
   StepAcc acc;
-  const uint32_t wlc = __ldca(&pl->wl_count);
-  const uint32_t wl_over = __ldca(&pl->wl_over);
+  const uint32_t wlc = pv.wl_count;
+  const uint32_t wl_over = pv.wl_over;
   // big frontier vertices first: one warp per kChunk-edge chunk, each lane
   // raising kChunk/32 targets as one batch
   const uint32_t nch = min(nchunk & ~kChunkOver, a.chunk_cap);
@@ -960,20 +1021,26 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk
         }
       if (mw) fp[mi] = 0u;
     }
-    uint32_t v[kBatch], b[kBatch], e[kBatch], val[kBatch];
+    uint32_t v[kBatch], b[kBatch], e[kBatch], val[kBatch], xu[kBatch], bwv[kBatch];
+    // every load of the four vertices first, in one round trip: an atomic on
+    // Pn between them would serialise the batch (Pn may alias Pc for the
+    // compiler), which on config 5's chain cost four DRAM latencies a step
 #pragma unroll
     for (int r = 0; r < kBatch; ++r) {
       v[r] = (wd[r] >> lane) & 1u ? wi[r] * 32u + lane : kNone;
-      b[r] = e[r] = 0u;
+      const bool on = v[r] != kNone;
+      xu[r] = on ? __ldca(c.Pc + v[r]) : 0u;
+      bwv[r] = on ? __ldcg(a.bigm + (v[r] >> 5)) : 0u;
+      b[r] = on ? __ldg(a.poff + v[r]) : 0u;
+      e[r] = on ? __ldg(a.poff + v[r] + 1) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
       val[r] = 0u;
-      if (v[r] != kNone) {  // all four loads in one round trip
-        const uint32_t xu = __ldca(c.Pc + v[r]);
-        const uint32_t bwv = __ldcg(a.bigm + (v[r] >> 5));
-        b[r] = __ldg(a.poff + v[r]);
-        e[r] = __ldg(a.poff + v[r] + 1);
-        atomicMax(c.Pn + v[r], xu);  // bring x_{k-2} up to x_{k-1}
-        val[r] = cand_of<RL>(a, xu, v[r]);
-        if ((bwv >> (v[r] & 31u)) & 1u) e[r] = b[r];  // big: chunks push its edges
+      if (v[r] != kNone) {
+        atomicMax(c.Pn + v[r], xu[r]);  // bring x_{k-2} up to x_{k-1}
+        val[r] = cand_of<RL>(a, xu[r], v[r]);
+        if ((bwv[r] >> (v[r] & 31u)) & 1u) e[r] = b[r];  // big: chunks push its edges
       }
     }
     for (uint32_t j = 0;; ++j) {
@@ -1216,6 +1283,7 @@ __device__ ShardRec exchange_step(const RunArgs& a, cg::grid_group& grid, uint32
 template <bool RL, bool SH>
 __device__ __forceinline__ void map_run_body(const RunArgs& a) {
   __shared__ BlockSh sh;
+  __shared__ SlotView spv;  // the last finished step's counters (ld_slot)
   // run statistics live in shared memory of block 0 (kept out of registers)
   __shared__ unsigned long long stat[kResRaised + 1];
   cg::grid_group grid = cg::this_grid();
@@ -1253,6 +1321,8 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
     for (;;) {
       unsigned long long steps = 0;
       bool prev_push = true;  // the previous tag's fedges is exact (push or setup)
+      if (threadIdx.x == 0) spv = ld_slot(&ctl->slot[g % 3u]);  // the setup's counters
+      __syncthreads();
       for (;;) {
         ++g;
         ++steps;
@@ -1261,9 +1331,9 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
         int mode = a.mode;
         // the previous step's (global) frontier size
         const bool xch = SH && a.world > 1;  // records come from the exchange
-        const unsigned long long p_fe = xch ? g_fe : __ldca(&ctl->slot[pslot].fedges);
-        const unsigned long long p_nr = xch ? g_nr : __ldca(&ctl->slot[pslot].nraised);
-        unsigned int p_nchunk = __ldca(&ctl->slot[pslot].nchunk);
+        const unsigned long long p_fe = xch ? g_fe : spv.fedges;
+        const unsigned long long p_nr = xch ? g_nr : spv.nraised;
+        unsigned int p_nchunk = spv.nchunk;
         if (mode != kModePull && mode != kModePush) {
           unsigned long long est;
           if (prev_push) {
@@ -1288,7 +1358,7 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
             rechunk_pass(a, g, &sh, grid);
             p_nchunk = __ldcg(&ctl->slot[pslot].nchunk);
           }
-          push_step<RL>(a, g, cur, p_nchunk, &sh, a.trace ? tkk : ~0ull);
+          push_step<RL>(a, g, cur, p_nchunk, spv, &sh, a.trace ? tkk : ~0ull);
         } else {
           CYC_STAT(kResEdges, a.m);
           CYC_STAT(kResRows, a.n);
@@ -1300,9 +1370,11 @@ __device__ __forceinline__ void map_run_body(const RunArgs& a) {
         cur ^= 1;
         prev_push = mode == kModePush;
         const SlotCtl* sl = &ctl->slot[slot];
-        uint32_t changed = __ldca(&sl->changed);
-        uint32_t w = __ldca(&sl->wit);
-        const uint32_t nc = __ldca(&sl->cand_cnt);
+        if (threadIdx.x == 0) spv = ld_slot(sl);  // one round trip for the block; read from shared below
+        __syncthreads();
+        uint32_t changed = spv.changed;
+        uint32_t w = spv.wit;
+        const uint32_t nc = spv.cand_cnt;
         if (lead && a.trace && tkk < a.trace_cap) {
           unsigned long long* tr = a.trace + 64u * tkk;
           tr[0] = ((unsigned long long)mode << 60) |
