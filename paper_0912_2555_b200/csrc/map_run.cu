@@ -187,7 +187,7 @@ struct BlockSh {
   unsigned long long w[32][3];
   unsigned long long bcast;
   uint32_t wmin[33];
-  uint32_t wl_n, wl_base;
+  uint32_t wl_n, wl_base, wl_cnt;
   uint32_t wl[kWlCap];
   uint32_t big_n;
   uint32_t bigv[kBigCap];
@@ -270,7 +270,18 @@ __device__ unsigned long long big_flush(const RunArgs& a, BlockSh* sh, uint4* bc
 __device__ void step_flags(const RunArgs& a, const StepAcc& acc, SlotCtl* sl, BlockSh* sh,
                            uint32_t* wl, uint32_t wl_cap, uint4* bc) {
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const unsigned long long bigdeg = big_flush(a, sh, bc, sl, true);
+  const unsigned long long bigdeg = big_flush(a, sh, bc, sl, true);  // begins with a CTA barrier
+  // the CTA's slice of the word list (wl_flush's job, folded in): thread 0's
+  // atomic is in flight while the counters are reduced (one round trip and
+  // two CTA barriers less per step than reducing first)
+  uint32_t wl_base = 0, wl_cnt = 0;
+  bool wl_ovf = false;
+  if (threadIdx.x == 0) {
+    const uint32_t n = sh->wl_n;  // every note_word of the step came before the barrier
+    wl_cnt = n < kWlCap ? n : kWlCap;
+    if (wl_cnt) wl_base = atomicAdd(&sl->wl_count, wl_cnt);
+    wl_ovf = n > kWlCap;
+  }
   const unsigned long long r = warp_sum64(acc.raised), f = warp_sum64(acc.first),
                            e = warp_sum64(acc.fedges) + (threadIdx.x == 0 ? bigdeg : 0ull);
   if (lane == 0) {
@@ -292,7 +303,15 @@ __device__ void step_flags(const RunArgs& a, const StepAcc& acc, SlotCtl* sl, Bl
       if (ee) atomicAdd(&sl->fedges, ee);
     }
   }
-  wl_flush(sh, sl, wl, wl_cap);
+  if (threadIdx.x == 0) {
+    if (wl_ovf || wl_base + wl_cnt > wl_cap) *(volatile unsigned int*)&sl->wl_over = 1u;
+    sh->wl_base = wl_base;
+    sh->wl_cnt = wl_cnt;
+    sh->wl_n = 0;  // next written after the grid barrier that ends the step
+  }
+  __syncthreads();
+  const uint32_t cnt = sh->wl_cnt, base = sh->wl_base;
+  for (uint32_t i = threadIdx.x; i < cnt && base + i < wl_cap; i += blockDim.x) wl[base + i] = sh->wl[i];
 }
 
 // A step's final counters, read once after the barrier that ends it: the
