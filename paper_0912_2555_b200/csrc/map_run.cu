@@ -817,9 +817,12 @@ __device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t
   uint32_t pv = 0, pm = 0, po = 0, npend = 0;     // finished rows awaiting write-back
   for (uint32_t c = cb; c < ce; c += B) {
     uint32_t w[B][H];
+    // saturated row (at step start, or its maximum so far in this warp's walk
+    // already reached vmax): its chunk cannot raise it, gather nothing
+    const bool row_sat = rmax == hot.vmax;
 #pragma unroll
     for (int k = 0; k < B; ++k)
-      if ((ro[k] & kCode) == hot.vmax)  // saturated row: its chunk cannot raise it
+      if ((ro[k] & kCode) == hot.vmax || (row_sat && rr[k] == row))
 #pragma unroll
         for (int r = 0; r < H; ++r) u[k][r] = np;
 #pragma unroll
