@@ -951,6 +951,73 @@ __device__ void pull_step(const RunArgs& a, uint32_t g, int cur, uint32_t vmax, 
 }
 
 // ------------------------------------------------------------------ push
+// Chunk descriptors of every big vertex in the words src[w] & bigm[w] (a
+// frontier), written without per-vertex global atomics: each CTA counts the
+// chunks of its contiguous word range (pass A), claims its slice with ONE
+// atomicAdd, and writes the descriptors at the same positions in pass B,
+// a warp per vertex at a time so hubs' thousands of chunks are written 32
+// at once. Replaces per-CTA shared lists that overflowed on whole frontiers
+// (config 3's F: the overflow sent its first push step through lane-by-lane
+// expansion against one global counter, ~0.5 ms of a 1.4 ms step).
+__device__ void chunk_words(const RunArgs& a, const uint32_t* src, uint4* bc, unsigned int* nchunk, BlockSh* sh) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  const uint32_t per = (a.nwords + a.nblk - 1u) / a.nblk;
+  const uint32_t w0 = min(vblk(a) * per, a.nwords), w1 = min(w0 + per, a.nwords);
+  auto chunks_of = [&](uint32_t m, uint32_t wi) {  // this lane's word: its big vertices' chunk count
+    uint32_t nc = 0;
+    while (m) {
+      const uint32_t v = wi * 32u + (__ffs(m) - 1u);
+      m &= m - 1u;
+      nc += (__ldg(a.poff + v + 1) - __ldg(a.poff + v) + kChunk - 1u) / kChunk;
+    }
+    return nc;
+  };
+  // pass A: chunks per warp (each warp takes 32 consecutive words per round)
+  uint32_t mine = 0;
+  for (uint32_t base = w0 + wid * 32u; base < w1; base += nwb * 32u) {
+    const uint32_t wi = base + lane;
+    const uint32_t m = wi < w1 ? __ldcg(src + wi) & __ldcg(a.bigm + wi) : 0u;
+    mine += chunks_of(m, wi);
+  }
+  mine = __reduce_add_sync(kFull, mine);
+  __syncthreads();
+  if (lane == 0) sh->wmin[wid] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // warps' offsets, then the CTA's slice of the list
+    uint32_t tot = 0;
+    for (uint32_t w = 0; w < nwb; ++w) {
+      const uint32_t x = sh->wmin[w];
+      sh->wmin[w] = tot;
+      tot += x;
+    }
+    sh->wmin[32] = tot ? atomicAdd(nchunk, tot) & ~kChunkOver : 0u;
+  }
+  __syncthreads();
+  uint32_t off = sh->wmin[32] + sh->wmin[wid];
+  // pass B: the same words in the same order
+  for (uint32_t base = w0 + wid * 32u; base < w1; base += nwb * 32u) {
+    const uint32_t wi = base + lane;
+    uint32_t m = wi < w1 ? __ldcg(src + wi) & __ldcg(a.bigm + wi) : 0u;
+    const uint32_t nc = chunks_of(m, wi);
+    const uint32_t incl = warp_incl_scan(nc);
+    uint32_t o = off + incl - nc;
+    off += __shfl_sync(kFull, incl, 31);
+    for (uint32_t live = __ballot_sync(kFull, m != 0u); live; live = __ballot_sync(kFull, m != 0u)) {
+      const uint32_t l = __ffs(live) - 1u;
+      const uint32_t ml = __shfl_sync(kFull, m, l), ol = __shfl_sync(kFull, o, l), wl = __shfl_sync(kFull, wi, l);
+      const uint32_t v = wl * 32u + (__ffs(ml) - 1u);
+      const uint32_t b = __ldg(a.poff + v), e = __ldg(a.poff + v + 1);
+      const uint32_t n = (e - b + kChunk - 1u) / kChunk;
+      for (uint32_t c = lane; c < n; c += 32u)
+        if (ol + c < a.chunk_cap) bc[ol + c] = make_uint4(v, b + c * kChunk, min(e, b + (c + 1u) * kChunk), 0u);
+      if (lane == l) {
+        m &= m - 1u;
+        o += n;
+      }
+    }
+  }
+}
+
 // Chunks of every big vertex of the frontier of step g-1, over this rank's
 // push rows, replacing the list step g-1 built: sharded runs (local raises
 // enlist nothing; other ranks raise most of the frontier) and steps whose
@@ -964,11 +1031,7 @@ __device__ void rechunk_pass(const RunArgs& a, uint32_t g, BlockSh* sh, cg::grid
   grid.sync();  // every block has read the count before it is reset
   if (vblk(a) == 0 && threadIdx.x == 0) plw->nchunk = 0;
   grid.sync();
-  for (uint32_t wi = gw; wi < a.nwords; wi += nw) {
-    const uint32_t word = __ldcg(fp + wi) & __ldcg(a.bigm + wi);
-    if ((word >> lane) & 1u) enlist_all(a, wi * 32u + lane, bpw, &plw->nchunk, sh);
-  }
-  big_flush(a, sh, bpw, plw, false);
+  chunk_words(a, fp, bpw, &plw->nchunk, sh);
   grid.sync();
 }
 
@@ -1187,17 +1250,15 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, uint64_t t, BlockSh* sh
         a.P[1][v] = val;
         if (accv) {
           vm = max(vm, oid<RL>(a, v) + 1u);
-          if (a.world == 1 && bit_of(a.bigm, v)) {
-            fe += enlist(a, v, bc, &sl->nchunk, sh);
-          } else {
-            fe += __ldg(a.poff + v + 1) - __ldg(a.poff + v);
-          }
+          fe += __ldg(a.poff + v + 1) - __ldg(a.poff + v);
         }
       }
     }
   }
-  const unsigned long long bigdeg = big_flush(a, sh, bc, sl, true);
-  fe = block_sum(fe, sh) + bigdeg;
+  // chunks of F's big vertices for the first push step (single device;
+  // sharded push steps re-chunk their rows every step)
+  if (a.world == 1) chunk_words(a, a.F, bc, &sl->nchunk, sh);
+  fe = block_sum(fe, sh);
   vm = ~block_min(~vm, sh);
   if (threadIdx.x == 0 && fe) atomicAdd(&sl->fedges, fe);
   if (threadIdx.x == 0 && vm) atomicMax(&a.ctl->it_vmax[t & 1u], vm);

@@ -24,7 +24,8 @@ g = C.c_void_p()
 _abi.check(L.cyc_graph_build(ctx.handle, C.cast(de, C.POINTER(C.c_uint32)), p.m, p.n,
                              C.cast(da, C.POINTER(C.c_uint64)), 1, C.byref(g)))
 L.cyc_device_free(ctx.handle, de)
-opt = eng.MapOptions(early_exit=early, mode=mode, trace_cap=int(os.environ.get("TRACE", "0"))).to_c()
+opt = eng.MapOptions(early_exit=early, mode=mode, trace_cap=int(os.environ.get("TRACE", "0"))).to_c(
+    0, int(os.environ.get("MAXSTEPS", "0")))
 for r in range(reps):
     st = _abi.MapStatsC()
     _abi.check(L.cyc_flush_l2(ctx.handle, 512 << 20))
