@@ -1106,6 +1106,63 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk
         }
       if (mw) fp[mi] = 0u;
     }
+    uint32_t cnt[kBatch], pre[kBatch + 1];
+    pre[0] = 0;
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      cnt[r] = __popc(wd[r]);
+      pre[r + 1] = pre[r] + cnt[r];
+    }
+    if (pre[kBatch] <= 32u) {
+      // sparse group (small frontiers, config 3's F): its vertices compacted
+      // one per lane, their edges flattened over the warp 32 at a time, so a
+      // vertex of degree d costs ceil(d/32) rounds, not d (a lane walking its
+      // own vertex's edges one round trip each)
+      uint32_t vx = kNone;
+#pragma unroll
+      for (int r = 0; r < kBatch; ++r)
+        if (lane >= pre[r] && lane < pre[r + 1]) vx = wi[r] * 32u + __fns(wd[r], 0u, (int)(lane - pre[r] + 1u));
+      const bool on = vx != kNone;
+      const uint32_t xv = on ? __ldca(c.Pc + vx) : 0u;
+      const uint32_t bw1 = on ? __ldcg(a.bigm + (vx >> 5)) : 0u;
+      const uint32_t b1 = on ? __ldg(a.poff + vx) : 0u;
+      uint32_t e1 = on ? __ldg(a.poff + vx + 1) : 0u;
+      uint32_t val1 = 0u;
+      if (on) {
+        atomicMax(c.Pn + vx, xv);  // bring x_{k-2} up to x_{k-1}
+        val1 = cand_of<RL>(a, xv, vx);
+        if ((bw1 >> (vx & 31u)) & 1u) e1 = b1;  // big: chunks push its edges
+      }
+      const uint32_t d1 = e1 - b1;
+      if (__reduce_max_sync(kFull, d1) <= (uint32_t)kBatch) {  // low degrees (chains): each lane its own edges
+        uint32_t t[kBatch], tv[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+          t[k] = (uint32_t)k < d1 ? __ldg(a.pcol + b1 + k) : kNone;
+          tv[k] = val1;
+        }
+        raise_batch<RL>(a, c, t, tv, acc);
+        continue;
+      }
+      const uint32_t incl = warp_incl_scan(d1), excl = incl - d1;
+      const uint32_t T = __shfl_sync(kFull, incl, 31);
+      for (uint32_t e0 = 0; e0 < T; e0 += 32u * kBatch) {
+        uint32_t t[kBatch], tv[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+          const uint32_t idx = e0 + 32u * k + lane;
+          uint32_t l = 0;  // owner: the last lane whose edges start at or before idx
+#pragma unroll
+          for (uint32_t st = 16; st > 0; st >>= 1)
+            if (__shfl_sync(kFull, excl, l + st) <= idx) l += st;
+          const uint32_t lb = __shfl_sync(kFull, b1, l), lx = __shfl_sync(kFull, excl, l);
+          tv[k] = __shfl_sync(kFull, val1, l);
+          t[k] = idx < T ? __ldg(a.pcol + lb + (idx - lx)) : kNone;
+        }
+        raise_batch<RL>(a, c, t, tv, acc);
+      }
+      continue;
+    }
     uint32_t v[kBatch], b[kBatch], e[kBatch], val[kBatch], xu[kBatch], bwv[kBatch];
     // every load of the four vertices first, in one round trip: an atomic on
     // Pn between them would serialise the batch (Pn may alias Pc for the
