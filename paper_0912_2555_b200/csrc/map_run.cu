@@ -1084,17 +1084,54 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk
   // each word; each word is cleared by the warp that consumes it.
   // sharded: the word lists only know this rank's raises; scan the replicated bitmap
   const bool scan = a.world > 1 || wl_over != 0u;
-  const uint32_t groups = scan ? (a.nwords + 3u) / 4u : (wlc + 3u) / 4u;
-  for (uint32_t it = gw; it < groups; it += nw) {
-    uint32_t wi[kBatch], wd[kBatch];
-#pragma unroll
-    for (int r = 0; r < kBatch; ++r) {
-      const uint32_t e = it * 4u + r;
-      wi[r] = scan ? (e < a.nwords ? e : kNone) : (e < wlc ? __ldcg(wlp + e) : kNone);
+  // one group = four frontier words (lane i owns bit i of each)
+  // up to 32 frontier vertices, one per lane (vx, kNone for none): their
+  // loads in one round trip, their edges flattened over the warp 32 at a
+  // time, so a vertex of degree d costs ceil(d/32) rounds, not d (a lane
+  // walking its own vertex's edges one round trip each)
+  auto sparse = [&](const uint32_t vx) {
+    const bool on = vx != kNone;
+    const uint32_t xv = on ? __ldca(c.Pc + vx) : 0u;
+    const uint32_t bw1 = on ? __ldcg(a.bigm + (vx >> 5)) : 0u;
+    const uint32_t b1 = on ? __ldg(a.poff + vx) : 0u;
+    uint32_t e1 = on ? __ldg(a.poff + vx + 1) : 0u;
+    uint32_t val1 = 0u;
+    if (on) {
+      atomicMax(c.Pn + vx, xv);  // bring x_{k-2} up to x_{k-1}
+      val1 = cand_of<RL>(a, xv, vx);
+      if ((bw1 >> (vx & 31u)) & 1u) e1 = b1;  // big: chunks push its edges
     }
+    const uint32_t d1 = e1 - b1;
+    if (__reduce_max_sync(kFull, d1) <= (uint32_t)kBatch) {  // low degrees (chains): each lane its own edges
+      uint32_t t[kBatch], tv[kBatch];
 #pragma unroll
-    for (int r = 0; r < kBatch; ++r) wd[r] = wi[r] != kNone ? __ldcg(fp + wi[r]) : 0u;
-    if (!(wd[0] | wd[1] | wd[2] | wd[3])) continue;
+      for (int k = 0; k < kBatch; ++k) {
+        t[k] = (uint32_t)k < d1 ? __ldg(a.pcol + b1 + k) : kNone;
+        tv[k] = val1;
+      }
+      raise_batch<RL>(a, c, t, tv, acc);
+      return;
+    }
+    const uint32_t incl = warp_incl_scan(d1), excl = incl - d1;
+    const uint32_t T = __shfl_sync(kFull, incl, 31);
+    for (uint32_t e0 = 0; e0 < T; e0 += 32u * kBatch) {
+      uint32_t t[kBatch], tv[kBatch];
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        const uint32_t idx = e0 + 32u * k + lane;
+        uint32_t l = 0;  // owner: the last lane whose edges start at or before idx
+#pragma unroll
+        for (uint32_t st = 16; st > 0; st >>= 1)
+          if (__shfl_sync(kFull, excl, l + st) <= idx) l += st;
+        const uint32_t lb = __shfl_sync(kFull, b1, l), lx = __shfl_sync(kFull, excl, l);
+        tv[k] = __shfl_sync(kFull, val1, l);
+        t[k] = idx < T ? __ldg(a.pcol + lb + (idx - lx)) : kNone;
+      }
+      raise_batch<RL>(a, c, t, tv, acc);
+    }
+  };
+  auto group = [&](const uint32_t (&wi)[kBatch], const uint32_t (&wd)[kBatch]) {
+    if (!(wd[0] | wd[1] | wd[2] | wd[3])) return;
     __syncwarp();
     {
       uint32_t mw = 0, mi = kNone;  // lane r < 4 clears word r (select chain, no local memory)
@@ -1113,55 +1150,13 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk
       cnt[r] = __popc(wd[r]);
       pre[r + 1] = pre[r] + cnt[r];
     }
-    if (pre[kBatch] <= 32u) {
-      // sparse group (small frontiers, config 3's F): its vertices compacted
-      // one per lane, their edges flattened over the warp 32 at a time, so a
-      // vertex of degree d costs ceil(d/32) rounds, not d (a lane walking its
-      // own vertex's edges one round trip each)
+    if (pre[kBatch] <= 32u) {  // sparse group: its vertices compacted one per lane
       uint32_t vx = kNone;
 #pragma unroll
       for (int r = 0; r < kBatch; ++r)
         if (lane >= pre[r] && lane < pre[r + 1]) vx = wi[r] * 32u + __fns(wd[r], 0u, (int)(lane - pre[r] + 1u));
-      const bool on = vx != kNone;
-      const uint32_t xv = on ? __ldca(c.Pc + vx) : 0u;
-      const uint32_t bw1 = on ? __ldcg(a.bigm + (vx >> 5)) : 0u;
-      const uint32_t b1 = on ? __ldg(a.poff + vx) : 0u;
-      uint32_t e1 = on ? __ldg(a.poff + vx + 1) : 0u;
-      uint32_t val1 = 0u;
-      if (on) {
-        atomicMax(c.Pn + vx, xv);  // bring x_{k-2} up to x_{k-1}
-        val1 = cand_of<RL>(a, xv, vx);
-        if ((bw1 >> (vx & 31u)) & 1u) e1 = b1;  // big: chunks push its edges
-      }
-      const uint32_t d1 = e1 - b1;
-      if (__reduce_max_sync(kFull, d1) <= (uint32_t)kBatch) {  // low degrees (chains): each lane its own edges
-        uint32_t t[kBatch], tv[kBatch];
-#pragma unroll
-        for (int k = 0; k < kBatch; ++k) {
-          t[k] = (uint32_t)k < d1 ? __ldg(a.pcol + b1 + k) : kNone;
-          tv[k] = val1;
-        }
-        raise_batch<RL>(a, c, t, tv, acc);
-        continue;
-      }
-      const uint32_t incl = warp_incl_scan(d1), excl = incl - d1;
-      const uint32_t T = __shfl_sync(kFull, incl, 31);
-      for (uint32_t e0 = 0; e0 < T; e0 += 32u * kBatch) {
-        uint32_t t[kBatch], tv[kBatch];
-#pragma unroll
-        for (int k = 0; k < kBatch; ++k) {
-          const uint32_t idx = e0 + 32u * k + lane;
-          uint32_t l = 0;  // owner: the last lane whose edges start at or before idx
-#pragma unroll
-          for (uint32_t st = 16; st > 0; st >>= 1)
-            if (__shfl_sync(kFull, excl, l + st) <= idx) l += st;
-          const uint32_t lb = __shfl_sync(kFull, b1, l), lx = __shfl_sync(kFull, excl, l);
-          tv[k] = __shfl_sync(kFull, val1, l);
-          t[k] = idx < T ? __ldg(a.pcol + lb + (idx - lx)) : kNone;
-        }
-        raise_batch<RL>(a, c, t, tv, acc);
-      }
-      continue;
+      sparse(vx);
+      return;
     }
     uint32_t v[kBatch], b[kBatch], e[kBatch], val[kBatch], xu[kBatch], bwv[kBatch];
     // every load of the four vertices first, in one round trip: an atomic on
@@ -1196,6 +1191,51 @@ __device__ void push_step(const RunArgs& a, uint32_t g, int cur, uint32_t nchunk
       if (!any) break;
       raise_batch<RL>(a, c, t, val, acc);
     }
+  };
+  // 32 frontier words, one per lane (myw = 0: none). Sparse windows (<= 64
+  // vertices, small frontiers) are compacted 32 vertices per round; dense ones
+  // go four words at a time, four vertices per lane.
+  auto window = [&](const uint32_t myi, const uint32_t myw) {
+    const uint32_t cw = __popc(myw), incl = warp_incl_scan(cw), excl = incl - cw;
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (total == 0u) return;
+    if (total <= 64u) {
+      if (myw) fp[myi] = 0u;
+      for (uint32_t c0 = 0; c0 < total; c0 += 32u) {
+        const uint32_t i = c0 + lane;
+        uint32_t l = 0;  // the lane whose word holds vertex i
+#pragma unroll
+        for (uint32_t st = 16; st > 0; st >>= 1)
+          if (__shfl_sync(kFull, excl, l + st) <= i) l += st;
+        const uint32_t w = __shfl_sync(kFull, myw, l), wi = __shfl_sync(kFull, myi, l);
+        const uint32_t k = i - __shfl_sync(kFull, excl, l);
+        sparse(i < total ? wi * 32u + __fns(w, 0u, (int)(k + 1u)) : kNone);
+      }
+      return;
+    }
+    for (uint32_t live = __ballot_sync(kFull, myw != 0u); live;) {
+      uint32_t wi[kBatch], wd[kBatch];
+#pragma unroll
+      for (int r = 0; r < kBatch; ++r) {
+        const uint32_t l = live ? __ffs(live) - 1u : 0u;
+        const uint32_t xi = __shfl_sync(kFull, myi, l), xw = __shfl_sync(kFull, myw, l);
+        wi[r] = live ? xi : kNone;
+        wd[r] = live ? xw : 0u;
+        live &= live - 1u;
+      }
+      group(wi, wd);
+    }
+  };
+  // windows: 32 consecutive words of the bitmap, or 4 entries of the list
+  // (list entries are few or come in contiguous waves of dense words: spread
+  // them over many warps; config 2 lost 14 % with 32-entry windows)
+  const uint32_t nwin = scan ? (a.nwords + 31u) / 32u : (wlc + 3u) / 4u;
+  for (uint32_t it = gw; it < nwin; it += nw) {
+    const uint32_t e = scan ? it * 32u + lane : it * 4u + lane;
+    const uint32_t myi = scan ? (e < a.nwords ? e : kNone)
+                              : (lane < 4u && e < wlc ? __ldcg(wlp + e) : kNone);
+    const uint32_t myw = myi != kNone ? __ldcg(fp + myi) : 0u;
+    window(myi, myw);
   }
   phase_mark(a, tk, 1);
   step_flags(a, acc, sl, sh, a.WL[g & 1u], a.wl_cap, a.BC[g & 1u]);
