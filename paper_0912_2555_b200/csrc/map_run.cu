@@ -64,6 +64,9 @@ constexpr int kModePull = 1, kModePush = 2;
 constexpr int kRows = 4;            // rows per lane in a pull step (the ovf test below assumes 4)
 static_assert(kRows == 4, "pull overflow test unrolled for 4 rows");
 constexpr int kBatch = 4;           // frontier vertices per lane in a push step
+#ifndef CYC_LIGHT_UNIT
+#define CYC_LIGHT_UNIT 16               // light slices per dynamic claim (pull_sell; 8-32 best on C3, 64+ leaves tails)
+#endif
 constexpr int kHeavyPerLane = kHeavyChunk / 32;  // pull heavy chunk edges per lane
 constexpr int kHeavyBatch = 4;                     // heavy chunks in flight per warp
 
@@ -633,50 +636,66 @@ __device__ __forceinline__ void pull_sell(const RunArgs& a, const uint32_t* __re
   const uint32_t nw = nwarps(a);
   static_assert((kRowPad / 32u) % R == 0, "slices per row padding must be a multiple of R");
   const uint32_t np = a.n_pad, nsl = (a.row_hi - a.row_lo) / 32u;  // this rank's slices
-  for (uint32_t s0 = gw * R; s0 < nsl; s0 += nw * R) {
-    const uint32_t base = a.row_lo + s0 * 32u;
-    uint4 d[R];
-    uint32_t own[R], best[R];
+  // Slices are claimed kLightUnit at a time from a per-step counter, the next
+  // claim in flight while the current unit runs: warps that finished their
+  // share of the heavy slab early take more light rows, so the step ends
+  // together (static shares left up to ~20 % of warp time at the barriers).
+  constexpr uint32_t kLightUnit = CYC_LIGHT_UNIT;
+  static_assert(kLightUnit % R == 0, "a unit holds whole slice groups");
+  (void)gw;
+  (void)nw;
+  uint32_t u0 = 0;
+  if (lane_id() == 0) u0 = atomicAdd(&sl->light_next, kLightUnit);
+  u0 = __shfl_sync(kFull, u0, 0);
+  while (u0 < nsl) {
+    uint32_t u1 = 0;  // the next claim, in flight meanwhile
+    if (lane_id() == 0) u1 = atomicAdd(&sl->light_next, kLightUnit);
+    for (uint32_t s0 = u0; s0 < min(u0 + kLightUnit, nsl); s0 += R) {
+      const uint32_t base = a.row_lo + s0 * 32u;
+      uint4 d[R];
+      uint32_t own[R], best[R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      d[k] = __ldg(a.sdesc + s0 + k);
-      own[k] = __ldca(P + base + 32u * k + lane);
-    }
-    uint32_t wmax = 0, skip = 0;
+      for (int k = 0; k < R; ++k) {
+        d[k] = __ldg(a.sdesc + s0 + k);
+        own[k] = __ldca(P + base + 32u * k + lane);
+      }
+      uint32_t wmax = 0, skip = 0;
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      best[k] = own[k] & kCode;
-      wmax = max(wmax, d[k].y);
-      skip |= ((d[k].z >> lane) & 1u) << k;
-    }
-    uint32_t wlim[R];  // a saturated row reads no columns at all
+      for (int k = 0; k < R; ++k) {
+        best[k] = own[k] & kCode;
+        wmax = max(wmax, d[k].y);
+        skip |= ((d[k].z >> lane) & 1u) << k;
+      }
+      uint32_t wlim[R];  // a saturated row reads no columns at all
 #pragma unroll
-    for (int k = 0; k < R; ++k) wlim[k] = best[k] == hot.vmax ? 0u : d[k].y;
-    for (uint32_t j = 0; j < wmax; j += J) {
-      uint32_t u[R][J], w[R][J];
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-#pragma unroll
-        for (int t = 0; t < J; ++t)
-          u[k][t] = j + t < wlim[k] ? ld_stream(a.sell + ((size_t)d[k].x + j + t) * 32u + lane) : np;
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-#pragma unroll
-        for (int t = 0; t < J; ++t) w[k][t] = ld_word(hot, P, u[k][t]);
-      if constexpr (RL) {
+      for (int k = 0; k < R; ++k) wlim[k] = best[k] == hot.vmax ? 0u : d[k].y;
+      for (uint32_t j = 0; j < wmax; j += J) {
+        uint32_t u[R][J], w[R][J];
 #pragma unroll
         for (int k = 0; k < R; ++k)
 #pragma unroll
           for (int t = 0; t < J; ++t)
-            if (w[k][t] & kFlag) u[k][t] = __ldg(a.orig + u[k][t]);
+            u[k][t] = j + t < wlim[k] ? ld_stream(a.sell + ((size_t)d[k].x + j + t) * 32u + lane) : np;
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int t = 0; t < J; ++t) w[k][t] = ld_word(hot, P, u[k][t]);
+        if constexpr (RL) {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+#pragma unroll
+            for (int t = 0; t < J; ++t)
+              if (w[k][t] & kFlag) u[k][t] = __ldg(a.orig + u[k][t]);
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int t = 0; t < J; ++t)
+            best[k] = max(best[k], max(w[k][t] & kCode, (w[k][t] >> 31) * (u[k][t] + 1u)));
       }
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-#pragma unroll
-        for (int t = 0; t < J; ++t)
-          best[k] = max(best[k], max(w[k][t] & kCode, (w[k][t] >> 31) * (u[k][t] + 1u)));
+      rows_epilogue<RL, R>(a, base, own, best, skip, Q, fb, sh, fp, bc, sl, acc);
     }
-    rows_epilogue<RL, R>(a, base, own, best, skip, Q, fb, sh, fp, bc, sl, acc);
+    u0 = __shfl_sync(kFull, u1, 0);
   }
 }
 
@@ -1373,6 +1392,7 @@ __device__ __forceinline__ void reset_slot(RunCtl* c, uint32_t s) {
   sl.wit = kNone;
   sl.wl_count = 0;
   sl.wl_over = 0;
+  sl.light_next = 0;
 }
 
 // ------------------------------------------------------- sharded exchange

@@ -21,6 +21,7 @@ struct alignas(64) SlotCtl {
   unsigned int wit;           // exact min self-witness (pull rows)
   unsigned int wl_count;      // frontier words listed for the next push step
   unsigned int wl_over;       // the list is incomplete: scan the bitmap instead
+  unsigned int light_next;    // pull steps on a plan: next unclaimed light slice (dynamic distribution)
 };
 constexpr unsigned int kChunkOver = 0x80000000u;
 
