@@ -64,6 +64,9 @@ constexpr int kModePull = 1, kModePush = 2;
 constexpr int kRows = 4;            // rows per lane in a pull step (the ovf test below assumes 4)
 static_assert(kRows == 4, "pull overflow test unrolled for 4 rows");
 constexpr int kBatch = 4;           // frontier vertices per lane in a push step
+#ifndef CYC_HEAVY_UNIT
+#define CYC_HEAVY_UNIT 64               // heavy-slab chunks per dynamic claim (pull_heavy_slab)
+#endif
 #ifndef CYC_LIGHT_UNIT
 #define CYC_LIGHT_UNIT 16               // light slices per dynamic claim (pull_sell; 8-32 best on C3, 64+ leaves tails)
 #endif
@@ -820,21 +823,29 @@ __device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t
   const uint32_t gw = gwarp(a);
   const uint32_t nw = nwarps(a);
   const uint32_t nh = a.n_hchunks, np = a.n_pad;
-  const uint32_t cb = (uint32_t)((uint64_t)gw * nh / nw), ce = (uint32_t)((uint64_t)(gw + 1u) * nh / nw);
-  if (cb >= ce) return;
+  // Chunks go in units of kHeavyUnit: unit gw first, then units claimed from
+  // a per-step counter (the next claim in flight while a unit runs), so the
+  // saturation skips' uneven savings do not leave warps idle at the barrier.
+  constexpr uint32_t kHeavyUnit = CYC_HEAVY_UNIT;
+  static_assert(kHeavyUnit % B == 0, "a unit holds whole rounds");
+  uint32_t ub = gw * kHeavyUnit;
+  if (ub >= nh) return;
+  uint32_t ue = min(ub + kHeavyUnit, nh);
+  uint32_t claim = 0;
+  if (lane == 0) claim = atomicAdd(&sl->heavy_next, kHeavyUnit);
   uint32_t u[B][H], rr[B], ro[B];
 #pragma unroll
   for (int k = 0; k < B; ++k) {
-    const bool ok = cb + k < ce;
-    rr[k] = ok ? ld_stream(a.hrow + cb + k) : kNone;
+    const bool ok = ub + k < ue;
+    rr[k] = ok ? ld_stream(a.hrow + ub + k) : kNone;
 #pragma unroll
-    for (int r = 0; r < H; ++r) u[k][r] = ok ? ld_stream(a.hcol + (size_t)(cb + k) * kHeavyChunk + 32u * r + lane) : np;
+    for (int r = 0; r < H; ++r) u[k][r] = ok ? ld_stream(a.hcol + (size_t)(ub + k) * kHeavyChunk + 32u * r + lane) : np;
   }
 #pragma unroll
   for (int k = 0; k < B; ++k) ro[k] = rr[k] != kNone ? __ldca(P + rr[k]) : 0u;
   uint32_t row = kNone, rmax = 0, rown = 0;       // the row this warp is on (uniform)
   uint32_t pv = 0, pm = 0, po = 0, npend = 0;     // finished rows awaiting write-back
-  for (uint32_t c = cb; c < ce; c += B) {
+  for (uint32_t c = ub; c < nh;) {
     uint32_t w[B][H];
     // saturated row (at step start, or its maximum so far in this warp's walk
     // already reached vmax): its chunk cannot raise it, gather nothing
@@ -848,14 +859,21 @@ __device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t
     for (int k = 0; k < B; ++k)
 #pragma unroll
       for (int r = 0; r < H; ++r) w[k][r] = ld_word(hot, P, u[k][r]);
+    uint32_t cn = c + B;  // the next round: on in this unit, or the claimed one
+    if (cn >= ue) {
+      ub = nw * kHeavyUnit + __shfl_sync(kFull, claim, 0);
+      ue = min(ub + kHeavyUnit, nh);
+      cn = ub;
+      if (lane == 0 && ub < nh) claim = atomicAdd(&sl->heavy_next, kHeavyUnit);
+    }
     uint32_t un[B][H], rn[B];
 #pragma unroll
     for (int k = 0; k < B; ++k) {
-      const bool ok = c + B + k < ce;
-      rn[k] = ok ? ld_stream(a.hrow + c + B + k) : kNone;
+      const bool ok = cn + k < ue;
+      rn[k] = ok ? ld_stream(a.hrow + cn + k) : kNone;
 #pragma unroll
       for (int r = 0; r < H; ++r)
-        un[k][r] = ok ? ld_stream(a.hcol + (size_t)(c + B + k) * kHeavyChunk + 32u * r + lane) : np;
+        un[k][r] = ok ? ld_stream(a.hcol + (size_t)(cn + k) * kHeavyChunk + 32u * r + lane) : np;
     }
     if constexpr (RL) {
 #pragma unroll
@@ -900,6 +918,7 @@ __device__ __forceinline__ void pull_heavy_slab(const RunArgs& a, const uint32_t
 #pragma unroll
       for (int r = 0; r < H; ++r) u[k][r] = un[k][r];
     }
+    c = cn;
   }
   if (row != kNone) {
     if (lane == npend) {
@@ -1393,6 +1412,7 @@ __device__ __forceinline__ void reset_slot(RunCtl* c, uint32_t s) {
   sl.wl_count = 0;
   sl.wl_over = 0;
   sl.light_next = 0;
+  sl.heavy_next = 0;
 }
 
 // ------------------------------------------------------- sharded exchange

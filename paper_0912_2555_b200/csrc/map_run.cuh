@@ -22,6 +22,7 @@ struct alignas(64) SlotCtl {
   unsigned int wl_count;      // frontier words listed for the next push step
   unsigned int wl_over;       // the list is incomplete: scan the bitmap instead
   unsigned int light_next;    // pull steps on a plan: next unclaimed light slice (dynamic distribution)
+  unsigned int heavy_next;    // ... and heavy-slab chunks claimed beyond every warp's first unit
 };
 constexpr unsigned int kChunkOver = 0x80000000u;
 
