@@ -528,7 +528,7 @@ __device__ __forceinline__ void rows_epilogue(const RunArgs& a, uint32_t base, c
                                               uint32_t* fb, BlockSh* sh, uint32_t* fp, uint4* bc, SlotCtl* sl,
                                               StepAcc& acc) {
   const uint32_t lane = lane_id();
-  uint32_t words[R];
+  uint32_t words[R], hvy[R];
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     const uint32_t v = base + 32u * k + lane;
@@ -539,20 +539,31 @@ __device__ __forceinline__ void rows_epilogue(const RunArgs& a, uint32_t base, c
       if (best[k] == id + 1u) atomicMin(&sl->wit, id);
     }
     words[k] = __ballot_sync(kFull, up);
+    hvy[k] = __ballot_sync(kFull, (skip >> k) & 1u);
     acc.raised += up;
     acc.first += up;
   }
   // next frontier words (the bitmap is zero at step start; heavy rows are
-  // disjoint): fire-and-forget ORs, previous frontier words consumed
+  // disjoint): fire-and-forget ORs, previous frontier words consumed. A word
+  // holding heavy rows may also be marked by their warps (mark(), which lists
+  // the word when it finds it zero): list it here only if this OR found it
+  // zero too, so the next push step's word list has no duplicates.
   if (lane < (uint32_t)R) {
-    uint32_t wd = 0;
+    uint32_t wd = 0, hw = 0;
 #pragma unroll
-    for (int k = 0; k < R; ++k) wd = lane == (uint32_t)k ? words[k] : wd;
+    for (int k = 0; k < R; ++k) {
+      wd = lane == (uint32_t)k ? words[k] : wd;
+      hw = lane == (uint32_t)k ? hvy[k] : hw;
+    }
     const uint32_t wi = (base >> 5) + lane;
     fp[wi] = 0u;
     if (wd) {
-      atomicOr(fb + wi, wd);
-      note_word(sh, wi);
+      if (!hw) {
+        atomicOr(fb + wi, wd);
+        note_word(sh, wi);
+      } else if (atomicOr(fb + wi, wd) == 0u) {
+        note_word(sh, wi);
+      }
     }
   }
   // raised vertices of big push degree: chunks for the next push step
