@@ -113,3 +113,39 @@ def test_layout_hot_staging_split(eng, R, hot, monkeypatch):
         for mode in ("auto", "pull"):
             assert_same_run(eng.run_map_detailed(s, acc, eng.MapOptions(early_exit=early, mode=mode,
                                                                         layout="degree")), ref)
+
+
+def test_auto_layout_builds_the_plan_from_the_second_loop(eng):
+    """Auto layout: a graph's first MAP loop runs in id order (the plan costs
+    more than one loop saves), the second builds and uses the degree-ordered
+    plan; both loops give the same run (R-MAT scale 24: a 64 MB map vector
+    whose hottest eighth takes most gathers, so auto picks the plan)."""
+    from paper_0912_2555_b200 import _abi
+    from test_gpu_parity import _device_snapshot
+
+    p = eng.preset(3)
+    p.scale = 24
+    eng.prepare(p)
+    ctx = eng.default_context()
+    L, C = _abi.lib(), _abi.C
+    de, da = C.c_void_p(), C.c_void_p()
+    _abi.check(L.cyc_device_alloc(ctx.handle, p.m * 8, C.byref(de)))
+    _abi.check(L.cyc_device_alloc(ctx.handle, ((p.n + 63) // 64) * 8, C.byref(da)))
+    try:
+        _abi.check(L.cyc_gen_fill(ctx.handle, C.byref(p), de, da))
+        s = _device_snapshot(eng, p, ctx, de, da, eng.Orientation.transposed)
+        opt = eng.MapOptions(early_exit=False)
+        runs = [eng.run_map_detailed(s, s.accepting, opt, hash_cap=64) for _ in range(3)]
+        assert [int(r.stats.device["layout"]) for r in runs] == [_abi.CYC_LAYOUT_IDENTITY, _abi.CYC_LAYOUT_DEGREE,
+                                                        _abi.CYC_LAYOUT_DEGREE]
+        pm = [r.stats.device["plan_ms"] for r in runs]
+        assert pm[0] < 1.0 and pm[1] > 1.0 and pm[2] == 0.0  # first: only the decision; second: the plan; third: cached
+        for r in runs[1:]:
+            assert (r.verdict.cycle_found(), r.verdict.witness, r.stats.kernel_calls, r.stats.iterations) == (
+                runs[0].verdict.cycle_found(), runs[0].verdict.witness, runs[0].stats.kernel_calls,
+                runs[0].stats.iterations)
+            assert np.array_equal(r.final_values, runs[0].final_values)
+            assert np.array_equal(r.iter_hash, runs[0].iter_hash)
+    finally:
+        L.cyc_device_free(ctx.handle, de)
+        L.cyc_device_free(ctx.handle, da)
