@@ -1386,18 +1386,27 @@ __device__ void reset_pass(const RunArgs& a, uint32_t g, uint64_t t, BlockSh* sh
       fz[wi] = 0u;
       if (f) note_word(sh, wi);
     }
-    for (uint32_t j = 0; j < 32u; ++j) {
-      const uint32_t fj = __shfl_sync(kFull, f, j);
-      const uint32_t v = (s * 32u + j) * 32u + lane;
-      if (v < a.n) {
-        const bool accv = (fj >> lane) & 1u;
-        const uint32_t val = accv ? kFlag : 0u;
-        a.P[0][v] = val;
-        a.P[1][v] = val;
-        if (accv) {
-          vm = max(vm, oid<RL>(a, v) + 1u);
-          fe += __ldg(a.poff + v + 1) - __ldg(a.poff + v);
+    // eight words per round: their degree / id loads in flight together
+    // (one load round trip per word serialised ~120 of them per warp)
+    for (uint32_t j0 = 0; j0 < 32u; j0 += 8u) {
+      uint32_t dv[8], iv[8];
+#pragma unroll
+      for (uint32_t q = 0; q < 8u; ++q) {
+        const uint32_t fj = __shfl_sync(kFull, f, j0 + q);
+        const uint32_t v = (s * 32u + j0 + q) * 32u + lane;
+        const bool accv = v < a.n && ((fj >> lane) & 1u);
+        if (v < a.n) {
+          const uint32_t val = accv ? kFlag : 0u;
+          a.P[0][v] = val;
+          a.P[1][v] = val;
         }
+        dv[q] = accv ? __ldg(a.poff + v + 1) - __ldg(a.poff + v) : 0u;
+        iv[q] = accv ? oid<RL>(a, v) + 1u : 0u;
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < 8u; ++q) {
+        fe += dv[q];
+        vm = max(vm, iv[q]);
       }
     }
   }
