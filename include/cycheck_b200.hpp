@@ -21,9 +21,12 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
+#include <cstdlib>
 #include <string>
 #include <thread>
 #include <utility>
@@ -126,34 +129,56 @@ class DeviceLog {
   DeviceLog(const Engine& e, const EdgeLogT& log, uint64_t lo, uint64_t hi) : e_(e), m_(hi - lo) {
     if (!m_) return;
     check(cyc_device_alloc(e.get(), m_ * 8, &dev_));
-    void* pin[2] = {nullptr, nullptr};
-    const uint64_t blk = std::min<uint64_t>(kStageEdges, m_);
-    for (auto& p : pin) check(cyc_host_alloc(blk * 8, &p));
-    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    auto fill = [&](uint32_t* dst, uint64_t b, uint64_t cnt) {  // edges [b, b+cnt) of the log
-      std::vector<std::thread> th;
-      const unsigned k = cnt < (1u << 16) ? 1u : nt;
-      for (unsigned t = 0; t < k; ++t)
-        th.emplace_back([&, t] {
-          const uint64_t s = cnt * t / k, f = cnt * (t + 1) / k;
-          for (uint64_t i = s; i < f; ++i) {
-            const auto pr = log.edge(b + i);
-            dst[2 * i] = pr.first;
-            dst[2 * i + 1] = pr.second;
-          }
-        });
-      for (auto& x : th) x.join();
+    uint64_t stage = kStageEdges;
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (const char* v = std::getenv("CYC_STAGE_LOG2")) stage = 1ull << std::atoi(v);  // tuning knobs
+    if (const char* v = std::getenv("CYC_STAGE_THREADS")) nt = (unsigned)std::max(1, std::atoi(v));
+    const uint64_t blk = std::min<uint64_t>(stage, m_);
+    const uint64_t nb = (m_ + blk - 1) / blk;
+    if (nb == 1 || m_ < (1u << 16)) nt = 1;
+    uint32_t* pin[2];
+    std::unique_lock<std::mutex> lk(staging(blk * 8, pin));  // one upload at a time owns the blocks
+    // Workers live for the whole upload: worker t fills slice t of every block
+    // (block i into pin[i & 1] once the copy of block i-2 has finished) while
+    // this thread issues block i's copy as soon as all slices are in. Spawning
+    // the workers per 32 MB block cost ~100 ms on a 2^30-edge log.
+    std::unique_ptr<std::atomic<unsigned>[]> filled(new std::atomic<unsigned>[nb]);
+    for (uint64_t i = 0; i < nb; ++i) filled[i].store(0, std::memory_order_relaxed);
+    std::atomic<uint64_t> free_upto{1};  // blocks <= this may be filled
+    std::atomic<bool> abort{false};
+    auto work = [&](unsigned t) {
+      for (uint64_t i = 0; i < nb; ++i) {
+        while (free_upto.load(std::memory_order_acquire) < i) {
+          if (abort.load(std::memory_order_relaxed)) return;
+          std::this_thread::yield();
+        }
+        const uint64_t b = i * blk, cnt = std::min(blk, m_ - b);
+        const uint64_t s = cnt * t / nt, f = cnt * (t + 1) / nt;
+        uint32_t* dst = pin[i & 1];
+        for (uint64_t j = s; j < f; ++j) {
+          const auto pr = log.edge(lo + b + j);
+          dst[2 * j] = pr.first;
+          dst[2 * j + 1] = pr.second;
+        }
+        filled[i].fetch_add(1, std::memory_order_release);
+      }
     };
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) th.emplace_back(work, t);
     cyc_status st = CYC_OK;
-    int cur = 0;
-    for (uint64_t off = 0; off < m_ && st == CYC_OK; off += blk, cur ^= 1) {
-      const uint64_t cnt = std::min(blk, m_ - off);
-      fill(static_cast<uint32_t*>(pin[cur]), lo + off, cnt);  // overlaps the previous block's copy
-      st = cyc_ctx_synchronize(e.get());                       // that copy is done: its buffer is free
-      if (st == CYC_OK) st = cyc_memcpy_async(e.get(), static_cast<char*>(dev_) + off * 8, pin[cur], cnt * 8);
+    for (uint64_t i = 0; i < nb && st == CYC_OK; ++i) {
+      while (filled[i].load(std::memory_order_acquire) < nt) std::this_thread::yield();
+      if (i >= 1) {
+        st = cyc_ctx_synchronize(e.get());  // block i-1's copy is done: its buffer may take block i+1
+        free_upto.store(i + 1, std::memory_order_release);
+      }
+      const uint64_t b = i * blk, cnt = std::min(blk, m_ - b);
+      if (st == CYC_OK) st = cyc_memcpy_async(e.get(), static_cast<char*>(dev_) + b * 8, pin[i & 1], cnt * 8);
     }
     if (st == CYC_OK) st = cyc_ctx_synchronize(e.get());
-    for (auto& p : pin) cyc_host_free(p);
+    abort.store(true);
+    free_upto.store(nb);
+    for (auto& x : th) x.join();
     check(st);
   }
   ~DeviceLog() {
@@ -165,6 +190,25 @@ class DeviceLog {
   uint64_t size() const { return m_; }
 
  private:
+  // Two pinned staging blocks kept for the process (pinning 2 x 32 MB per
+  // upload cost milliseconds every snapshot); one upload at a time uses them.
+  static std::unique_lock<std::mutex> staging(uint64_t bytes, uint32_t* (&pin)[2]) {
+    static std::mutex mu;
+    static void* buf[2] = {nullptr, nullptr};
+    static uint64_t cap = 0;
+    std::unique_lock<std::mutex> lk(mu);
+    if (cap < bytes) {
+      for (auto& p : buf) {
+        if (p) cyc_host_free(p);
+        p = nullptr;
+      }
+      for (auto& p : buf) check(cyc_host_alloc(bytes, &p));
+      cap = bytes;
+    }
+    pin[0] = static_cast<uint32_t*>(buf[0]);
+    pin[1] = static_cast<uint32_t*>(buf[1]);
+    return lk;
+  }
   Engine e_;
   uint64_t m_ = 0;
   void* dev_ = nullptr;

@@ -53,6 +53,29 @@ static int time_dropin(int scale) {
     static_cast<uint32_t*>(pin)[2 * i + 1] = e.second;
   }
   const Bitset acc = log.accepting_prefix(p.n);
+  // DROPIN_VARIANTS="log2:threads,...": DeviceLog staging block / fill threads sweep
+  if (const char* vs = std::getenv("DROPIN_VARIANTS")) {
+    std::string all(vs);
+    size_t pos = 0;
+    while (pos < all.size()) {
+      size_t q = all.find(',', pos);
+      if (q == std::string::npos) q = all.size();
+      const std::string item = all.substr(pos, q - pos);
+      pos = q + 1;
+      const size_t c = item.find(':');
+      setenv("CYC_STAGE_LOG2", item.substr(0, c).c_str(), 1);
+      setenv("CYC_STAGE_THREADS", item.substr(c + 1).c_str(), 1);
+      double best = 1e30;
+      for (int rep = 0; rep < 3; ++rep) {
+        auto tb = clk::now();
+        b200::DeviceLog dl(gpu, log, 0, p.m);
+        best = std::min(best, ms(tb));
+      }
+      std::printf("{\"variant\": \"%s\", \"device_log_ms\": %.2f}\n", item.c_str(), best);
+    }
+    unsetenv("CYC_STAGE_LOG2");
+    unsetenv("CYC_STAGE_THREADS");
+  }
   double best_drop = 1e30, best_pin = 1e30, csr_ms = 0, kernel_ms = 0;
   bool same = true;
   for (int rep = 0; rep < 3; ++rep) {
