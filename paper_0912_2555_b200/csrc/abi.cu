@@ -582,8 +582,10 @@ cyc_status cyc_ctx_reserve(cyc_ctx* ctx, uint64_t m_log, uint32_t n, int backgro
           a->get<uint8_t>(a->ucnt, nn * 4, s);
           a->get<uint8_t>(a->lists, nn * 12, s);
         }
-        // staged log, snapshot / gather / plan columns and offsets
-        const size_t sizes[] = {m_log * 8, m_log * 4, m_log * 4, m_log * 4, m_log * 4, nn * 4, nn * 4, nn * 4, nn * 4};
+        // staged log, snapshot / gather columns, the plan's two relabelled
+        // column arrays and heavy slab (built on a graph's second loop), offsets
+        const size_t sizes[] = {m_log * 8, m_log * 4, m_log * 4, m_log * 4, m_log * 4, m_log * 4,
+                                nn * 4,    nn * 4,    nn * 4,    nn * 4,    nn * 4,    nn * 4};
         std::vector<std::pair<void*, size_t>> got;
         for (size_t b : sizes) {
           if (b < cyc::kBigBlock) continue;
