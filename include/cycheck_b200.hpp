@@ -179,7 +179,11 @@ class DeviceLog {
     abort.store(true);
     free_upto.store(nb);
     for (auto& x : th) x.join();
-    check(st);
+    if (st != CYC_OK) {  // the destructor will not run
+      cyc_device_free(e.get(), dev_);
+      dev_ = nullptr;
+      check(st);
+    }
   }
   ~DeviceLog() {
     if (dev_) cyc_device_free(e_.get(), dev_);
