@@ -435,8 +435,8 @@ def run_b200(args, rank, world, local):
                          "edges_touched": int(stats.edges_touched), "rows_touched": int(stats.rows_touched)},
         "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "ms": round(e2e_ms, 3),
                 "h2d_bytes_per_step": m_log * 8 + nw64 * 8, "d2h_bytes_per_step": C.sizeof(_abi.MapStatsC),
-                "what": "cyc_check from a pinned host edge log: H2D + both CSRs + storage plan + run_map "
-                        "(early_exit off) + stats D2H"},
+                "what": "cyc_check from a pinned host edge log: H2D + both CSRs + run_map (early_exit off; "
+                        "a one-shot call runs its loop in id order, auto layout) + stats D2H"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "k_map_run (persistent, one launch per run_map)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
