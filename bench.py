@@ -11,7 +11,7 @@ transposed snapshot, no restriction:
   (map_engine.cpp:94-121, 8 Jacobi steps on this graph). One bench step = one
   run_map; GTEPS = m x kernel_calls / device time of the loop kernel.
 * e2e: the same metric through the C ABI from a pinned HOST edge log
-  (cyc_check: H2D + both CSRs + storage plan + run_map + stats D2H).
+  (cyc_check: H2D + both CSRs + run_map in id order + stats D2H).
 * time_to_verdict_ms: early_exit on (the `cycheck graph` default), device-
   resident and from host memory, plus the first (cold) call of the process.
 
